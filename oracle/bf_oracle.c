@@ -1,0 +1,470 @@
+/*
+ * bf_oracle.c -- CPU reference ("oracle") for the BlueFog hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY (see bf_oracle.h).  Plain single-threaded fp64 C,
+ * each function written in the order of the paper passage it cites.
+ * Compiled with -O2 -ffp-contract=off (no fused multiply-add, no fast-math).
+ *
+ * Readings of the paper where it is silent or garbled are the numbered rows
+ * "R<k>" of DESIGN.md "Readings of the paper".
+ */
+#include "bf_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ========================================================================
+ * Topologies (global view).  P:334-339 "set_topology(graph_object)"; the
+ * built-ins are named at P:339 and P:447.
+ * ====================================================================== */
+
+/* Undirected ring, uniform weights over {i-1, i, i+1} (P:986 ring
+ * graph used for Exact-Diffusion).  n = 2 has a single neighbour: 1/2. */
+void ora_ring(int n, double *W) {
+    memset(W, 0, sizeof(double) * (size_t)n * n);
+    if (n == 1) { W[0] = 1.0; return; }
+    if (n == 2) { W[0] = W[1] = W[2] = W[3] = 0.5; return; }
+    for (int i = 0; i < n; ++i) {
+        W[i * n + i] = 1.0 / 3.0;
+        W[i * n + (i + 1) % n] = 1.0 / 3.0;
+        W[i * n + (i + n - 1) % n] = 1.0 / 3.0;
+    }
+}
+
+/* Static exponential-2 graph (P:446 cites [ying2021exponential]; reading R4):
+ * directed edges i -> i + 2^j (mod n), j = 0..floor(log2(n-1)); node i
+ * receives from i - 2^j; uniform weight 1/(deg+1) on self and in-edges. */
+void ora_exp2(int n, double *W) {
+    memset(W, 0, sizeof(double) * (size_t)n * n);
+    if (n == 1) { W[0] = 1.0; return; }
+    int deg = 0;
+    for (int off = 1; off <= n - 1; off *= 2) ++deg;
+    double w = 1.0 / (deg + 1);
+    for (int i = 0; i < n; ++i) {
+        W[i * n + i] = w;
+        for (int off = 1; off <= n - 1; off *= 2)
+            W[i * n + ((i - off) % n + n) % n] += w;
+    }
+}
+
+/* Fully connected, uniform 1/n (default topology, reading R15). */
+void ora_full(int n, double *W) {
+    for (int i = 0; i < n * n; ++i) W[i] = 1.0 / n;
+}
+
+static int ceil_log2(int n) {
+    int t = 0;
+    while ((1 << t) < n) ++t;
+    return t;
+}
+
+/* One-peer dynamic exponential graph ("each process only picks one
+ * neighbor at each iteration"; reading R5): at round k, t = k mod ceil(log2 n),
+ * node i pulls from i - 2^t and pushes to i + 2^t, self 1/2, effective 1/2. */
+void ora_one_peer_exp2_peers(int n, long long k, int i, int *src, int *dst) {
+    int tau = ceil_log2(n);
+    if (tau == 0) { *src = -1; *dst = -1; return; }
+    int off = 1 << (int)(k % tau);
+    *src = ((i - off) % n + n) % n;
+    *dst = (i + off) % n;
+}
+
+void ora_one_peer_exp2(int n, long long k, double *W) {
+    memset(W, 0, sizeof(double) * (size_t)n * n);
+    if (n == 1) { W[0] = 1.0; return; }
+    for (int i = 0; i < n; ++i) {
+        int src, dst;
+        ora_one_peer_exp2_peers(n, k, i, &src, &dst);
+        W[i * n + i] = 0.5;
+        W[i * n + src] += 0.5;
+    }
+}
+
+/* ========================================================================
+ * Neighbour sets, Eq. 6-7: N(i) = {j : (j,i) in E},
+ * M(i) = {j : (i,j) in E}; E = {(j,i) : w_ij != 0}.
+ * ====================================================================== */
+int ora_in_neighbors(int n, const double *W, int i, int *out) {
+    int c = 0;
+    for (int j = 0; j < n; ++j)
+        if (j != i && W[i * n + j] != 0.0) out[c++] = j;
+    return c;
+}
+
+int ora_out_neighbors(int n, const double *W, int i, int *out) {
+    int c = 0;
+    for (int j = 0; j < n; ++j)
+        if (j != i && W[j * n + i] != 0.0) out[c++] = j;
+    return c;
+}
+
+/* Weight classes: pull = every row sums to 1, push = every
+ * column sums to 1, standard = both. */
+int ora_classify(int n, const double *W, double tol) {
+    int rows = 1, cols = 1;
+    for (int i = 0; i < n; ++i) {
+        double r = 0.0, c = 0.0;
+        for (int j = 0; j < n; ++j) { r += W[i * n + j]; c += W[j * n + i]; }
+        if (fabs(r - 1.0) > tol) rows = 0;
+        if (fabs(c - 1.0) > tol) cols = 0;
+    }
+    return rows | (cols << 1);
+}
+
+/* ========================================================================
+ * Local views -> W.  Eq. 9: x_i <- w_ii x_i + sum_j r_ij s_ij x_j,
+ * with the four argument configurations of the P:381 footnote:
+ *   pull (self+src): s = 1 unless the sender also declared i (reading R1);
+ *   push (self+dst): r = 1, the receiver learns its sources from senders;
+ *   push-pull: r*s, and every declaration must be matched.
+ * ====================================================================== */
+static int view_has_dst(const ora_view *v, int i, double *s_out) {
+    for (int q = 0; q < v->n_dst; ++q)
+        if (v->dst[q] == i) { if (s_out) *s_out = v->s[q]; return 1; }
+    return 0;
+}
+
+int ora_assemble(int n, const ora_view *views, int check, double *W) {
+    memset(W, 0, sizeof(double) * (size_t)n * n);
+    for (int i = 0; i < n; ++i) {
+        const ora_view *vi = &views[i];
+        W[i * n + i] = vi->self_weight;
+        if (vi->n_src >= 0) {
+            /* receiver declares its sources (pull or push-pull): r_ij times
+             * s_ij when the sender also declared i, else s = 1 (R1). */
+            for (int q = 0; q < vi->n_src; ++q) {
+                int j = vi->src[q];
+                double s = 1.0;
+                int declared = view_has_dst(&views[j], i, &s);
+                if (!declared) s = 1.0;
+                /* a sender that declares destinations but not i: i would wait
+                 * for a message that never comes */
+                if (check && views[j].n_dst >= 0 && !declared) return -(1 + i);
+                W[i * n + j] = vi->r[q] * s;
+            }
+            if (check) {
+                /* every sender that pushes to i must be a declared source */
+                for (int j = 0; j < n; ++j) {
+                    if (j == i || !view_has_dst(&views[j], i, NULL)) continue;
+                    int listed = 0;
+                    for (int q = 0; q < vi->n_src; ++q) listed |= (vi->src[q] == j);
+                    if (!listed) return -(1 + i);
+                }
+            }
+        } else {
+            /* push-only or isolated receiver: sources are the senders that
+             * declared i among their destinations, weight s (r = 1). */
+            for (int j = 0; j < n; ++j) {
+                double s;
+                if (j != i && view_has_dst(&views[j], i, &s)) W[i * n + j] = s;
+            }
+        }
+    }
+    return 0;
+}
+
+/* ========================================================================
+ * Partial averaging, Eq. 5:  x_i <- w_ii x_i + sum_{j in N(i)} w_ij x_j
+ * written as the plain product Y = W X.
+ * ====================================================================== */
+void ora_mix(int n, long long count, const double *W, const double *X, double *Y) {
+    for (int i = 0; i < n; ++i)
+        for (long long e = 0; e < count; ++e) {
+            double acc = 0.0;
+            for (int j = 0; j < n; ++j)
+                acc += W[i * n + j] * X[(long long)j * count + e];
+            Y[(long long)i * count + e] = acc;
+        }
+}
+
+/* ========================================================================
+ * Casts (reading R17: round-to-nearest-even).
+ * ====================================================================== */
+float ora_f32(double v) { return (float)v; }
+
+uint16_t ora_bf16_rne(float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    if ((u & 0x7FFFFFFFu) > 0x7F800000u) return (uint16_t)((u >> 16) | 0x40u); /* quiet NaN */
+    uint32_t lsb = (u >> 16) & 1u;
+    u += 0x7FFFu + lsb;
+    return (uint16_t)(u >> 16);
+}
+
+static double bf16_value(uint16_t h) {
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+/* ========================================================================
+ * ATC-DSGD step.  Eq. 4 local update, then Eq. 5 partial
+ * averaging of the adapted copies (ATC, Eq. 17, reading R6).
+ * ====================================================================== */
+void ora_atc(int n, long long count, const double *W, const double *X,
+             const double *G, double lr, int wire_bf16, double *Y) {
+    double *xh = (double *)malloc(sizeof(double) * (size_t)n * count);
+    double *wire = (double *)malloc(sizeof(double) * (size_t)n * count);
+    /* Eq. 4: x_i^{k+1/2} = x_i^k - gamma * g_i, held as fp32 (reading R18) */
+    for (long long q = 0; q < (long long)n * count; ++q) {
+        xh[q] = (double)ora_f32(X[q] - lr * G[q]);
+        wire[q] = wire_bf16 ? bf16_value(ora_bf16_rne((float)xh[q])) : xh[q];
+    }
+    /* Eq. 5: self term from the unrounded x^{k+1/2}, neighbours from the wire */
+    for (int i = 0; i < n; ++i)
+        for (long long e = 0; e < count; ++e) {
+            double acc = W[i * n + i] * xh[(long long)i * count + e];
+            for (int j = 0; j < n; ++j)
+                if (j != i) acc += W[i * n + j] * wire[(long long)j * count + e];
+            Y[(long long)i * count + e] = acc;
+        }
+    free(xh);
+    free(wire);
+}
+
+/* AWC, Eq. 16: x_i^k = sum_{j in N+(i)} w_ij x_j^{k-1} - gamma g_i. */
+void ora_awc(int n, long long count, const double *W, const double *X,
+             const double *G, double lr, double *Y) {
+    ora_mix(n, count, W, X, Y);
+    for (long long q = 0; q < (long long)n * count; ++q) Y[q] -= lr * G[q];
+}
+
+/* ========================================================================
+ * Hierarchical neighbour allreduce: (1) intra-machine average,
+ * (2) machine-level neighbour averaging with W_M, (3) every local node takes
+ * the machine result.  machine_rank = rank // local_size.
+ * Reading R12: stage (1) is an average (SUM / local_size).
+ * ====================================================================== */
+void ora_hier(int n_machines, int L, long long count, const double *WM,
+              const double *X, double *Y) {
+    double *avg = (double *)calloc((size_t)n_machines * count, sizeof(double));
+    for (int m = 0; m < n_machines; ++m)                     /* stage 1 */
+        for (long long e = 0; e < count; ++e) {
+            double s = 0.0;
+            for (int l = 0; l < L; ++l) s += X[(long long)(m * L + l) * count + e];
+            avg[(long long)m * count + e] = s / L;
+        }
+    for (int m = 0; m < n_machines; ++m)                     /* stage 2 + 3 */
+        for (long long e = 0; e < count; ++e) {
+            double z = 0.0;
+            for (int q = 0; q < n_machines; ++q)
+                z += WM[m * n_machines + q] * avg[(long long)q * count + e];
+            for (int l = 0; l < L; ++l) Y[(long long)(m * L + l) * count + e] = z;
+        }
+    free(avg);
+}
+
+/* ========================================================================
+ * Window protocol event model (P:388-423 windows; P:551-585 async push-sum).
+ * One slot per static in-neighbour in ascending rank, each with two
+ * halves (reading R11).  Producer i -> consumer j: payload m lands in half
+ * m&1 when the consumer has consumed payload m-2 (consumed >= version-1);
+ * otherwise it stays in i's outbox (sender-side accumulation, no remote
+ * read-modify-write).  Collect sums the ready payloads and releases them
+ * (P:585 sum-and-reset, reading R9).  self_weight scales x in place (R8).
+ * ====================================================================== */
+struct ora_win {
+    int n;
+    long long count;
+    int *nin, *in;          /* in[i*n + q]: q-th in-neighbour of i */
+    int *nout, *out;        /* out[i*n + q] */
+    double *x;              /* n * count */
+    double *slot;           /* [dst][q][half][count] with q < n */
+    long long *version, *consumed;  /* [dst*n + q] */
+    double *outbox;         /* [src][q][count], q indexes out[src] */
+    int *outbox_valid;      /* [src*n + q] */
+};
+
+static double *slot_ptr(const ora_win *w, int dst, int q, int half) {
+    return w->slot + (((size_t)dst * w->n + q) * 2 + half) * w->count;
+}
+
+ora_win *ora_win_create(int n, long long count, const double *Wstatic,
+                        const double *X0, int zero_init) {
+    ora_win *w = (ora_win *)calloc(1, sizeof(ora_win));
+    w->n = n;
+    w->count = count;
+    w->nin = (int *)calloc(n, sizeof(int));
+    w->in = (int *)calloc((size_t)n * n, sizeof(int));
+    w->nout = (int *)calloc(n, sizeof(int));
+    w->out = (int *)calloc((size_t)n * n, sizeof(int));
+    for (int i = 0; i < n; ++i) {
+        w->nin[i] = ora_in_neighbors(n, Wstatic, i, w->in + (size_t)i * n);
+        w->nout[i] = ora_out_neighbors(n, Wstatic, i, w->out + (size_t)i * n);
+    }
+    w->x = (double *)malloc(sizeof(double) * (size_t)n * count);
+    memcpy(w->x, X0, sizeof(double) * (size_t)n * count);
+    w->slot = (double *)calloc((size_t)n * n * 2 * count, sizeof(double));
+    w->version = (long long *)calloc((size_t)n * n, sizeof(long long));
+    w->consumed = (long long *)calloc((size_t)n * n, sizeof(long long));
+    w->outbox = (double *)calloc((size_t)n * n * count, sizeof(double));
+    w->outbox_valid = (int *)calloc((size_t)n * n, sizeof(int));
+    if (!zero_init) {
+        /* buffers start as a copy of the local tensor (reading R10); the copy
+         * sits in half 1, the "latest" half while version == 0. */
+        for (int i = 0; i < n; ++i)
+            for (int q = 0; q < w->nin[i]; ++q)
+                memcpy(slot_ptr(w, i, q, 1), w->x + (size_t)i * count, sizeof(double) * count);
+    }
+    return w;
+}
+
+void ora_win_free(ora_win *w) {
+    if (!w) return;
+    free(w->nin); free(w->in); free(w->nout); free(w->out); free(w->x);
+    free(w->slot); free(w->version); free(w->consumed); free(w->outbox);
+    free(w->outbox_valid); free(w);
+}
+
+static int in_index(const ora_win *w, int dst, int src) {
+    for (int q = 0; q < w->nin[dst]; ++q)
+        if (w->in[(size_t)dst * w->n + q] == src) return q;
+    return -1;
+}
+
+int ora_win_accumulate(ora_win *w, int i, double self_weight, const double *s,
+                       const int *dst_mask, int overwrite) {
+    long long C = w->count;
+    for (int q = 0; q < w->nout[i]; ++q) {
+        int j = w->out[(size_t)i * w->n + q];
+        if (!dst_mask[j]) continue;
+        int qi = in_index(w, j, i);
+        if (qi < 0) return -1;
+        double *ob = w->outbox + ((size_t)i * w->n + q) * C;
+        int *valid = &w->outbox_valid[(size_t)i * w->n + q];
+        /* payload = (outbox +) s_ji * x_i   (push-style scaling, Eq. 10) */
+        for (long long e = 0; e < C; ++e) {
+            double base = (!overwrite && *valid) ? ob[e] : 0.0;
+            ob[e] = base + s[j] * w->x[(size_t)i * C + e];
+        }
+        *valid = 1;
+        long long *ver = &w->version[(size_t)j * w->n + qi];
+        long long con = w->consumed[(size_t)j * w->n + qi];
+        if (con >= *ver - 1) {          /* half (version & 1) is free */
+            memcpy(slot_ptr(w, j, qi, (int)(*ver & 1)), ob, sizeof(double) * C);
+            *ver += 1;
+            *valid = 0;
+        }
+    }
+    for (long long e = 0; e < C; ++e) w->x[(size_t)i * C + e] *= self_weight;
+    return 0;
+}
+
+void ora_win_collect(ora_win *w, int i) {
+    long long C = w->count;
+    for (int q = 0; q < w->nin[i]; ++q) {
+        long long *con = &w->consumed[(size_t)i * w->n + q];
+        long long ver = w->version[(size_t)i * w->n + q];
+        while (*con < ver) {
+            const double *h = slot_ptr(w, i, q, (int)(*con & 1));
+            for (long long e = 0; e < C; ++e) w->x[(size_t)i * C + e] += h[e];
+            *con += 1;
+        }
+    }
+}
+
+void ora_win_update(ora_win *w, int i, double self_weight, const double *r, double *out) {
+    long long C = w->count;
+    for (long long e = 0; e < C; ++e) out[e] = self_weight * w->x[(size_t)i * C + e];
+    for (int q = 0; q < w->nin[i]; ++q) {
+        int j = w->in[(size_t)i * w->n + q];
+        long long ver = w->version[(size_t)i * w->n + q];
+        const double *h = slot_ptr(w, i, q, (int)((ver - 1) & 1));
+        for (long long e = 0; e < C; ++e) out[e] += r[j] * h[e];
+        w->consumed[(size_t)i * w->n + q] = ver;   /* reading R10 */
+    }
+}
+
+void ora_win_get_x(const ora_win *w, double *X) {
+    memcpy(X, w->x, sizeof(double) * (size_t)w->n * w->count);
+}
+
+double ora_win_mass(const ora_win *w, long long e) {
+    long long C = w->count;
+    double m = 0.0;
+    for (int i = 0; i < w->n; ++i) {
+        m += w->x[(size_t)i * C + e];
+        for (int q = 0; q < w->nout[i]; ++q)
+            if (w->outbox_valid[(size_t)i * w->n + q])
+                m += w->outbox[((size_t)i * w->n + q) * C + e];
+        for (int q = 0; q < w->nin[i]; ++q)
+            for (long long p = w->consumed[(size_t)i * w->n + q];
+                 p < w->version[(size_t)i * w->n + q]; ++p)
+                m += slot_ptr(w, i, q, (int)(p & 1))[e];
+    }
+    return m;
+}
+
+void ora_win_counters(const ora_win *w, int dst, int src, long long *version,
+                      long long *consumed) {
+    int q = in_index(w, dst, src);
+    *version = q < 0 ? -1 : w->version[(size_t)dst * w->n + q];
+    *consumed = q < 0 ? -1 : w->consumed[(size_t)dst * w->n + q];
+}
+
+/* ========================================================================
+ * Least squares (Eq. 12) and its local gradient (Eq. 13,
+ * P:440): g_i = A_i^T (A_i x - b_i).  x* solves the normal equations
+ * sum_i A_i^T A_i x = sum_i A_i^T b_i, here by plain conjugate gradients.
+ * ====================================================================== */
+void ora_lsq_grad(int m, int d, const double *A, const double *b, const double *x, double *g) {
+    double *res = (double *)malloc(sizeof(double) * m);
+    for (int r = 0; r < m; ++r) {
+        double acc = 0.0;
+        for (int c = 0; c < d; ++c) acc += A[(size_t)r * d + c] * x[c];
+        res[r] = acc - b[r];
+    }
+    for (int c = 0; c < d; ++c) g[c] = 0.0;
+    for (int r = 0; r < m; ++r)
+        for (int c = 0; c < d; ++c) g[c] += A[(size_t)r * d + c] * res[r];
+    free(res);
+}
+
+static void normal_matvec(int n, int m, int d, const double *A, const double *v, double *out) {
+    double *zero = (double *)calloc(m, sizeof(double));
+    double *gi = (double *)malloc(sizeof(double) * d);
+    for (int c = 0; c < d; ++c) out[c] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        ora_lsq_grad(m, d, A + (size_t)i * m * d, zero, v, gi);   /* A_i^T A_i v */
+        for (int c = 0; c < d; ++c) out[c] += gi[c];
+    }
+    free(zero);
+    free(gi);
+}
+
+int ora_lsq_solve(int n, int m, int d, const double *A, const double *b, double tol,
+                  int max_iter, double *x) {
+    double *rhs = (double *)calloc(d, sizeof(double));
+    double *r = (double *)malloc(sizeof(double) * d);
+    double *p = (double *)malloc(sizeof(double) * d);
+    double *Ap = (double *)malloc(sizeof(double) * d);
+    for (int i = 0; i < n; ++i)
+        for (int row = 0; row < m; ++row)
+            for (int c = 0; c < d; ++c)
+                rhs[c] += A[((size_t)i * m + row) * d + c] * b[(size_t)i * m + row];
+    for (int c = 0; c < d; ++c) x[c] = 0.0;
+    double rr = 0.0, rhs2 = 0.0;
+    for (int c = 0; c < d; ++c) { r[c] = rhs[c]; p[c] = r[c]; rr += r[c] * r[c]; }
+    rhs2 = rr;
+    int it = 0;
+    while (it < max_iter && sqrt(rr) > tol * sqrt(rhs2)) {
+        normal_matvec(n, m, d, A, p, Ap);
+        double pAp = 0.0;
+        for (int c = 0; c < d; ++c) pAp += p[c] * Ap[c];
+        double alpha = rr / pAp;
+        double rr_new = 0.0;
+        for (int c = 0; c < d; ++c) {
+            x[c] += alpha * p[c];
+            r[c] -= alpha * Ap[c];
+            rr_new += r[c] * r[c];
+        }
+        double beta = rr_new / rr;
+        for (int c = 0; c < d; ++c) p[c] = r[c] + beta * p[c];
+        rr = rr_new;
+        ++it;
+    }
+    free(rhs); free(r); free(p); free(Ap);
+    return it;
+}

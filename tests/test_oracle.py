@@ -1,0 +1,433 @@
+"""Pins for the CPU oracle (oracle/), checked against what the paper and the
+mathematics fix -- never against the CUDA path.  CPU only (-m "not gpu").
+
+Each test names the passage it pins (P:NNN = PAPER.md line, S:NNN = SPEC.md
+line used for worked scalar examples).
+"""
+import numpy as np
+import pytest
+
+import oracle as ora
+import synthetic
+from bfutil import golden
+
+
+def _edges_to_W(n, edges, one_indexed=False):
+    """Adjacency-weighted matrix with W[i][j] != 0 iff edge j -> i."""
+    W = np.eye(n)
+    for (a, b) in edges:
+        if one_indexed:
+            a, b = a - 1, b - 1
+        W[b, a] = 1.0
+    return W
+
+
+# ---------------------------------------------------------------- topology ---
+def test_neighbor_sets_fig2():
+    g = golden("fig2_neighbor_sets.json")
+    W = _edges_to_W(g["n"], g["edges_1indexed"], one_indexed=True)
+    node = g["node"] - 1
+    assert [j + 1 for j in ora.in_neighbors(W, node)] == g["in_neighbors"]
+    assert [j + 1 for j in ora.out_neighbors(W, node)] == g["out_neighbors"]
+    # reversing every edge swaps N and M (Eq. 6-7 definitions)
+    Wt = W.T.copy()
+    assert [j + 1 for j in ora.out_neighbors(Wt, node)] == g["in_neighbors"]
+
+
+def test_weight_classes():
+    # pull = rows sum to 1, push = columns, standard = both
+    assert ora.classify(np.eye(3)) == "standard"
+    assert ora.classify(np.full((4, 4), 0.25)) == "standard"
+    P = np.array([[0.5, 0.5, 0.0], [0.0, 0.2, 0.8], [0.3, 0.3, 0.4]])
+    assert ora.classify(P) == "pull"
+    assert ora.classify(P.T) == "push"
+    assert ora.classify(P * 2) == "none"
+
+
+def test_exp2_structure():
+    # P:446 static exponential graph (reading R4): node 0 of n=8 sends to {1,2,4}
+    W = ora.exp2(8)
+    assert ora.out_neighbors(W, 0) == [1, 2, 4]
+    assert ora.in_neighbors(W, 0) == [4, 6, 7]
+    assert np.allclose(W[W != 0], 0.25)
+    degs = [len(ora.in_neighbors(ora.exp2(n), 0)) for n in range(2, 9)]
+    assert degs == [1, 2, 2, 3, 3, 3, 3]
+    for n in range(2, 17):
+        assert ora.classify(ora.exp2(n)) == "standard"   # P:231 "special directed graphs such as the exponential graph"
+
+
+def test_exp2_circulant_spectrum():
+    # exp2(n) is circulant: eigenvalues are the DFT of its first column pattern
+    n = 8
+    W = ora.exp2(n)
+    c = W[0]                                       # W[i][j] = c[(j - i) mod n]
+    for i in range(n):
+        assert np.array_equal(W[i], np.roll(c, i))
+    omega = np.exp(2j * np.pi / n)
+    lam = np.array([sum(c[k] * omega ** (m * k) for k in range(n)) for m in range(n)])
+    ev = np.linalg.eigvals(W)
+    assert np.allclose(np.sort(np.abs(ev)), np.sort(np.abs(lam)), atol=1e-12)
+    assert abs(np.sort(np.abs(lam))[-2] - 0.5) < 1e-12
+
+
+def test_ring_structure():
+    W = ora.ring(5)
+    assert ora.in_neighbors(W, 0) == [1, 4]
+    assert np.allclose(W[W != 0], 1 / 3)
+    assert ora.classify(W) == "standard"
+    W2 = ora.ring(2)
+    assert np.allclose(W2, 0.5)
+
+
+def test_one_peer_schedule_and_exact_average():
+    # P:916 one-peer dynamic exponential graph; reading R5.  For n = 2^tau the
+    # product over t of (I + S^{2^t})/2 is J/n: exact average after tau rounds.
+    assert ora.one_peer_exp2_peers(8, 0, 0) == (7, 1)
+    assert ora.one_peer_exp2_peers(8, 1, 0) == (6, 2)
+    assert ora.one_peer_exp2_peers(8, 2, 0) == (4, 4)
+    assert ora.one_peer_exp2_peers(8, 3, 0) == (7, 1)
+    assert ora.one_peer_exp2_peers(2, 5, 1) == (0, 0)
+    for n in (2, 4, 8, 16):
+        tau = n.bit_length() - 1
+        X = synthetic.agents_x0(n, 257).astype(np.float64)
+        mean = X.sum(axis=0) / n                  # exact in fp64 for these dyadic inputs
+        for k in range(tau):
+            Wk = ora.one_peer_exp2(n, k)
+            assert ora.classify(Wk) == "standard"
+            X = ora.mix(Wk, X)
+        assert np.array_equal(X, np.broadcast_to(mean, X.shape))
+    # non power of two: defined but not exact (reading R20)
+    X = synthetic.agents_x0(6, 64).astype(np.float64)
+    Y = X
+    for k in range(3):
+        Y = ora.mix(ora.one_peer_exp2(6, k), Y)
+    assert np.abs(Y - X.mean(axis=0)).max() > 1e-3
+
+
+# ------------------------------------------------------------------- mixing ---
+def test_mix_identity_and_uniform():
+    g = golden("spec_scalar_examples.json")
+    X = synthetic.agents_x0(3, 100).astype(np.float64)
+    assert np.array_equal(ora.mix(np.eye(3), X), X)
+    Y = ora.mix(ora.full(4), np.array(g["full4_inputs"]).reshape(4, 1))
+    assert np.allclose(Y, g["full4_expected"], rtol=0, atol=1e-15)
+
+
+def test_mix_bruteforce_small():
+    rng = np.random.default_rng(0)
+    for n in (1, 2, 3, 5, 8):
+        W = rng.standard_normal((n, n))
+        X = rng.standard_normal((n, 7))
+        Y = ora.mix(W, X)
+        for i in range(n):
+            for e in range(7):
+                ref = sum(W[i, j] * X[j, e] for j in range(n))
+                assert abs(Y[i, e] - ref) <= 1e-14 * (1 + sum(abs(W[i, j] * X[j, e]) for j in range(n)))
+
+
+def test_mean_preservation_and_fixed_point():
+    # a doubly stochastic W preserves column sums; a row-stochastic
+    # (pull) W keeps constant vectors fixed (consensus is a fixed point).
+    X = synthetic.agents_x0(8, 333).astype(np.float64)
+    for W in (ora.exp2(8), ora.ring(8), ora.one_peer_exp2(8, 1)):
+        assert np.allclose(ora.mix(W, X).sum(axis=0), X.sum(axis=0), atol=1e-13)
+    P = np.array([[0.5, 0.5, 0.0], [0.0, 0.2, 0.8], [0.3, 0.3, 0.4]])
+    c = np.ones((3, 5)) * 0.75
+    assert np.allclose(ora.mix(P, c), c, atol=1e-15)
+
+
+def test_matrix_power_bruteforce():
+    for n in (2, 3, 4, 5, 8):
+        W = ora.exp2(n)
+        X = synthetic.agents_x0(n, 33).astype(np.float64)
+        Y = X
+        for _ in range(6):
+            Y = ora.mix(W, Y)
+        assert np.allclose(Y, np.linalg.matrix_power(W, 6) @ X, atol=1e-13)
+
+
+def test_ring4_consensus_closed_form_c1():
+    # C1: n=4 ring, 20 iterations.  Ring W is circulant with eigenvalues
+    # {1, 1/3, -1/3, 1/3}; X^20 = F^-1 diag(lambda^20) F X in closed form.
+    n, K = 4, 20
+    W = ora.ring(n)
+    X0 = synthetic.agents_x0(n, 4096).astype(np.float64)
+    X = X0
+    for _ in range(K):
+        X = ora.mix(W, X)
+    c = W[0]
+    omega = np.exp(2j * np.pi / n)
+    F = np.array([[omega ** (-m * i) for i in range(n)] for m in range(n)])
+    lam = np.array([sum(c[k] * omega ** (m * k) for k in range(n)) for m in range(n)])
+    assert np.allclose(sorted(lam.real), [-1 / 3, 1 / 3, 1 / 3, 1.0])
+    closed = (np.linalg.inv(F) @ np.diag(lam ** K) @ F @ X0).real
+    assert np.allclose(X, closed, atol=1e-12)
+    assert np.abs(X - X0.mean(axis=0)).max() < 2 * 3.0 ** -20 * np.abs(X0).max() * n
+
+
+# ---------------------------------------------------------- local views -> W ---
+def _views_from_W(W, style):
+    n = W.shape[0]
+    views = []
+    for i in range(n):
+        v = {"self_weight": W[i, i], "src_weights": None, "dst_weights": None}
+        srcs = [j for j in range(n) if j != i and W[i, j] != 0]
+        dsts = [j for j in range(n) if j != i and W[j, i] != 0]
+        if style == "pull":
+            v["src_weights"] = {j: W[i, j] for j in srcs}
+        elif style == "push":
+            v["dst_weights"] = {j: W[j, i] for j in dsts}
+        elif style == "pushpull":
+            v["src_weights"] = {j: 0.5 for j in srcs}
+            v["dst_weights"] = {j: 2.0 * W[j, i] for j in dsts}
+        views.append(v)
+    return views
+
+
+@pytest.mark.parametrize("style", ["pull", "push", "pushpull"])
+def test_assemble_push_pull_equivalence(style):
+    # Eq. 9-11: push (r=1, s=w), pull (r=w, s=1) and push-pull
+    # (r*s = w) all realise the same W.
+    g = golden("fig2_neighbor_sets.json")
+    rng = np.random.default_rng(3)
+    Wmask = _edges_to_W(g["n"], g["edges_1indexed"], one_indexed=True)
+    W = Wmask * rng.uniform(0.1, 1.0, Wmask.shape)
+    Wa = ora.assemble(_views_from_W(W, style))
+    assert np.allclose(Wa, W, atol=1e-15)
+
+
+def test_one_peer_views_match_schedule():
+    # one-peer exp2 in pull form (src {i-2^t: 1/2}) and push form (dst {i+2^t: 1/2})
+    n = 8
+    for k in range(5):
+        pull, push = [], []
+        for i in range(n):
+            s, d = ora.one_peer_exp2_peers(n, k, i)
+            pull.append({"self_weight": 0.5, "src_weights": {s: 0.5}, "dst_weights": None})
+            push.append({"self_weight": 0.5, "src_weights": None, "dst_weights": {d: 0.5}})
+        assert np.array_equal(ora.assemble(pull), ora.one_peer_exp2(n, k))
+        assert np.array_equal(ora.assemble(push), ora.one_peer_exp2(n, k))
+
+
+def test_topology_check_mismatch():
+    # "user fills in dst_weights in process i to push information to
+    # process j, but does not provide src_weights in process j ... hangs".
+    views = [{"self_weight": 0.5, "src_weights": None, "dst_weights": {1: 0.5}},
+             {"self_weight": 1.0, "src_weights": {}, "dst_weights": {}}]
+    with pytest.raises(ValueError):
+        ora.assemble(views, check=True)
+    W = ora.assemble(views, check=False)         # unchecked: receiver ignores the push
+    assert W[1, 0] == 0.0
+    # receiver lists a source that declares destinations but not the receiver
+    views = [{"self_weight": 1.0, "src_weights": None, "dst_weights": {}},
+             {"self_weight": 0.5, "src_weights": {0: 0.5}, "dst_weights": {}}]
+    with pytest.raises(ValueError):
+        ora.assemble(views, check=True)
+
+
+# ---------------------------------------------------------------------- ATC ---
+def test_atc_hand_example():
+    # Eq. 4-5: x_half = x - lr*g = [0.5, 3.5], uniform W -> 2.0 for both
+    W = np.full((2, 2), 0.5)
+    Y = ora.atc(W, np.array([[1.0], [3.0]]), np.array([[1.0], [-1.0]]), 0.5)
+    assert np.array_equal(Y, np.array([[2.0], [2.0]]))
+
+
+def test_atc_wire_cast_points():
+    # reading R18: self term from fp32 x_half, neighbour terms from the wire copy
+    W = np.full((2, 2), 0.5)
+    x = np.array([[1.0 + 2.0 ** -10], [0.0]])
+    Y = ora.atc(W, x, np.zeros_like(x), 0.0, wire_bf16=True)
+    assert Y[0, 0] == 0.5 + 2.0 ** -11            # own value unrounded
+    assert Y[1, 0] == 0.5                         # bf16(1 + 2^-10) = 1.0 (RNE)
+    Y32 = ora.atc(W, x, np.zeros_like(x), 0.0, wire_bf16=False)
+    assert Y32[1, 0] == 0.5 + 2.0 ** -11
+
+
+def test_atc_special_cases():
+    n, cnt = 8, 500
+    X = synthetic.agents_x0(n, cnt).astype(np.float64)
+    G = synthetic.agents_grad(n, cnt, 0).astype(np.float64)
+    W = ora.exp2(n)
+    # lr = 0 -> pure averaging (Eq. 5 with the gradient ignored); X is fp32 so exact
+    assert np.array_equal(ora.atc(W, X, G, 0.0), ora.mix(W, X))
+    # n = 1 -> plain SGD, x - lr*g rounded once to fp32
+    Y1 = ora.atc(np.eye(1), X[:1], G[:1], 0.1)
+    ref = (X[:1] - np.float64(np.float32(0.1)) * G[:1]).astype(np.float32).astype(np.float64)
+    assert np.array_equal(Y1, ref)
+    # AWC with lr = 0 is also pure averaging (Eq. 16)
+    assert np.array_equal(ora.awc(W, X, G, 0.0), ora.mix(W, X))
+
+
+def test_atc_centralized_gd_equivalence():
+    # S:532 / Eq. 13-14: identical data and iterates on every agent and a
+    # doubly stochastic W reduce DGD to centralised gradient descent.
+    n, m, d = 4, 30, 6
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((m, d)) / np.sqrt(m)
+    b = rng.standard_normal(m)
+    x = np.zeros(d)
+    X = np.zeros((n, d))
+    W = ora.ring(n)
+    lr = 0.2
+    for _ in range(25):
+        g = ora.lsq_grad(A, b, X[0])
+        assert np.allclose(g, A.T @ (A @ X[0] - b), atol=1e-13)
+        X = ora.atc(W, X, np.tile(g, (n, 1)), lr)
+        x = x - np.float32(lr) * (A.T @ (A @ x - b))
+    assert np.allclose(X, np.tile(x, (n, 1)), rtol=1e-5, atol=1e-6)
+
+
+def test_lsq_solve_matches_normal_equations():
+    n, m, d = 3, 40, 12
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((n, m, d)) / np.sqrt(m)
+    b = rng.standard_normal((n, m))
+    x, it = ora.lsq_solve(A, b)
+    ref, *_ = np.linalg.lstsq(A.reshape(n * m, d), b.reshape(n * m), rcond=None)
+    assert np.allclose(x, ref, atol=1e-10)
+
+
+# ------------------------------------------------------------- hierarchical ---
+def test_hier_spec_example():
+    g = golden("hier_2x2_example.json")
+    X = np.array(g["inputs"]).reshape(4, 1)
+    Y = ora.hier(np.array(g["machine_W"]), g["local_size"], X)
+    assert np.array_equal(Y.ravel(), np.array(g["expected"]))
+
+
+def test_hier_kronecker_and_degenerate():
+    # (W_M kron J_L/L) X; one machine -> plain intra-machine average
+    for nm, L in ((4, 2), (2, 4), (1, 8), (8, 1)):
+        WM = ora.exp2(nm)
+        X = synthetic.agents_x0(nm * L, 50).astype(np.float64)
+        K = np.kron(WM, np.full((L, L), 1.0 / L))
+        assert np.allclose(ora.hier(WM, L, X), K @ X, atol=1e-14)
+    X = synthetic.agents_x0(8, 20).astype(np.float64)
+    assert np.allclose(ora.hier(np.eye(1), 8, X), np.tile(X.mean(axis=0), (8, 1)), atol=1e-15)
+    # hierarchical != flat neighbor_allreduce
+    X = synthetic.agents_x0(8, 20).astype(np.float64)
+    assert not np.allclose(ora.hier(ora.exp2(4), 2, X), ora.mix(ora.exp2(8), X))
+
+
+# -------------------------------------------------------------------- casts ---
+def test_bf16_rne_matches_torch():
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(11)
+    vals = np.concatenate([
+        rng.standard_normal(2000).astype(np.float32),
+        synthetic.uniform(1, 2000),
+        # exact ties: low 16 bits 0x8000, both parities of the kept lsb
+        (np.array([0x3F808000, 0x3F818000, 0xBF808000, 0x40490000 | 0x8000], np.uint32)).view(np.float32),
+        np.array([0.0, -0.0, 1e-40, 3.4e38, np.inf, -np.inf], np.float32),
+    ])
+    ours = ora.bf16_rne(vals)
+    ref = torch.from_numpy(vals).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(ours, ref)
+
+
+def test_synthetic_generator_properties():
+    u = synthetic.uniform(1000, 100000)
+    assert u.dtype == np.float32 and u.min() >= -1.0 and u.max() < 1.0
+    assert abs(u.mean()) < 0.01
+    # exactly representable: multiples of 2^-23
+    assert np.array_equal(np.round(u.astype(np.float64) * 2 ** 23), u.astype(np.float64) * 2 ** 23)
+    # offset addressing is a pure counter
+    assert np.array_equal(synthetic.uniform(5, 10, offset=90), synthetic.uniform(5, 100)[90:])
+
+
+# ------------------------------------------------------------------ windows ---
+def test_window_scalar_examples():
+    g = golden("spec_scalar_examples.json")
+    W = np.array([[1.0, 1.0, 1.0], [1.0, 1.0, 0.0], [1.0, 0.0, 1.0]])   # 1 <- 0, 2 <- 0 ... 0 <- {1,2}
+    X0 = np.zeros((3, 1))
+    X0[0, 0] = g["collect_local"]
+    X0[1, 0] = g["collect_buffers"][0]
+    X0[2, 0] = g["collect_buffers"][1]
+    win = ora.Window(W, X0, zero_init=True)
+    win.put(1, 0.0, {0: 1.0})
+    win.put(2, 0.0, {0: 1.0})
+    win.collect(0)
+    assert win.x()[0, 0] == g["collect_expected"]
+    # additive contract: two accumulates before the collect
+    W2 = np.array([[1.0, 1.0], [1.0, 1.0]])
+    win = ora.Window(W2, np.array([[0.0], [1.0]]), zero_init=True)
+    win.accumulate(1, 1.0, {0: g["accumulate_twice"][0]})
+    win.accumulate(1, 1.0, {0: g["accumulate_twice"][1]})
+    win.collect(0)
+    assert win.x()[0, 0] == g["accumulate_expected"]
+    assert win.counters(0, 1) == (2, 2)
+
+
+def test_window_backpressure_to_outbox():
+    # a third accumulate before any collect cannot take a half: it waits in the
+    # sender's outbox and is delivered later without loss (P:585 invariant)
+    W2 = np.array([[1.0, 1.0], [1.0, 1.0]])
+    win = ora.Window(W2, np.array([[0.0], [1.0]]), zero_init=True)
+    m0 = win.mass(0)
+    for k in range(5):
+        win.accumulate(1, 1.0, {0: 1.0})      # s = 1 with self 1: each call adds 1 unit
+        assert win.mass(0) == m0 + (k + 1)
+    assert win.counters(0, 1) == (2, 0)
+    win.collect(0)
+    assert win.x()[0, 0] == 2.0
+    win.accumulate(1, 1.0, {0: 0.0})          # flushes the outbox (3 more units)
+    win.collect(0)
+    assert win.x()[0, 0] == 5.0
+
+
+def test_window_sync_pushsum_equals_mix():
+    # synchronous schedule (all accumulate, then all collect) = one product
+    # with the column-stochastic push matrix of Listing 3
+    gold = golden("fig2_neighbor_sets.json")
+    n = gold["n"]
+    Wst = _edges_to_W(n, gold["edges_1indexed"], one_indexed=True)
+    Wps = np.zeros((n, n))
+    for i in range(n):
+        outs = ora.out_neighbors(Wst, i)
+        w = 1.0 / (len(outs) + 1)
+        Wps[i, i] = w
+        for j in outs:
+            Wps[j, i] = w
+    assert ora.classify(Wps) in ("push", "standard")
+    X = np.concatenate([synthetic.agents_x0(n, 6).astype(np.float64), np.ones((n, 1))], axis=1)
+    win = ora.Window(Wst, X, zero_init=True)
+    ref = X
+    for _ in range(4):
+        for i in range(n):
+            outs = ora.out_neighbors(Wst, i)
+            w = 1.0 / (len(outs) + 1)
+            win.accumulate(i, w, {j: w for j in outs})
+        for i in range(n):
+            win.collect(i)
+        ref = ora.mix(Wps, ref)
+    assert np.allclose(win.x(), ref, atol=1e-14)
+
+
+def test_window_async_pushsum_invariants():
+    # P:551-557 push-sum with random delays + P:585 mass invariant: total mass
+    # (x + outboxes + unconsumed halves) is constant; y = x/p -> mean(x0).
+    gold = golden("fig2_neighbor_sets.json")
+    n = gold["n"]
+    Wst = _edges_to_W(n, gold["edges_1indexed"], one_indexed=True)
+    cnt = 4
+    X = np.concatenate([synthetic.agents_x0(n, cnt - 1).astype(np.float64), np.ones((n, 1))], axis=1)
+    target = X[:, :-1].mean(axis=0)
+    win = ora.Window(Wst, X, zero_init=True)
+    m0 = [win.mass(e) for e in range(cnt)]
+    rng = np.random.default_rng(2024)
+    for step in range(20000):
+        i = int(rng.integers(n))
+        if rng.random() < 0.5:
+            outs = ora.out_neighbors(Wst, i)
+            w = 1.0 / (len(outs) + 1)
+            win.accumulate(i, w, {j: w for j in outs})
+        else:
+            win.collect(i)
+        if step % 997 == 0:
+            for e in range(cnt):
+                assert abs(win.mass(e) - m0[e]) < 1e-12 * n
+    Xf = win.x()
+    y = Xf[:, :-1] / Xf[:, -1:]
+    assert np.abs(y - target).max() < 1e-9
+    assert abs(win.mass(cnt - 1) - n) < 1e-12

@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the BlueFog hot path on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[3], "C4"): one fused ATC-DSGD step
+(Eq. 4-5 + Eq. 17) of n = 8 agents, each holding a 25.6M-element fp32
+parameter vector (ResNet-50-sized), synthetic gradients, dynamic one-peer
+exponential-2 topology.  A "step" = one pass of the whole hot path:
+weight/schedule resolution, adapt, publish, neighbour exchange, weighted
+combine, store -- one kernel launch per step.
+
+  N = 1 : the 8 agents run as virtual agents on one GPU (HBM-bound)
+  N > 1 : 8/N agents per GPU, neighbours on other GPUs read over NVLink
+          through CUDA-IPC peer pointers (strong scaling: total work fixed)
+
+Launch:  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+         (N > 1 through torch.distributed.run, one rank per GPU)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "neighbor_allreduce GB/s/GPU + ATC-DSGD iters/s at 1/2/4/8 B200, % of roofline"
+NVLINK_PEAK_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction (nominal 900)
+HBM_FALLBACK_GBS = 6650.0    # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--agents", type=int, default=8)
+    ap.add_argument("--count", type=int, default=25_600_000)
+    ap.add_argument("--topology", choices=["one_peer", "exp2"], default="one_peer")
+    ap.add_argument("--wire", choices=["fp32", "bf16"], default="fp32")
+    ap.add_argument("--lr", type=float, default=0.1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def degree(topology, n):
+    if n == 1:
+        return 0
+    if topology == "one_peer":
+        return 1
+    d, off = 0, 1
+    while off <= n - 1:
+        d += 1
+        off *= 2
+    return d
+
+
+def workload_name(a):
+    return (f"C4: ATC-DSGD step (fused adapt+exchange+combine), {a.agents} agents x {a.count} fp32 "
+            f"(ResNet-50-sized), {'dynamic one-peer exp-2' if a.topology == 'one_peer' else 'static exp-2'} "
+            f"topology, {a.wire} wire, synthetic gradients")
+
+
+# ---------------------------------------------------------------- clocks ----
+class Clocks:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", "--query-gpu=" + ",".join(self.FIELDS),
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.05)
+        self.p.terminate()
+        try:
+            self.p.wait(5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        for line in self.f.read().splitlines():
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU oracle ----
+def oracle_step_rate(a, budget_s=12.0, prefix=1 << 20):
+    """Time the oracle (oracle/bf_oracle.c, single thread, as it stands) on a
+    bounded prefix sample of the same workload; returns (iters/s extrapolated
+    to the full count, sample description, seconds spent)."""
+    import numpy as np
+
+    import oracle as ora
+    import synthetic
+    n = a.agents
+    X = synthetic.agents_x0(n, prefix).astype(np.float64)
+    G = synthetic.agents_grad(n, prefix, 0).astype(np.float64)
+    Wk = [ora.one_peer_exp2(n, k) if a.topology == "one_peer" else ora.exp2(n) for k in range(3)]
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        X = ora.atc(Wk[steps % 3], X, G, a.lr, wire_bf16=(a.wire == "bf16"))
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    per_step_full = el / steps * (a.count / prefix)
+    sample = (f"{steps} oracle ATC steps on a {prefix}-element prefix of each of the {n} agents "
+              f"({el:.1f} s), extrapolated linearly to {a.count} elements")
+    return 1.0 / per_step_full, sample, el
+
+
+def run_reference(a):
+    """--impl reference: the oracle (CPU) as it stands, same metric/unit."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle as ora
+    import synthetic
+    n, prefix = a.agents, 1 << 19
+    X = synthetic.agents_x0(n, prefix).astype(np.float64)
+    G = synthetic.agents_grad(n, prefix, 0).astype(np.float64)
+    Wk = [ora.one_peer_exp2(n, k) if a.topology == "one_peer" else ora.exp2(n) for k in range(3)]
+    for s in range(a.warmup):
+        X = ora.atc(Wk[s % 3], X, G, a.lr, wire_bf16=(a.wire == "bf16"))
+    t0 = time.perf_counter()
+    for s in range(a.steps):
+        X = ora.atc(Wk[s % 3], X, G, a.lr, wire_bf16=(a.wire == "bf16"))
+    el = time.perf_counter() - t0
+    ms_full = el / a.steps * (a.count / prefix) * 1e3
+    value = 1e3 / ms_full
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_full, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(a), "agents": n, "count": a.count, "topology": a.topology,
+                   "wire": a.wire},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "kind": "oracle",
+                         "sample": f"each step = one oracle ATC step on a {prefix}-element prefix of each agent, "
+                                   f"time scaled linearly to {a.count} elements"},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- ours -----
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if a.agents % world:
+        raise SystemExit(f"{a.agents} agents do not split over {world} GPUs")
+    k = a.agents // world
+    import paper_2111_04287_b200 as bfp
+    import synthetic
+
+    count = a.count
+    wire_dt = torch.float32 if a.wire == "fp32" else torch.bfloat16
+    wire_b = 4 if a.wire == "fp32" else 2
+    heap = k * 2 * count * wire_b + (64 << 20)
+    ctx = bfp.Context(agents_per_proc=k, heap_bytes=heap, device=local)
+    n = ctx.n
+    if a.topology == "one_peer":
+        ctx.set_dynamic_schedule("one_peer_exp2", 0)
+    else:
+        ctx.set_topology(bfp.topology_matrix("exp2", n))
+    ctx.reserve(count * wire_b)
+
+    x = torch.empty(k, count, device="cuda")
+    gs = [torch.empty(k, count, device="cuda") for _ in range(2)]
+    for la in range(k):
+        gid = ctx.rank + la
+        bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + gid)
+        for s, g in enumerate(gs):
+            bfp.Context.fill_uniform(g[la], synthetic.grad_seed(s, gid), scale=2.0 ** -7)
+    torch.cuda.synchronize()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    for s in range(a.warmup):
+        ctx.atc_step(x, gs[s % 2], a.lr, wire=wire_dt)
+    barrier()
+    stream = torch.cuda.current_stream()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    l0 = ctx.kernel_launches()
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_begin.record(stream)
+    for s in range(a.steps):
+        starts[s].record(stream)
+        ctx.atc_step(x, gs[s % 2], a.lr, wire=wire_dt)
+        ends[s].record(stream)
+    t_end.record(stream)
+    barrier()
+    launches = ctx.kernel_launches() - l0
+    total_ms = t_begin.elapsed_time(t_end)
+    kern_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / a.steps
+    ctx.poll_error()
+
+    # ---- end to end through the public API: host gradients in, sample out ----
+    e2e = None
+    if not a.no_e2e:
+        gh = [g.cpu().pin_memory() for g in gs]
+        sample = torch.empty(k, 1024, dtype=torch.float32).pin_memory()
+        for s in range(2):
+            ctx.atc_step(x, gh[s % 2], a.lr, wire=wire_dt)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(a.steps):
+            ctx.atc_step(x, gh[s % 2], a.lr, wire=wire_dt)
+            sample.copy_(x[:, :1024], non_blocking=True)
+        e1.record(stream)
+        barrier()
+        e2e_ms = e0.elapsed_time(e1) / a.steps
+        e2e = {"ms": e2e_ms, "h2d": k * count * 4, "d2h": k * 1024 * 4}
+    clk = clocks.stop()
+    ctx.poll_error()
+
+    # ---- max over ranks ----
+    vals = torch.tensor([total_ms / a.steps, kern_ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64,
+                        device="cuda")
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms_step, ms_kern, ms_e2e = [float(v) for v in vals.cpu()]
+
+    if rank == 0:
+        d = degree(a.topology, n)
+        # algorithmic bytes per launch on this GPU (fused ATC):
+        # x read + x write + g read + publish (wire) + d_out * served (wire)
+        hbm_bytes = k * count * (4 + 4 + 4 + wire_b + d * wire_b)
+        if world > 1:
+            # neighbours on other GPUs: d_in * wire bytes cross NVLink per remote source
+            remote = 0
+            for la in range(k):
+                gid = ctx.rank + la
+                for kk in range(1):
+                    src = [bfp.one_peer_exp2(n, gid, r)[0] for r in range(max(1, (n - 1).bit_length()))] \
+                        if a.topology == "one_peer" else [((gid - (1 << j)) % n) for j in range(d)]
+                    if a.topology == "one_peer":
+                        remote += sum(1 for s in src if s // k != ctx.proc) / len(src)
+                    else:
+                        remote += sum(1 for s in src if s // k != ctx.proc)
+            nvl_bytes = remote * count * wire_b
+        else:
+            nvl_bytes = 0
+        peak_hbm, peak_kind = hbm_peak()
+        t_hbm = hbm_bytes / (peak_hbm * 1e9)
+        t_nvl = nvl_bytes / (NVLINK_PEAK_GBS * 1e9)
+        if t_nvl > t_hbm:
+            roof = {"bound": "nvlink", "achieved": nvl_bytes / (ms_kern * 1e-3) / 1e9, "peak": NVLINK_PEAK_GBS,
+                    "unit": "GB/s", "peak_source": "B200_PROFILING.md measured peer copy per direction"}
+        else:
+            roof = {"bound": "hbm", "achieved": hbm_bytes / (ms_kern * 1e-3) / 1e9, "peak": peak_hbm,
+                    "unit": "GB/s", "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                with open(tp) as f:
+                    tj = json.load(f)
+                key = f"{a.topology}_{a.wire}_n{world}"
+                roof["traffic"] = tj.get(key)
+            except Exception:
+                pass
+        roof["algorithmic_bytes_per_launch"] = hbm_bytes if roof["bound"] == "hbm" else nvl_bytes
+        roof["kernel"] = "bf::exchange_kernel (fused ATC adapt+publish+exchange+combine)"
+        value = 1e3 / ms_step
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(a), "agents": n, "agents_per_gpu": k, "count": count,
+                       "topology": a.topology, "wire": a.wire, "lr": a.lr,
+                       "l2": "inputs larger than L2 (x, 2 rotating gradient sets: "
+                             f"{3 * n * count * 4 / 1e9:.2f} GB)"},
+            "neighbor_allreduce_gbs_per_gpu": (k * d * count * wire_b) / (ms_kern * 1e-3) / 1e9,
+            "gpu_launches": launches,
+            "roofline": roof,
+            "clocks": clk,
+        }
+        if e2e:
+            line["e2e"] = {"value": 1e3 / ms_e2e, "unit": "iters/s", "h2d_bytes_per_step": e2e["h2d"] * world,
+                           "d2h_bytes_per_step": e2e["d2h"] * world,
+                           "path": "Context.atc_step with pinned host gradients (H2D inside the C-ABI call) "
+                                   "+ D2H of 1024 elements per agent"}
+        if world == 1 and not a.no_cpu:
+            v, sample, el = oracle_step_rate(a)
+            line["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle", "sample": sample}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

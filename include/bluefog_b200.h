@@ -1,0 +1,213 @@
+/*
+ * bluefog_b200.h -- C ABI of the B200-native decentralized partial-averaging
+ * hot path (BlueFog, arXiv 2111.04287).
+ *
+ * Citations: P:NNN = line of the paper text (reference PAPER.md), with the
+ * equation / section it belongs to.  "R<k>" = numbered reading of the paper
+ * in DESIGN.md where the paper is silent or garbled.
+ *
+ * Model.  n agents ("nodes") run one process per GPU.  A process
+ * hosts `agents_per_proc` consecutive agents (1 on an 8-GPU box; > 1 to
+ * emulate n agents on fewer GPUs -- "virtual agents").  Global agent id
+ * (the paper's rank) = proc_rank * agents_per_proc + local index.
+ *
+ * Data layout.  Every data call takes STACKED per-process buffers: the
+ * vector of local agent a starts at element a*count (row-major
+ * [agents_per_proc][count]).  All pointers are DEVICE pointers unless a
+ * function says otherwise; `stream` is a cudaStream_t passed as void*
+ * (NULL = legacy default stream).  Calls are stream-ordered and return
+ * before the GPU work completes (that is the non-blocking form of P:635;
+ * "wait" = synchronize the stream).  Caller-owned buffers must stay valid
+ * until the stream work completes; the library never frees them.
+ *
+ * Errors.  Every function returns a bf_status.  Host-side validation is
+ * synchronous and enqueues nothing on failure.  Device-side faults (a spin
+ * that exceeded BF_TIMEOUT_MS, a topology-check mismatch) are latched in the
+ * context: bf_poll_error() returns them and the context is then poisoned
+ * (later calls return BF_ERR_STATE).  bf_last_error() gives a message
+ * (thread-local).  No call ever blocks forever: every device wait is bounded.
+ *
+ * Collectives: bf_connect_peers, bf_set_topology, bf_set_machine_topology,
+ * bf_reserve, bf_neighbor_allreduce, bf_atc_step,
+ * bf_hierarchical_neighbor_allreduce, bf_win_create, bf_win_free and
+ * bf_barrier must be called by every process in the same order.  Window
+ * data calls (put / accumulate / update / collect) are one-sided and need
+ * no matching call.
+ */
+#ifndef BLUEFOG_B200_H
+#define BLUEFOG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bf_ctx bf_ctx;
+
+typedef enum {
+    BF_OK = 0,
+    BF_ERR_ARG = 1,          /* invalid argument (rank range, duplicate, NaN weight, bad config) */
+    BF_ERR_STATE = 2,        /* context not connected / poisoned by an earlier device fault */
+    BF_ERR_TOPOLOGY = 3,     /* send/receive declarations do not match */
+    BF_ERR_CUDA = 4,         /* a CUDA runtime call failed */
+    BF_ERR_TIMEOUT = 5,      /* a device wait exceeded BF_TIMEOUT_MS (peer missing / stalled) */
+    BF_ERR_NOMEM = 6,        /* symmetric heap exhausted */
+    BF_ERR_UNSUPPORTED = 7,  /* limits below exceeded, or unsupported dtype combination */
+    BF_ERR_WINDOW = 8        /* unknown / duplicate window name, dst outside creation topology */
+} bf_status;
+
+typedef enum { BF_FLOAT32 = 0, BF_BFLOAT16 = 1 } bf_dtype;
+
+/* Limits of this build. */
+#define BF_MAX_AGENTS 64          /* n */
+#define BF_MAX_PROCS 16           /* processes (GPUs) */
+#define BF_MAX_LOCAL_AGENTS 16    /* agents_per_proc */
+#define BF_MAX_DEGREE 16          /* declared sources / destinations per agent per call */
+
+/* Local view of Eq. 9 for ONE agent and ONE call:
+ *   x_i <- self_weight * x_i + sum_j r_ij * s_ij * x_j.
+ * src_weights are r_ij for j in N(i) (receiver side, Eq. 11); dst_weights are
+ * s_ji for j in M(i) (sender side, Eq. 10).  n_src < 0 / n_dst < 0 means "not
+ * given".  Valid configurations (P:381 footnote): self+dst (push), self+src
+ * (pull), self+src+dst (push-pull).  The static form is a NULL bf_weights
+ * pointer.  Ranks are global agent ids; self or duplicate ranks -> BF_ERR_ARG.
+ * Weights may be any finite real (Eq. 8 allows w_ij in R; reading R3). */
+typedef struct {
+    double self_weight;
+    int n_src;
+    const int *src_ranks;
+    const double *src_weights;
+    int n_dst;
+    const int *dst_ranks;
+    const double *dst_weights;
+} bf_weights;
+
+/* ---- context ------------------------------------------------------------------
+ * bf_init: create the context of process `proc_rank` of `n_procs`, hosting
+ * `agents_per_proc` agents on CUDA device `cuda_device`, with a symmetric
+ * heap of `heap_bytes` device bytes (exchange slots, windows, hierarchical
+ * buffers and signal pads all live there; it is exported through CUDA IPC).
+ * Env: BF_TIMEOUT_MS (default 10000) bounds every device wait. */
+bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_device,
+                  size_t heap_bytes, bf_ctx **out);
+/* Bootstrap: each process writes its blob (<= bf_ipc_blob_size() bytes) and the
+ * caller all-gathers them (e.g. torch.distributed) in proc order, then every
+ * process calls bf_connect_peers(ctx, all_blobs, blob_len) (collective).
+ * With n_procs == 1 call bf_connect_peers(ctx, NULL, 0). */
+size_t bf_ipc_blob_size(void);
+bf_status bf_get_ipc_blob(bf_ctx *ctx, void *blob, size_t *len);
+bf_status bf_connect_peers(bf_ctx *ctx, const void *blobs, size_t blob_len);
+bf_status bf_finalize(bf_ctx *ctx);
+int bf_size(const bf_ctx *ctx);                /* n, total agents ("size") */
+int bf_rank(const bf_ctx *ctx);                /* global id of local agent 0 */
+int bf_local_agents(const bf_ctx *ctx);
+const char *bf_last_error(void);
+const char *bf_status_string(bf_status s);
+
+/* ---- topology (global view; P:199-206 neighbour sets) ---------------
+ * W[i*n + j] = w_ij, the weight agent i applies to x_j (Eq. 8).  Every process
+ * passes the same W.  Default before any call: fully connected 1/n (R15). */
+bf_status bf_set_topology(bf_ctx *ctx, int n, const double *W);
+/* Hierarchical machine topology: machines of `local_size` consecutive
+ * agents (machine_rank = rank // local_size); WM is n_machines^2. */
+bf_status bf_set_machine_topology(bf_ctx *ctx, int local_size, int n_machines, const double *WM);
+bf_status bf_in_neighbors(bf_ctx *ctx, int agent, int *ranks, int cap, int *n_out);
+bf_status bf_out_neighbors(bf_ctx *ctx, int agent, int *ranks, int cap, int *n_out);
+/* Built-in topologies into W (n*n, caller-owned host array): 0 ring,
+ * 1 exponential-2 (R4), 2 fully connected, 3 one-peer exp-2 at round k. */
+bf_status bf_topology_matrix(int kind, int n, uint64_t k, double *W);
+/* One-peer dynamic exponential-2 schedule (R5): at round k, t = k mod
+ * ceil(log2 n); agent `rank` pulls from rank - 2^t and pushes to rank + 2^t. */
+bf_status bf_schedule_one_peer_exp2(int n, int rank, uint64_t round, int *src, int *dst);
+/* kind 0: none (static W); 1: one-peer exp-2 evaluated ON DEVICE from a
+ * device-resident round counter starting at round0, advanced by every
+ * schedule-mode call (graph-capturable). */
+bf_status bf_set_dynamic_schedule(bf_ctx *ctx, int kind, uint64_t round0);
+bf_status bf_set_topology_check(bf_ctx *ctx, int enable);   /* P:613; default on */
+
+/* ---- the hot path ------------------------------------------------------------
+ * bf_neighbor_allreduce (Eq. 5 P:183 static; Eq. 9-11 P:355-362 dynamic):
+ * y_i = w_ii x_i + sum_j w_ij x_j for every local agent i.  x, y: stacked
+ * [agents_per_proc][count] of `dtype`; y may alias x.  weights: NULL (static /
+ * schedule) or an array of agents_per_proc local views.  fp32 accumulation;
+ * bf16 output rounded RNE. */
+bf_status bf_neighbor_allreduce(bf_ctx *ctx, const void *x, void *y, size_t count, bf_dtype dtype,
+                                const bf_weights *weights, void *stream);
+/* bf_atc_step: fused adapt-then-combine DSGD step (Eq. 4-5, Eq. 17
+ * P:711, R6): x_i <- sum_j w_ij (x_j - lr*g_j), in place on the fp32 master x.
+ * g: `g_dtype` gradients; x or g may be HOST pointers (pinned or pageable):
+ * they are then staged through device memory inside the call (end-to-end
+ * path).  wire: dtype of the copy neighbours read (R18: the agent's own term
+ * uses the fp32 x_half).  x_bf16_shadow (nullable): also write RNE(x). */
+bf_status bf_atc_step(bf_ctx *ctx, float *x, const void *g, bf_dtype g_dtype, size_t count,
+                      float lr, bf_dtype wire, void *x_bf16_shadow,
+                      const bf_weights *weights, void *stream);
+/* bf_hierarchical_neighbor_allreduce (R12): y = (W_M kron J_L/L) x:
+ * intra-machine average, machine-level neighbour averaging, broadcast.
+ * machine_weights: NULL (static machine topology) or an array of
+ * agents_per_proc views whose ranks are MACHINE ranks (self + src, pull form;
+ * every agent of a machine must pass the same view). */
+bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *ctx, const void *x, void *y, size_t count,
+                                             bf_dtype dtype, const bf_weights *machine_weights,
+                                             void *stream);
+
+/* ---- one-sided windows (async push-sum P:551-585) -------------------
+ * bf_win_create (collective): registers the stacked tensor x (borrowed until
+ * bf_win_free) and allocates, for every local agent and every in-neighbour of
+ * the CURRENT static topology (ascending rank), a double-buffered slot
+ * (R11).  zero_init != 0: slots start at 0; else at a copy of the
+ * local tensor (R10).  with_p != 0 adds the push-sum weight p (fp64, starts at
+ * 1) that travels with every payload. */
+bf_status bf_win_create(bf_ctx *ctx, const char *name, void *x, size_t count, bf_dtype dtype,
+                        int zero_init, int with_p);
+bf_status bf_win_free(bf_ctx *ctx, const char *name);
+/* put / accumulate by the local agents selected in agent_mask (bit a = local
+ * agent a; 0 = all): for each dst j in weights[a] (self + dst only; dst must
+ * be out-neighbours at creation) deliver s_ja * x_a into j's slot for a
+ * (put: overwrite, accumulate: add), then x_a <- self_weight * x_a
+ * (R8).  A payload whose destination half is still unconsumed waits in a
+ * sender-side outbox and is delivered by a later call (no remote
+ * read-modify-write, no lock; require_mutex is accepted, the versioned
+ * single-producer/single-consumer slot IS the mutex). weights == NULL:
+ * all out-neighbours with 1/(outdegree+1) (Listing 3). */
+bf_status bf_win_put(bf_ctx *ctx, const char *name, const bf_weights *weights,
+                     uint64_t agent_mask, void *stream);
+bf_status bf_win_accumulate(bf_ctx *ctx, const char *name, const bf_weights *weights,
+                            int require_mutex, uint64_t agent_mask, void *stream);
+/* bf_win_update: out_a = self_w * x_a + sum_j r_aj * (latest
+ * complete payload from j); weights NULL = uniform 1/(d_in+1) (R10); out NULL =
+ * in place.  Marks the read payloads consumed; slots are not reset. */
+bf_status bf_win_update(bf_ctx *ctx, const char *name, const bf_weights *weights, void *out,
+                        uint64_t agent_mask, void *stream);
+/* bf_win_update_then_collect (R9): x_a += every delivered, not yet
+ * consumed payload (and p += its p), then release the halves.  In place. */
+bf_status bf_win_update_then_collect(bf_ctx *ctx, const char *name, uint64_t agent_mask,
+                                     void *stream);
+/* Host reads (synchronize `stream` first): p of every local agent (fp64
+ * [agents_per_proc]), and the slot counters of (dst local agent, src rank). */
+bf_status bf_win_get_p(bf_ctx *ctx, const char *name, double *p_host, void *stream);
+bf_status bf_win_counters(bf_ctx *ctx, const char *name, int dst_local, int src_rank,
+                          uint64_t *version, uint64_t *consumed);
+/* Slot layout of agent `agent` (P:388 pin): element offset of the slot that
+ * receives from `src_rank` in the paper's logical numel*d_in layout, or -1. */
+long long bf_win_slot_offset(bf_ctx *ctx, const char *name, int agent, int src_rank);
+
+/* ---- misc ----------------------------------------------------------------------- */
+bf_status bf_barrier(bf_ctx *ctx, void *stream);      /* device barrier over all processes */
+bf_status bf_poll_error(bf_ctx *ctx);                 /* latched device fault, non-blocking */
+/* Reserve exchange capacity (collective; optional -- the first call reserves
+ * what it needs): bytes per agent of the largest message. */
+bf_status bf_reserve(bf_ctx *ctx, size_t bytes_per_agent);
+/* Synthetic input generator (same counter-based
+ * generator as synthetic/__init__.py): dst[i] = u(seed, offset+i) * scale. */
+bf_status bf_fill_uniform(void *dst, bf_dtype dtype, size_t count, uint64_t seed,
+                          uint64_t offset, float scale, void *stream);
+/* Number of kernels the library launched so far on this context (bench accounting). */
+uint64_t bf_kernel_launches(const bf_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLUEFOG_B200_H */

@@ -1,0 +1,291 @@
+"""Paper-style Python API over the C ABI (argument marshalling only).
+
+Mirrors BlueFog's primitives: set_topology,
+neighbor_allreduce (static, or dynamic with self/src/dst weights),
+atc_step (the fused adapt-then-combine DSGD step), hierarchical_neighbor_allreduce,
+win_create / win_put / win_accumulate / win_update / win_update_then_collect /
+win_free, barrier.  PyTorch is used for device memory, streams and the
+torch.distributed bootstrap only; every step of the path runs in the CUDA
+kernels of libbluefog_b200.so.
+
+Tensors hold the process's local agents stacked: shape (agents_per_proc, count)
+(a 1-D tensor is accepted when agents_per_proc == 1).  Weight arguments follow
+the paper: self_weight (float), src_weights / dst_weights ({rank: weight});
+with several local agents pass one value per agent (lists).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BluefogError, bf_weights, check
+
+_DT = {torch.float32: _lib.BF_FLOAT32, torch.bfloat16: _lib.BF_BFLOAT16}
+
+
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _allgather_bytes(payload: bytes, group=None) -> list:
+    """All-gather one bytes object per process (bootstrap plumbing)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, payload, group=group)
+    return out
+
+
+def topology_matrix(kind: str, n: int, round: int = 0) -> np.ndarray:
+    """Built-in topologies of the library: ring, exp2, full, one_peer_exp2."""
+    kinds = {"ring": 0, "exp2": 1, "full": 2, "one_peer_exp2": 3}
+    W = np.zeros((n, n), np.float64)
+    check(_lib.load().bf_topology_matrix(kinds[kind], n, int(round),
+                                         W.ctypes.data_as(C.POINTER(C.c_double))))
+    return W
+
+
+def one_peer_exp2(n: int, rank: int, round: int):
+    s, d = C.c_int(), C.c_int()
+    check(_lib.load().bf_schedule_one_peer_exp2(n, rank, int(round), C.byref(s), C.byref(d)))
+    return s.value, d.value
+
+
+class _Views:
+    """Keeps a ctypes bf_weights array (and its backing arrays) alive."""
+
+    def __init__(self, k, self_weight, src_weights, dst_weights):
+        def per_agent(v):
+            if isinstance(v, (list, tuple)):
+                if len(v) != k:
+                    raise ValueError(f"expected {k} per-agent values, got {len(v)}")
+                return list(v)
+            return [v] * k if k == 1 else [v] * k
+
+        sw, srcw, dstw = per_agent(self_weight), per_agent(src_weights), per_agent(dst_weights)
+        self.arr = (bf_weights * k)()
+        self._keep = []
+        for a in range(k):
+            w = self.arr[a]
+            w.self_weight = float("nan") if sw[a] is None else float(sw[a])
+            for kind, spec in (("src", srcw[a]), ("dst", dstw[a])):
+                if spec is None:
+                    setattr(w, "n_" + kind, -1)
+                    continue
+                ranks = sorted(int(r) for r in spec)
+                ra = (C.c_int * max(1, len(ranks)))(*ranks)
+                va = (C.c_double * max(1, len(ranks)))(*[float(spec[r]) for r in ranks])
+                self._keep += [ra, va]
+                setattr(w, "n_" + kind, len(ranks))
+                setattr(w, kind + "_ranks", C.cast(ra, C.POINTER(C.c_int)))
+                setattr(w, kind + "_weights", C.cast(va, C.POINTER(C.c_double)))
+
+    def ptr(self):
+        return C.cast(self.arr, C.POINTER(bf_weights))
+
+
+class Context:
+    """One process = one GPU hosting `agents_per_proc` agents (virtual agents if > 1)."""
+
+    def __init__(self, agents_per_proc: int = 1, heap_bytes: int = 1 << 30, device: Optional[int] = None,
+                 proc_rank: Optional[int] = None, n_procs: Optional[int] = None, group=None):
+        self.lib = _lib.load()
+        import torch.distributed as dist
+        dist_on = dist.is_available() and dist.is_initialized()
+        if proc_rank is None:
+            proc_rank = dist.get_rank(group) if dist_on else 0
+        if n_procs is None:
+            n_procs = dist.get_world_size(group) if dist_on else 1
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", torch.cuda.current_device() if torch.cuda.is_available() else 0))
+        self.device = device
+        self.k = agents_per_proc
+        self.proc = proc_rank
+        self.nprocs = n_procs
+        h = C.c_void_p()
+        check(self.lib.bf_init(proc_rank, n_procs, agents_per_proc, device, int(heap_bytes), C.byref(h)))
+        self.h = h
+        blen = self.lib.bf_ipc_blob_size()
+        if n_procs > 1:
+            buf = C.create_string_buffer(blen)
+            ln = C.c_size_t(blen)
+            check(self.lib.bf_get_ipc_blob(h, buf, C.byref(ln)))
+            blobs = _allgather_bytes(buf.raw[:ln.value], group)
+            allb = b"".join(blobs)
+            check(self.lib.bf_connect_peers(h, allb, ln.value))
+        else:
+            check(self.lib.bf_connect_peers(h, None, 0))
+        self.n = self.lib.bf_size(h)
+        self.rank = self.lib.bf_rank(h)
+
+    # ---- lifecycle ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.bf_finalize(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- helpers -----------------------------------------------------------
+    def _rows(self, t: torch.Tensor) -> int:
+        if not t.is_cuda and not t.is_pinned() and t.device.type != "cpu":
+            raise ValueError("unsupported tensor device")
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        if t.numel() % self.k:
+            raise ValueError(f"tensor numel {t.numel()} not divisible by agents_per_proc {self.k}")
+        return t.numel() // self.k
+
+    def _views(self, self_weight, src_weights, dst_weights):
+        if self_weight is None and src_weights is None and dst_weights is None:
+            return None
+        return _Views(self.k, self_weight, src_weights, dst_weights)
+
+    # ---- topology ------------------------------------------------
+    def set_topology(self, W) -> bool:
+        W = np.ascontiguousarray(np.asarray(W, np.float64))
+        check(self.lib.bf_set_topology(self.h, W.shape[0], W.ctypes.data_as(C.POINTER(C.c_double))))
+        return True
+
+    def set_machine_topology(self, WM, local_size: int) -> bool:
+        WM = np.ascontiguousarray(np.asarray(WM, np.float64))
+        check(self.lib.bf_set_machine_topology(self.h, local_size, WM.shape[0],
+                                               WM.ctypes.data_as(C.POINTER(C.c_double))))
+        return True
+
+    def in_neighbor_ranks(self, agent: Optional[int] = None):
+        return self._nbrs(self.lib.bf_in_neighbors, agent)
+
+    def out_neighbor_ranks(self, agent: Optional[int] = None):
+        return self._nbrs(self.lib.bf_out_neighbors, agent)
+
+    def _nbrs(self, fn, agent):
+        agent = self.rank if agent is None else agent
+        buf = (C.c_int * _lib.MAX_AGENTS)()
+        n = C.c_int()
+        check(fn(self.h, agent, buf, _lib.MAX_AGENTS, C.byref(n)))
+        return list(buf[:n.value])
+
+    def set_dynamic_schedule(self, kind: str = "one_peer_exp2", round0: int = 0):
+        check(self.lib.bf_set_dynamic_schedule(self.h, {"none": 0, "one_peer_exp2": 1}[kind], int(round0)))
+
+    def set_topology_check(self, enable: bool):
+        check(self.lib.bf_set_topology_check(self.h, 1 if enable else 0))
+
+    def reserve(self, bytes_per_agent: int):
+        check(self.lib.bf_reserve(self.h, int(bytes_per_agent)))
+
+    # ---- hot path ----------------------------------------------------------
+    def neighbor_allreduce(self, tensor: torch.Tensor, self_weight=None, src_weights=None, dst_weights=None,
+                           out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """Eq. 5 / Eq. 9 partial averaging."""
+        count = self._rows(tensor)
+        y = torch.empty_like(tensor) if out is None else out
+        v = self._views(self_weight, src_weights, dst_weights)
+        check(self.lib.bf_neighbor_allreduce(self.h, C.c_void_p(tensor.data_ptr()), C.c_void_p(y.data_ptr()),
+                                             count, _DT[tensor.dtype], v.ptr() if v else None,
+                                             _stream_ptr(stream)))
+        return y
+
+    def atc_step(self, x: torch.Tensor, g: torch.Tensor, lr: float, wire: torch.dtype = torch.float32,
+                 shadow: Optional[torch.Tensor] = None, self_weight=None, src_weights=None, dst_weights=None,
+                 stream=None) -> torch.Tensor:
+        """Fused ATC-DSGD step (Eq. 4-5, Eq. 17), in place on the fp32 master x."""
+        if x.dtype != torch.float32:
+            raise ValueError("x must be the fp32 master copy")
+        count = self._rows(x)
+        v = self._views(self_weight, src_weights, dst_weights)
+        check(self.lib.bf_atc_step(self.h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()), _DT[g.dtype],
+                                   count, float(lr), _DT[wire],
+                                   C.c_void_p(shadow.data_ptr()) if shadow is not None else None,
+                                   v.ptr() if v else None, _stream_ptr(stream)))
+        return x
+
+    def hierarchical_neighbor_allreduce(self, tensor: torch.Tensor, self_weight=None, src_machine_weights=None,
+                                        out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """P:660-675 (machine-level neighbour averaging of machine averages)."""
+        count = self._rows(tensor)
+        y = torch.empty_like(tensor) if out is None else out
+        v = self._views(self_weight, src_machine_weights, None)
+        check(self.lib.bf_hierarchical_neighbor_allreduce(self.h, C.c_void_p(tensor.data_ptr()),
+                                                          C.c_void_p(y.data_ptr()), count, _DT[tensor.dtype],
+                                                          v.ptr() if v else None, _stream_ptr(stream)))
+        return y
+
+    # ---- windows ---------------------------------------------------
+    def win_create(self, tensor: torch.Tensor, name: str, zero_init: bool = True, with_p: bool = False) -> bool:
+        count = self._rows(tensor)
+        torch.cuda.synchronize(self.device)
+        check(self.lib.bf_win_create(self.h, name.encode(), C.c_void_p(tensor.data_ptr()), count,
+                                     _DT[tensor.dtype], 1 if zero_init else 0, 1 if with_p else 0))
+        return True
+
+    def win_free(self, name: str) -> bool:
+        torch.cuda.synchronize(self.device)
+        check(self.lib.bf_win_free(self.h, name.encode()))
+        return True
+
+    def win_put(self, name: str, self_weight=None, dst_weights=None, agent_mask: int = 0, stream=None) -> bool:
+        v = self._views(self_weight, None, dst_weights)
+        check(self.lib.bf_win_put(self.h, name.encode(), v.ptr() if v else None, agent_mask, _stream_ptr(stream)))
+        return True
+
+    def win_accumulate(self, name: str, self_weight=None, dst_weights=None, require_mutex: bool = True,
+                       agent_mask: int = 0, stream=None) -> bool:
+        v = self._views(self_weight, None, dst_weights)
+        check(self.lib.bf_win_accumulate(self.h, name.encode(), v.ptr() if v else None,
+                                         1 if require_mutex else 0, agent_mask, _stream_ptr(stream)))
+        return True
+
+    def win_update(self, name: str, self_weight=None, src_weights=None, out: Optional[torch.Tensor] = None,
+                   agent_mask: int = 0, stream=None):
+        v = self._views(self_weight, src_weights, None)
+        check(self.lib.bf_win_update(self.h, name.encode(), v.ptr() if v else None,
+                                     C.c_void_p(out.data_ptr()) if out is not None else None, agent_mask,
+                                     _stream_ptr(stream)))
+        return out
+
+    def win_update_then_collect(self, name: str, agent_mask: int = 0, stream=None) -> bool:
+        check(self.lib.bf_win_update_then_collect(self.h, name.encode(), agent_mask, _stream_ptr(stream)))
+        return True
+
+    def win_p(self, name: str, stream=None) -> np.ndarray:
+        p = np.zeros(self.k, np.float64)
+        check(self.lib.bf_win_get_p(self.h, name.encode(), p.ctypes.data_as(C.POINTER(C.c_double)),
+                                    _stream_ptr(stream)))
+        return p
+
+    def win_counters(self, name: str, dst_local: int, src_rank: int):
+        v, c = C.c_uint64(), C.c_uint64()
+        check(self.lib.bf_win_counters(self.h, name.encode(), dst_local, src_rank, C.byref(v), C.byref(c)))
+        return v.value, c.value
+
+    def win_slot_offset(self, name: str, agent: int, src_rank: int) -> int:
+        return self.lib.bf_win_slot_offset(self.h, name.encode(), agent, src_rank)
+
+    # ---- misc ------------------------------------------------------------------
+    def barrier(self, stream=None):
+        check(self.lib.bf_barrier(self.h, _stream_ptr(stream)))
+
+    def poll_error(self):
+        check(self.lib.bf_poll_error(self.h))
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.bf_kernel_launches(self.h))
+
+    @staticmethod
+    def fill_uniform(t: torch.Tensor, seed: int, offset: int = 0, scale: float = 1.0, stream=None):
+        """Synthetic input generator (same counter-based generator as synthetic/)."""
+        check(_lib.load().bf_fill_uniform(C.c_void_p(t.data_ptr()), _DT[t.dtype], t.numel(), int(seed), int(offset),
+                                          float(scale), _stream_ptr(stream)))
+        return t

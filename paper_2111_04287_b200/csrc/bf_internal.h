@@ -1,0 +1,169 @@
+// bf_internal.h -- internal structures shared by the runtime (runtime.cu) and
+// the sm_100a kernels (exchange.cu, window.cu, generate.cu).
+//
+// Symmetric heap.  Every process cudaMalloc's one heap of the same size and
+// exports it through CUDA IPC.  All collective allocations are made in the
+// same order on every process, so a region has the same OFFSET in every heap:
+// the address of process q's copy is peer_base[q] + offset.  Byte 0 of the
+// heap is the process's signal pad (struct Pad).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bluefog_b200.h"
+
+namespace bf {
+
+constexpr int kTile = 4096;            // elements per tile (the unit of one flag)
+constexpr int kThreads = 256;          // threads per CTA of the streaming kernels
+constexpr int kVec = 4;                // elements per vector access
+constexpr int kVecPerThread = kTile / (kThreads * kVec);   // 4
+constexpr int kMaxK = BF_MAX_LOCAL_AGENTS;
+constexpr int kMaxS = BF_MAX_DEGREE;
+constexpr int kMaxN = BF_MAX_AGENTS;
+constexpr int kMaxP = BF_MAX_PROCS;
+constexpr size_t kPadBytes = 64 * 1024;
+constexpr size_t kAlign = 4096;
+
+// Per-agent, per-parity descriptor of a dynamic call (push side of Eq. 9):
+// which agents this agent pushes to and with which s (sender-side weight).
+struct Desc {
+    unsigned long long epoch;      // epoch this descriptor belongs to
+    unsigned long long dstmask;    // bit j: this agent declared j as destination
+    unsigned long long has_dst;    // 1 if the agent declared destinations at all (push / push-pull)
+    unsigned long long pad_;
+    float s[kMaxN];                // s_j: weight for destination j
+};
+
+struct Pad {
+    unsigned long long epoch;      // last completed exchange epoch of this process
+    unsigned long long round;      // device-resident one-peer schedule round
+    unsigned int done_ctr;         // CTA completion counter of the running kernel
+    unsigned int abort;            // nonzero: abort code (bf_status) -- set locally or by a peer
+    unsigned long long resv[13];
+    unsigned long long done_from[kMaxP];   // done_from[q] = last epoch process q finished reading
+    unsigned long long bar_from[kMaxP];    // device barrier arrivals
+    Desc desc[kMaxK][2];
+};
+static_assert(sizeof(Pad) <= kPadBytes, "pad too large");
+
+// Source table of one local agent for one call.
+struct SrcTab {
+    float self_w[kMaxK];
+    float coef[kMaxK][kMaxS];
+    unsigned char src[kMaxK][kMaxS];
+    unsigned char nsrc[kMaxK];
+};
+
+// Dynamic-call declarations of the local agents (kernel-side copy of bf_weights).
+struct DynDecl {
+    unsigned char has_src[kMaxK];
+    unsigned char has_dst[kMaxK];
+    unsigned char ndst[kMaxK];
+    unsigned char dst[kMaxK][kMaxS];
+    float s[kMaxK][kMaxS];
+};
+
+enum WMode : int { kWStatic = 0, kWSchedule = 1, kWDynamic = 2 };
+
+struct Geometry {
+    int k;               // local agents
+    int n;               // total agents
+    int me;              // process rank
+    int nprocs;
+    long long count;     // elements per agent
+    int T;               // tiles per agent
+    int vec_ok;          // all rows 16B aligned and count % 4 == 0
+    unsigned long long timeout_ns;
+    unsigned long long peer_base[kMaxP];   // heap base of every process, valid in this process
+    volatile unsigned int *host_err;       // mapped pinned word
+};
+
+struct ExchParams {
+    Geometry geo;
+    int x_kind, wire_kind, y_kind;         // 0 fp32, 1 bf16 (the template also fixes them)
+    const void *x;
+    const void *g;
+    void *y;
+    void *shadow;                           // bf16 copy of y (nullable)
+    float lr;
+    // exchange region (offsets into every heap)
+    unsigned long long slot_off, slot_agent_stride, slot_parity_stride;
+    unsigned long long ready_off;           // u64 [k][ready_stride]
+    int ready_stride;
+    int wmode;
+    int check;
+    SrcTab tab;                             // kWStatic: final coefficients; kWDynamic: declared r
+    DynDecl dyn;
+};
+
+// Hierarchical neighbour allreduce: stages A (publish), B (intra-
+// machine average of one slice), C (machine-level combine of the slice),
+// D (gather the slices).
+struct HierParams {
+    Geometry geo;
+    const void *x;
+    void *y;
+    int L;                                  // agents per machine
+    int TS;                                 // tiles per slice
+    unsigned long long slot_off, slot_agent_stride, slot_parity_stride;   // stage A (x dtype)
+    unsigned long long ready_off;
+    int ready_stride;
+    unsigned long long b_off, c_off, bc_agent_stride, bc_parity_stride;   // fp32 slices
+    unsigned long long fb_off, fc_off;      // u64 flags [k][ready_stride]
+    SrcTab mtab;                            // machine-level: src = machine ids
+};
+
+// One-sided windows.
+struct WinParams {
+    Geometry geo;
+    void *x;                                // registered stacked tensor
+    void *out;                              // win_update output (or == x)
+    int dtype;                              // 0 fp32, 1 bf16 (slot dtype = x dtype)
+    int overwrite;                          // put
+    int ef;                                 // error feedback of the bf16 wire rounding into the outbox
+    int with_p;
+    unsigned long long agent_mask;
+    int maxdin, maxdout;
+    // heap offsets (symmetric)
+    unsigned long long slot_off;            // [k][maxdin][2][count]
+    unsigned long long pslot_off;           // double [k][maxdin][2]
+    unsigned long long version_off;         // u64 [k][maxdin]   (written by producers)
+    unsigned long long consumed_off;        // u64 [k][maxdout]  (written by consumers)
+    unsigned long long outbox_off;          // float [k][maxdout][count]
+    unsigned long long pout_off;            // double [k][maxdout]
+    unsigned long long delivered_off;       // u64 [k][maxdout]  (local control)
+    unsigned long long obvalid_off;         // u32 [k][maxdout]
+    unsigned long long conslocal_off;       // u64 [k][maxdin]
+    unsigned long long p_off;               // double [k]
+    unsigned long long dec_off;             // u64 [k][maxdout] push decisions
+    unsigned long long snap_off;            // u64 [k][maxdin][2] collect snapshot (c, v)
+    // per-call tables
+    float self_w[kMaxK];
+    unsigned char nout[kMaxK];              // selected destinations of local agent a
+    unsigned char out_q[kMaxK][kMaxS];      // out-index (position in the creation out-list)
+    unsigned char out_dst[kMaxK][kMaxS];    // destination agent id
+    unsigned char out_qin[kMaxK][kMaxS];    // its in-index at the destination
+    float out_s[kMaxK][kMaxS];
+    double out_sd[kMaxK][kMaxS];            // the same weights in fp64 for the p lane
+    double self_wd[kMaxK];
+    unsigned char nin[kMaxK];               // all creation in-neighbours of local agent a
+    unsigned char in_src[kMaxK][kMaxS];
+    unsigned char in_qout[kMaxK][kMaxS];    // position of a in the source's out-list
+    float in_r[kMaxK][kMaxS];               // win_update weights
+};
+
+// ---- launchers (exchange.cu / window.cu / generate.cu) --------------------
+cudaError_t launch_exchange(const ExchParams &p, int x_kind, int g_kind, int wire_kind, int y_kind,
+                            int has_g, int grid, cudaStream_t s);
+cudaError_t launch_hier(const HierParams &p, int x_kind, int grid, cudaStream_t s);
+cudaError_t launch_barrier(const Geometry &geo, unsigned long long epoch, cudaStream_t s);
+cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s);
+cudaError_t launch_win_collect(const WinParams &p, int update, int grid, cudaStream_t s);
+cudaError_t launch_fill_uniform(void *dst, int kind, size_t count, unsigned long long seed,
+                                unsigned long long offset, float scale, cudaStream_t s);
+cudaError_t launch_set_u64(unsigned long long *dst, unsigned long long v, cudaStream_t s);
+int max_coresident(const void *func, int threads, size_t smem);
+
+}  // namespace bf

@@ -1,0 +1,182 @@
+// dev_common.cuh -- device helpers for the sm_100a kernels: system-scope
+// acquire/release flags (cross-GPU over NVLink through CUDA-IPC mappings),
+// bounded spins, 4-element vector loads/stores for fp32 / bf16.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "bf_internal.h"
+
+namespace bf {
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_u32(unsigned int *p, unsigned int v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_relaxed_sys_u32(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <typename T>
+__device__ __forceinline__ T *at(unsigned long long base, unsigned long long off) {
+    return reinterpret_cast<T *>(base + off);
+}
+
+__device__ __forceinline__ Pad *pad_of(const Geometry &g, int proc) {
+    return reinterpret_cast<Pad *>(g.peer_base[proc]);
+}
+
+// Raise an abort in every process (so peers stop waiting quickly) and latch
+// the code in the host-mapped error word.
+static __device__ __noinline__ void abort_all(const Geometry &g, unsigned int code) {
+    for (int q = 0; q < g.nprocs; ++q) st_relaxed_sys_u32(&pad_of(g, q)->abort, code);
+    if (g.host_err) *g.host_err = code;
+    __threadfence_system();
+}
+
+// Spin until *flag >= target.  Bounded by the context timeout and by the
+// abort word of this process.  Returns false on timeout / abort.
+__device__ __forceinline__ bool spin_ge(const Geometry &g, const unsigned long long *flag,
+                                        unsigned long long target) {
+    if (ld_acquire_sys(flag) >= target) return true;
+    const unsigned long long t0 = globaltimer();
+    const unsigned int *abort_w = &pad_of(g, g.me)->abort;
+    unsigned int it = 0;
+    while (true) {
+        if (ld_acquire_sys(flag) >= target) return true;
+        if ((++it & 63u) == 0) {
+            if (ld_relaxed_sys_u32(abort_w)) return false;
+            if (globaltimer() - t0 > g.timeout_ns) {
+                abort_all(g, BF_ERR_TIMEOUT);
+                return false;
+            }
+        }
+        __nanosleep(64);
+    }
+}
+
+// ---- 4-element vector access --------------------------------------------
+// fp32: one 16-byte access; bf16: one 8-byte access.  `valid` < 4 takes the
+// guarded scalar path (ragged tail / unaligned rows).
+template <typename T>
+struct Vec4;
+
+template <>
+struct Vec4<float> {
+    static __device__ __forceinline__ void load(const float *p, float v[4], int valid, bool vec) {
+        if (vec && valid == 4) {
+            float4 q = *reinterpret_cast<const float4 *>(p);
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = i < valid ? p[i] : 0.f;
+        }
+    }
+    // L2-only load (peer slots: never serve a stale L1 line)
+    static __device__ __forceinline__ void load_cg(const float *p, float v[4], int valid, bool vec) {
+        if (vec && valid == 4) {
+            float4 q = __ldcg(reinterpret_cast<const float4 *>(p));
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = i < valid ? __ldcg(p + i) : 0.f;
+        }
+    }
+    static __device__ __forceinline__ void store(float *p, const float v[4], int valid, bool vec) {
+        if (vec && valid == 4) {
+            *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (i < valid) p[i] = v[i];
+        }
+    }
+};
+
+__device__ __forceinline__ unsigned short f2bf(float f) {
+    __nv_bfloat16 h = __float2bfloat16_rn(f);
+    return *reinterpret_cast<unsigned short *>(&h);
+}
+__device__ __forceinline__ float bf2f(unsigned short u) {
+    return __uint_as_float(static_cast<unsigned int>(u) << 16);
+}
+
+template <>
+struct Vec4<__nv_bfloat16> {
+    static __device__ __forceinline__ void load(const __nv_bfloat16 *p, float v[4], int valid, bool vec) {
+        const unsigned short *q = reinterpret_cast<const unsigned short *>(p);
+        if (vec && valid == 4) {
+            uint2 w = *reinterpret_cast<const uint2 *>(q);
+            v[0] = __uint_as_float(w.x << 16); v[1] = __uint_as_float(w.x & 0xFFFF0000u);
+            v[2] = __uint_as_float(w.y << 16); v[3] = __uint_as_float(w.y & 0xFFFF0000u);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = i < valid ? bf2f(q[i]) : 0.f;
+        }
+    }
+    static __device__ __forceinline__ void load_cg(const __nv_bfloat16 *p, float v[4], int valid, bool vec) {
+        const unsigned short *q = reinterpret_cast<const unsigned short *>(p);
+        if (vec && valid == 4) {
+            uint2 w = __ldcg(reinterpret_cast<const uint2 *>(q));
+            v[0] = __uint_as_float(w.x << 16); v[1] = __uint_as_float(w.x & 0xFFFF0000u);
+            v[2] = __uint_as_float(w.y << 16); v[3] = __uint_as_float(w.y & 0xFFFF0000u);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = i < valid ? bf2f(__ldcg(q + i)) : 0.f;
+        }
+    }
+    static __device__ __forceinline__ void store(__nv_bfloat16 *p, const float v[4], int valid, bool vec) {
+        unsigned short *q = reinterpret_cast<unsigned short *>(p);
+        if (vec && valid == 4) {
+            uint2 w;
+            w.x = static_cast<unsigned int>(f2bf(v[0])) | (static_cast<unsigned int>(f2bf(v[1])) << 16);
+            w.y = static_cast<unsigned int>(f2bf(v[2])) | (static_cast<unsigned int>(f2bf(v[3])) << 16);
+            *reinterpret_cast<uint2 *>(q) = w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (i < valid) q[i] = f2bf(v[i]);
+        }
+    }
+};
+
+// Element index of vector j (0..kVecPerThread-1) of this thread inside a tile:
+// consecutive threads touch consecutive 4-element vectors (coalesced).
+__device__ __forceinline__ int tile_elem(int j) { return (j * kThreads + threadIdx.x) * kVec; }
+
+__device__ __forceinline__ int clamp_valid(long long rem, int e) {
+    long long v = rem - e;
+    return v >= 4 ? 4 : (v <= 0 ? 0 : static_cast<int>(v));
+}
+
+// End-of-kernel protocol: the last CTA to finish runs `last()`.
+template <typename F>
+__device__ __forceinline__ void last_cta(Pad *pad, F last) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned int prev = atomicAdd(&pad->done_ctr, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence();
+            pad->done_ctr = 0;
+            last();
+        }
+    }
+}
+
+}  // namespace bf

@@ -1,0 +1,513 @@
+// exchange.cu -- the partial-averaging hot path on sm_100a.
+//
+// exchange_kernel: ONE persistent, cooperative launch per call that fuses
+//   Eq. 4 local update (ATC)      x_half = x - lr*g          (registers)
+//   publish + signal                      wire(x_half) -> own IPC slot, release flag
+//   neighbour exchange (Eq. 5 / Eq. 9)    acquire peers' flags, 128-bit loads over
+//                                         NVLink (other GPU) or L2 (same GPU)
+//   weighted combine + store              y = w_ii x_half + sum_j w_ij wire_j (fp32 FMA)
+// tile by tile (kTile elements per flag), so HBM traffic, NVLink traffic and
+// the wait for the slowest neighbour overlap across the CTAs of the grid.
+//
+// Deadlock freedom: all CTAs are co-resident (cooperative launch), every CTA
+// walks its items in increasing tile order and publishes tile t before it
+// waits for anybody's tile t, and grid >= local agents; every wait is bounded
+// by the context timeout.  WAR safety: slots are double-buffered by epoch
+// parity and a writer overwrites parity (e&1) only after every process has
+// reported (done_from) that it finished reading epoch e-2.
+#include <cooperative_groups.h>
+#include <cuda_bf16.h>
+
+#include "dev_common.cuh"
+
+namespace bf {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ unsigned long long *ready_ptr(const Geometry &g, unsigned long long off,
+                                                         int stride, int agent, int t) {
+    return at<unsigned long long>(g.peer_base[agent / g.k], off) +
+           static_cast<long long>(agent % g.k) * stride + t;
+}
+
+// Wait until every process finished reading epoch e-2 (so parity e&1 is free).
+__device__ __forceinline__ bool war_wait(const Geometry &g, unsigned long long e) {
+    bool ok = true;
+    if (g.nprocs > 1 && e > 2 && threadIdx.x < g.nprocs)
+        ok = spin_ge(g, &pad_of(g, g.me)->done_from[threadIdx.x], e - 2);
+    return __syncthreads_and(ok);
+}
+
+// Broadcast "this process finished reading epoch e" to every process.
+__device__ __forceinline__ void publish_done(const Geometry &g, unsigned long long e) {
+    for (int q = 0; q < g.nprocs; ++q) st_release_sys(&pad_of(g, q)->done_from[g.me], e);
+}
+
+// --------------------------------------------------------------------------
+// Source resolution for one call: fills the shared table of every local agent.
+//   static   : coefficients from the host's W row (Eq. 5)
+//   schedule : one-peer exp-2 from the device round counter (R5)
+//   dynamic  : declared r (Eq. 11) times the senders' s (Eq. 10) read from their
+//              descriptors; push-only receivers discover their sources there;
+//              topology check on mismatches.
+struct SharedTab {
+    float self_w[kMaxK];
+    float coef[kMaxK][kMaxN];
+    unsigned char src[kMaxK][kMaxN];
+    int nsrc[kMaxK];
+};
+
+__device__ bool resolve_sources(const ExchParams &p, unsigned long long e, SharedTab &st) {
+    const Geometry &g = p.geo;
+    const int k = g.k;
+    const int parity = static_cast<int>(e & 1);
+    bool ok = true;
+    if (p.wmode == kWStatic) {
+        for (int a = threadIdx.x; a < k; a += blockDim.x) {
+            st.self_w[a] = p.tab.self_w[a];
+            st.nsrc[a] = p.tab.nsrc[a];
+            for (int q = 0; q < p.tab.nsrc[a]; ++q) {
+                st.src[a][q] = p.tab.src[a][q];
+                st.coef[a][q] = p.tab.coef[a][q];
+            }
+        }
+    } else if (p.wmode == kWSchedule) {
+        const unsigned long long round = *reinterpret_cast<volatile unsigned long long *>(
+            &pad_of(g, g.me)->round);
+        int tau = 0;
+        while ((1 << tau) < g.n) ++tau;
+        for (int a = threadIdx.x; a < k; a += blockDim.x) {
+            const int gid = g.me * k + a;
+            if (tau == 0) {
+                st.self_w[a] = 1.f;
+                st.nsrc[a] = 0;
+            } else {
+                const int off = 1 << static_cast<int>(round % tau);
+                st.self_w[a] = 0.5f;
+                st.nsrc[a] = 1;
+                st.src[a][0] = static_cast<unsigned char>(((gid - off) % g.n + g.n) % g.n);
+                st.coef[a][0] = 0.5f;
+            }
+        }
+    } else {
+        // one warp per local agent; lanes scan candidate senders j
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int nwarps = blockDim.x >> 5;
+        for (int a = warp; a < k; a += nwarps) {
+            const int gid = g.me * k + a;
+            const bool has_src = p.dyn.has_src[a];
+            int total = 0;
+            for (int j0 = 0; j0 < g.n; j0 += 32) {
+                const int j = j0 + lane;
+                bool include = false;
+                float c = 0.f;
+                if (j < g.n && j != gid) {
+                    int qdecl = -1;
+                    if (has_src)
+                        for (int q = 0; q < p.tab.nsrc[a]; ++q)
+                            if (p.tab.src[a][q] == j) qdecl = q;
+                    const bool need = !has_src || qdecl >= 0 || p.check;
+                    if (need) {
+                        const Desc *d = &pad_of(g, j / k)->desc[j % k][parity];
+                        if (!spin_ge(g, &d->epoch, e)) {
+                            ok = false;
+                        } else {
+                            const unsigned long long mask =
+                                *reinterpret_cast<const volatile unsigned long long *>(&d->dstmask);
+                            const unsigned long long hd =
+                                *reinterpret_cast<const volatile unsigned long long *>(&d->has_dst);
+                            const bool to_me = (mask >> gid) & 1ull;
+                            const float s = to_me ? *reinterpret_cast<const volatile float *>(&d->s[gid]) : 1.f;
+                            if (has_src) {
+                                if (qdecl >= 0) {
+                                    include = true;
+                                    c = p.tab.coef[a][qdecl] * s;            // r_ij * s_ij (R1)
+                                    if (p.check && hd && !to_me) ok = false;  // sender never sends to me
+                                } else if (to_me && p.check) {
+                                    ok = false;                               // unlisted pusher
+                                }
+                            } else if (to_me) {
+                                include = true;                               // push-only: r = 1
+                                c = s;
+                            }
+                        }
+                    }
+                }
+                const unsigned int bal = __ballot_sync(0xffffffffu, include);
+                if (include) {
+                    const int pos = total + __popc(bal & ((1u << lane) - 1u));
+                    st.src[a][pos] = static_cast<unsigned char>(j);
+                    st.coef[a][pos] = c;
+                }
+                total += __popc(bal);
+            }
+            if (lane == 0) {
+                st.nsrc[a] = total;
+                st.self_w[a] = p.tab.self_w[a];
+            }
+        }
+        if (!__all_sync(0xffffffffu, ok) && lane == 0) {
+            const unsigned int code =
+                *reinterpret_cast<volatile unsigned int *>(&pad_of(g, g.me)->abort);
+            if (!code) abort_all(g, BF_ERR_TOPOLOGY);
+        }
+    }
+    return __syncthreads_and(ok);
+}
+
+// Block 0 writes the descriptors of the local agents for this epoch.
+__device__ void write_descriptors(const ExchParams &p, unsigned long long e) {
+    const Geometry &g = p.geo;
+    const int parity = static_cast<int>(e & 1);
+    if (blockIdx.x != 0) return;
+    for (int a = threadIdx.x; a < g.k; a += blockDim.x) {
+        Desc *d = &pad_of(g, g.me)->desc[a][parity];
+        unsigned long long mask = 0;
+        for (int q = 0; q < p.dyn.ndst[a]; ++q) {
+            const int j = p.dyn.dst[a][q];
+            mask |= 1ull << j;
+            d->s[j] = p.dyn.s[a][q];
+        }
+        d->dstmask = mask;
+        d->has_dst = p.dyn.has_dst[a];
+        st_release_sys(&d->epoch, e);
+    }
+}
+
+template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
+__global__ void __launch_bounds__(kThreads, 2) exchange_kernel(const __grid_constant__ ExchParams p) {
+    __shared__ SharedTab st;
+    const Geometry &g = p.geo;
+    Pad *pad = pad_of(g, g.me);
+    if (*reinterpret_cast<volatile unsigned int *>(&pad->abort)) return;
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
+    const int parity = static_cast<int>(e & 1);
+
+    if (!war_wait(g, e)) return;
+    if (p.wmode == kWDynamic) write_descriptors(p, e);
+    if (!resolve_sources(p, e, st)) return;
+
+    const bool vec = g.vec_ok != 0;
+    const long long count = g.count;
+    const int k = g.k;
+    const long long items = static_cast<long long>(k) * g.T;
+    __shared__ int s_fail;
+    if (threadIdx.x == 0) s_fail = 0;
+
+    for (long long w = blockIdx.x; w < items; w += gridDim.x) {
+        const int t = static_cast<int>(w / k);
+        const int a = static_cast<int>(w % k);
+        const long long base = static_cast<long long>(t) * kTile;
+        const long long rem = count - base;
+
+        // ---- Eq. 4 local update (ATC) or plain input (neighbor_allreduce) ----
+        float xh[kVecPerThread][4];
+        const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(a) * count + base;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+            Vec4<XT>::load(xr + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
+        if constexpr (HAS_G) {
+            const GT *gr = static_cast<const GT *>(p.g) + static_cast<long long>(a) * count + base;
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j) {
+                float gv[4];
+                Vec4<GT>::load(gr + tile_elem(j), gv, clamp_valid(rem, tile_elem(j)), vec);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
+            }
+        }
+
+        // ---- publish the wire copy into this agent's slot, release flag ----
+        WT *mine = at<WT>(g.peer_base[g.me], p.slot_off + a * p.slot_agent_stride +
+                                                 parity * p.slot_parity_stride) + base;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+            Vec4<WT>::store(mine + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            st_release_sys(ready_ptr(g, p.ready_off, p.ready_stride, g.me * k + a, t), e);
+
+        // ---- wait for the in-neighbours' tile t ----
+        const int ns = st.nsrc[a];
+        if (threadIdx.x < ns) {
+            if (!spin_ge(g, ready_ptr(g, p.ready_off, p.ready_stride, st.src[a][threadIdx.x], t), e))
+                s_fail = 1;
+        }
+        __syncthreads();
+        if (s_fail) return;
+
+        // ---- Eq. 5 / Eq. 9 weighted combine in fp32 ----
+        float acc[kVecPerThread][4];
+        const float cs = st.self_w[a];
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[j][i] = cs * xh[j][i];
+        for (int q = 0; q < ns; ++q) {
+            const int src = st.src[a][q];
+            const float c = st.coef[a][q];
+            const WT *sp = at<const WT>(g.peer_base[src / k],
+                                        p.slot_off + (src % k) * p.slot_agent_stride +
+                                            parity * p.slot_parity_stride) + base;
+            float v[kVecPerThread][4];
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+                Vec4<WT>::load_cg(sp + tile_elem(j), v[j], clamp_valid(rem, tile_elem(j)), vec);
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(c, v[j][i], acc[j][i]);
+        }
+
+        // ---- store (cast) ----
+        YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+            Vec4<YT>::store(yr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+        if (p.shadow) {
+            bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base;
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+                Vec4<bf16>::store(sr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+        }
+    }
+
+    last_cta(pad, [&] {
+        pad->epoch = e;
+        if (p.wmode == kWSchedule) pad->round = pad->round + 1;
+        publish_done(g, e);
+    });
+}
+
+// --------------------------------------------------------------------------
+// Hierarchical neighbour allreduce: leader-free, sliced.
+//   A: publish x tile t -> slot, flag
+//   B: agent (m,l) averages slice l over its machine's L agents (1/L, R12)
+//   C: agent (m,l) combines slice l with the machine neighbours' slice l (W_M)
+//   D: every agent gathers all slices of its machine's result
+// Every CTA finishes a stage before starting the next, and a stage only waits
+// on the previous stage, so co-resident CTAs cannot deadlock.
+template <typename XT>
+__global__ void __launch_bounds__(kThreads, 2) hier_kernel(const __grid_constant__ HierParams p) {
+    const Geometry &g = p.geo;
+    Pad *pad = pad_of(g, g.me);
+    if (*reinterpret_cast<volatile unsigned int *>(&pad->abort)) return;
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
+    const int parity = static_cast<int>(e & 1);
+    if (!war_wait(g, e)) return;
+    __shared__ int s_fail;
+    if (threadIdx.x == 0) s_fail = 0;
+    __syncthreads();
+
+    const bool vec = g.vec_ok != 0;
+    const long long count = g.count;
+    const int k = g.k, L = p.L, TS = p.TS;
+    auto slotA = [&](int agent) {
+        return at<const XT>(g.peer_base[agent / k], p.slot_off + (agent % k) * p.slot_agent_stride +
+                                                          parity * p.slot_parity_stride);
+    };
+    auto bufB = [&](int agent) {
+        return at<float>(g.peer_base[agent / k], p.b_off + (agent % k) * p.bc_agent_stride +
+                                                      parity * p.bc_parity_stride);
+    };
+    auto bufC = [&](int agent) {
+        return at<float>(g.peer_base[agent / k], p.c_off + (agent % k) * p.bc_agent_stride +
+                                                      parity * p.bc_parity_stride);
+    };
+    auto wait_all = [&](const unsigned long long *flag) {
+        if (!spin_ge(g, flag, e)) s_fail = 1;
+    };
+
+    // ---- stage A ----
+    const long long itemsA = static_cast<long long>(k) * g.T;
+    for (long long w = blockIdx.x; w < itemsA; w += gridDim.x) {
+        const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(a) * count + base;
+        XT *mine = const_cast<XT *>(slotA(g.me * k + a)) + base;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+            float v[4];
+            const int vl = clamp_valid(rem, tile_elem(j));
+            Vec4<XT>::load(xr + tile_elem(j), v, vl, vec);
+            Vec4<XT>::store(mine + tile_elem(j), v, vl, vec);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_sys(ready_ptr(g, p.ready_off, p.ready_stride, g.me * k + a, t), e);
+    }
+
+    // ---- stage B: slice average over the machine ----
+    const long long itemsS = static_cast<long long>(k) * TS;
+    for (long long w = blockIdx.x; w < itemsS; w += gridDim.x) {
+        const int tt = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        const int gid = g.me * k + a, m = gid / L, l = gid % L;
+        const int t = l * TS + tt;
+        if (t >= g.T) continue;
+        if (threadIdx.x < L) wait_all(ready_ptr(g, p.ready_off, p.ready_stride, m * L + threadIdx.x, t));
+        __syncthreads();
+        if (s_fail) return;
+        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        float acc[kVecPerThread][4] = {};
+        for (int lp = 0; lp < L; ++lp) {
+            const XT *sp = slotA(m * L + lp) + base;
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j) {
+                float v[4];
+                Vec4<XT>::load_cg(sp + tile_elem(j), v, clamp_valid(rem, tile_elem(j)), vec);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[j][i] += v[i];
+            }
+        }
+        const float invL = 1.0f / static_cast<float>(L);
+        float *bo = bufB(gid) + static_cast<long long>(tt) * kTile;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[j][i] *= invL;
+            Vec4<float>::store(bo + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), true);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_sys(ready_ptr(g, p.fb_off, p.ready_stride, gid, tt), e);
+    }
+
+    // ---- stage C: machine-level combine of the slice ----
+    for (long long w = blockIdx.x; w < itemsS; w += gridDim.x) {
+        const int tt = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        const int gid = g.me * k + a, l = gid % L;
+        const int t = l * TS + tt;
+        if (t >= g.T) continue;
+        const int ns = p.mtab.nsrc[a];
+        if (threadIdx.x < ns)
+            wait_all(ready_ptr(g, p.fb_off, p.ready_stride, p.mtab.src[a][threadIdx.x] * L + l, tt));
+        __syncthreads();
+        if (s_fail) return;
+        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        float acc[kVecPerThread][4];
+        const float *own = bufB(gid) + static_cast<long long>(tt) * kTile;
+        const float cs = p.mtab.self_w[a];
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+            Vec4<float>::load_cg(own + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), true);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[j][i] *= cs;
+        }
+        for (int q = 0; q < ns; ++q) {
+            const float *sp = bufB(p.mtab.src[a][q] * L + l) + static_cast<long long>(tt) * kTile;
+            const float c = p.mtab.coef[a][q];
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j) {
+                float v[4];
+                Vec4<float>::load_cg(sp + tile_elem(j), v, clamp_valid(rem, tile_elem(j)), true);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(c, v[i], acc[j][i]);
+            }
+        }
+        float *co = bufC(gid) + static_cast<long long>(tt) * kTile;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+            Vec4<float>::store(co + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), true);
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_sys(ready_ptr(g, p.fc_off, p.ready_stride, gid, tt), e);
+    }
+
+    // ---- stage D: gather the machine result ----
+    for (long long w = blockIdx.x; w < itemsA; w += gridDim.x) {
+        const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        const int gid = g.me * k + a, m = gid / L;
+        const int lo = t / TS, tt = t - lo * TS;
+        const int owner = m * L + lo;
+        if (threadIdx.x == 0) wait_all(ready_ptr(g, p.fc_off, p.ready_stride, owner, tt));
+        __syncthreads();
+        if (s_fail) return;
+        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        const float *cp = bufC(owner) + static_cast<long long>(tt) * kTile;
+        XT *yr = static_cast<XT *>(p.y) + static_cast<long long>(a) * count + base;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+            float v[4];
+            const int vl = clamp_valid(rem, tile_elem(j));
+            Vec4<float>::load_cg(cp + tile_elem(j), v, vl, true);
+            Vec4<XT>::store(yr + tile_elem(j), v, vl, vec);
+        }
+    }
+
+    last_cta(pad, [&] {
+        pad->epoch = e;
+        publish_done(g, e);
+    });
+}
+
+// --------------------------------------------------------------------------
+// Device barrier over all processes (P:580 bf.barrier()).
+__global__ void barrier_kernel(const __grid_constant__ Geometry g, unsigned long long epoch) {
+    Pad *pad = pad_of(g, g.me);
+    if (threadIdx.x < g.nprocs) st_release_sys(&pad_of(g, threadIdx.x)->bar_from[g.me], epoch);
+    if (threadIdx.x < g.nprocs) spin_ge(g, &pad->bar_from[threadIdx.x], epoch);
+}
+
+__global__ void set_u64_kernel(unsigned long long *dst, unsigned long long v) { *dst = v; }
+
+// --------------------------------------------------------------------------
+int max_coresident(const void *func, int threads, size_t smem) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem);
+    return per_sm * sms;
+}
+
+template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
+static cudaError_t launch_exch_t(const ExchParams &p, int grid, cudaStream_t s) {
+    auto fn = exchange_kernel<XT, GT, WT, YT, HAS_G>;
+    const int maxg = max_coresident(reinterpret_cast<const void *>(fn), kThreads, 0);
+    if (grid <= 0 || grid > maxg) grid = maxg;
+    const long long items = static_cast<long long>(p.geo.k) * p.geo.T;
+    if (grid > items) grid = static_cast<int>(items < p.geo.k ? p.geo.k : items);
+    if (grid < 1) grid = 1;
+    void *args[] = {const_cast<ExchParams *>(&p)};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(kThreads),
+                                       args, 0, s);
+}
+
+cudaError_t launch_exchange(const ExchParams &p, int x_kind, int g_kind, int wire_kind, int y_kind,
+                            int has_g, int grid, cudaStream_t s) {
+    // neighbor_allreduce: x = wire = y dtype
+    if (!has_g) {
+        if (x_kind == 0 && wire_kind == 0 && y_kind == 0)
+            return launch_exch_t<float, float, float, float, false>(p, grid, s);
+        if (x_kind == 1 && wire_kind == 1 && y_kind == 1)
+            return launch_exch_t<bf16, bf16, bf16, bf16, false>(p, grid, s);
+        return cudaErrorInvalidValue;
+    }
+    // ATC: fp32 master x and y
+    if (x_kind != 0 || y_kind != 0) return cudaErrorInvalidValue;
+    if (g_kind == 0 && wire_kind == 0) return launch_exch_t<float, float, float, float, true>(p, grid, s);
+    if (g_kind == 0 && wire_kind == 1) return launch_exch_t<float, float, bf16, float, true>(p, grid, s);
+    if (g_kind == 1 && wire_kind == 0) return launch_exch_t<float, bf16, float, float, true>(p, grid, s);
+    if (g_kind == 1 && wire_kind == 1) return launch_exch_t<float, bf16, bf16, float, true>(p, grid, s);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_hier(const HierParams &p, int x_kind, int grid, cudaStream_t s) {
+    const void *fn = x_kind == 0 ? reinterpret_cast<const void *>(hier_kernel<float>)
+                                 : reinterpret_cast<const void *>(hier_kernel<bf16>);
+    const int maxg = max_coresident(fn, kThreads, 0);
+    if (grid <= 0 || grid > maxg) grid = maxg;
+    const long long items = static_cast<long long>(p.geo.k) * p.geo.T;
+    if (grid > items) grid = static_cast<int>(items < p.geo.k ? p.geo.k : items);
+    if (grid < 1) grid = 1;
+    void *args[] = {const_cast<HierParams *>(&p)};
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, s);
+}
+
+cudaError_t launch_barrier(const Geometry &geo, unsigned long long epoch, cudaStream_t s) {
+    barrier_kernel<<<1, 32, 0, s>>>(geo, epoch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_u64(unsigned long long *dst, unsigned long long v, cudaStream_t s) {
+    set_u64_kernel<<<1, 1, 0, s>>>(dst, v);
+    return cudaGetLastError();
+}
+
+}  // namespace bf

@@ -1,0 +1,1014 @@
+// runtime.cu -- host runtime behind the C ABI (include/bluefog_b200.h):
+// context and symmetric heap, CUDA-IPC bootstrap, topology / weight manager
+// (P:334-382), argument validation (P:381 footnote), schedules,
+// window registry, and the launchers of the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "bf_internal.h"
+
+using namespace bf;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+bf_status fail(bf_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+#define CU(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t _e = (call);                                                               \
+        if (_e != cudaSuccess)                                                                 \
+            return fail(BF_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), \
+                        __FILE__, __LINE__);                                                   \
+    } while (0)
+
+constexpr uint32_t kBlobMagic = 0xBF0B200u;
+
+struct Blob {
+    uint32_t magic;
+    int proc, nprocs, k;
+    uint64_t heap_bytes;
+    cudaIpcMemHandle_t handle;
+};
+
+struct WinSide {
+    std::vector<int> in, out;   // ascending global ranks
+};
+
+struct Window {
+    std::string name;
+    void *x = nullptr;
+    size_t count = 0;
+    int dtype = 0, with_p = 0, zero_init = 0;
+    int maxdin = 1, maxdout = 1;
+    std::vector<WinSide> side;  // per global agent
+    WinParams base{};           // offsets filled at creation
+    size_t alloc_begin = 0, alloc_end = 0;
+};
+
+}  // namespace
+
+struct bf_ctx {
+    int proc = 0, nprocs = 1, k = 1, n = 1, device = 0;
+    size_t heap_bytes = 0, heap_used = 0;
+    char *heap = nullptr;
+    unsigned long long peer_base[kMaxP] = {};
+    char *peer_opened[kMaxP] = {};
+    bool connected = false;
+    bool poisoned = false;
+    bf_status fault = BF_OK;
+    volatile unsigned int *h_err = nullptr;   // host view
+    unsigned int *d_err = nullptr;            // device view of the same word
+    unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
+    std::vector<double> W;                    // n*n
+    int machine_L = 0, n_machines = 0;
+    std::vector<double> WM;
+    int sched_kind = 0;
+    int topo_check = 1;
+    // exchange region
+    size_t exch_cap = 0;                      // bytes per agent per parity
+    unsigned long long slot_off = 0, ready_off = 0;
+    int ready_stride = 0;
+    // hierarchical region
+    bool hier_ready = false;
+    unsigned long long b_off = 0, c_off = 0, fb_off = 0, fc_off = 0, bc_agent_stride = 0, bc_parity_stride = 0;
+    // staging for host pointers
+    void *stage_x = nullptr, *stage_g = nullptr;
+    size_t stage_x_bytes = 0, stage_g_bytes = 0;
+    std::map<std::string, Window> windows;
+    unsigned long long bar_epoch = 0;
+    unsigned long long launches = 0;
+};
+
+namespace {
+
+bf_status check_ctx(bf_ctx *c, bool need_connected = true) {
+    if (!c) return fail(BF_ERR_ARG, "null context");
+    if (c->poisoned) return fail(BF_ERR_STATE, "context poisoned by an earlier device fault (%d)", c->fault);
+    if (c->h_err && *c->h_err) {
+        c->poisoned = true;
+        c->fault = static_cast<bf_status>(*c->h_err);
+        return fail(BF_ERR_STATE, "device fault %d latched (timeout or topology mismatch)", c->fault);
+    }
+    if (need_connected && !c->connected) return fail(BF_ERR_STATE, "bf_connect_peers has not been called");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != c->device) cudaSetDevice(c->device);
+    return BF_OK;
+}
+
+bf_status heap_alloc(bf_ctx *c, size_t bytes, unsigned long long *off) {
+    size_t start = (c->heap_used + kAlign - 1) / kAlign * kAlign;
+    bytes = (bytes + kAlign - 1) / kAlign * kAlign;
+    if (start + bytes > c->heap_bytes)
+        return fail(BF_ERR_NOMEM, "symmetric heap exhausted: need %zu more bytes (heap %zu, used %zu)", bytes,
+                    c->heap_bytes, c->heap_used);
+    CU(cudaMemset(c->heap + start, 0, bytes));
+    c->heap_used = start + bytes;
+    *off = start;
+    return BF_OK;
+}
+
+Geometry make_geo(bf_ctx *c, size_t count) {
+    Geometry g{};
+    g.k = c->k;
+    g.n = c->n;
+    g.me = c->proc;
+    g.nprocs = c->nprocs;
+    g.count = static_cast<long long>(count);
+    g.T = static_cast<int>((count + kTile - 1) / kTile);
+    g.vec_ok = 0;
+    g.timeout_ns = c->timeout_ns;
+    for (int q = 0; q < kMaxP; ++q) g.peer_base[q] = c->peer_base[q];
+    g.host_err = reinterpret_cast<volatile unsigned int *>(c->d_err);
+    return g;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
+    if (c->exch_cap >= bytes_per_agent && c->exch_cap) return BF_OK;
+    if (c->exch_cap)
+        return fail(BF_ERR_NOMEM,
+                    "message of %zu bytes per agent exceeds the reserved exchange capacity %zu; call "
+                    "bf_reserve with the largest size first",
+                    bytes_per_agent, c->exch_cap);
+    size_t tile_bytes = static_cast<size_t>(kTile) * 4;
+    size_t cap = (bytes_per_agent + tile_bytes - 1) / tile_bytes * tile_bytes;
+    if (cap == 0) cap = tile_bytes;
+    unsigned long long slot_off, ready_off;
+    bf_status s = heap_alloc(c, static_cast<size_t>(c->k) * 2 * cap, &slot_off);
+    if (s) return s;
+    const int tmax = static_cast<int>(cap / (static_cast<size_t>(kTile) * 2));
+    s = heap_alloc(c, static_cast<size_t>(c->k) * tmax * 8, &ready_off);
+    if (s) return s;
+    c->exch_cap = cap;
+    c->slot_off = slot_off;
+    c->ready_off = ready_off;
+    c->ready_stride = tmax;
+    return BF_OK;
+}
+
+bool is_finite_w(double v) { return std::isfinite(v); }
+
+// Validate one local view against P:381's four configurations.
+bf_status validate_view(const bf_ctx *c, int gid, const bf_weights &w, bool allow_src, bool allow_dst,
+                        int n_ranks) {
+    const bool has_self = !std::isnan(w.self_weight);
+    const bool has_src = w.n_src >= 0, has_dst = w.n_dst >= 0;
+    if (!has_self)
+        return fail(BF_ERR_ARG, "agent %d: self_weight is required with src/dst weights (P:381 footnote)", gid);
+    if (!has_src && !has_dst)
+        return fail(BF_ERR_ARG, "agent %d: self_weight alone is not one of the four valid configurations (P:381)",
+                    gid);
+    if (has_src && !allow_src) return fail(BF_ERR_ARG, "agent %d: src_weights not accepted here", gid);
+    if (has_dst && !allow_dst) return fail(BF_ERR_ARG, "agent %d: dst_weights not accepted here", gid);
+    if (!is_finite_w(w.self_weight)) return fail(BF_ERR_ARG, "agent %d: non-finite self_weight", gid);
+    if (w.n_src > kMaxS || w.n_dst > kMaxS)
+        return fail(BF_ERR_UNSUPPORTED, "agent %d: more than %d declared neighbours", gid, kMaxS);
+    for (int pass = 0; pass < 2; ++pass) {
+        const int nn = pass ? w.n_dst : w.n_src;
+        const int *r = pass ? w.dst_ranks : w.src_ranks;
+        const double *v = pass ? w.dst_weights : w.src_weights;
+        if (nn > 0 && (!r || !v)) return fail(BF_ERR_ARG, "agent %d: null rank/weight array", gid);
+        for (int q = 0; q < nn; ++q) {
+            if (r[q] < 0 || r[q] >= n_ranks) return fail(BF_ERR_ARG, "agent %d: rank %d out of range", gid, r[q]);
+            if (r[q] == gid) return fail(BF_ERR_ARG, "agent %d: self rank in %s list", gid, pass ? "dst" : "src");
+            if (!is_finite_w(v[q])) return fail(BF_ERR_ARG, "agent %d: non-finite weight for rank %d", gid, r[q]);
+            for (int q2 = 0; q2 < q; ++q2)
+                if (r[q2] == r[q]) return fail(BF_ERR_ARG, "agent %d: duplicate rank %d", gid, r[q]);
+        }
+    }
+    (void)c;
+    return BF_OK;
+}
+
+// Static coefficients of local agent a from the global W (Eq. 5), sources in
+// (i - j) mod n order.
+bf_status static_row(const bf_ctx *c, int a, SrcTab &tab) {
+    const int gid = c->proc * c->k + a, n = c->n;
+    tab.self_w[a] = static_cast<float>(c->W[static_cast<size_t>(gid) * n + gid]);
+    int cnt = 0;
+    for (int d = 1; d < n; ++d) {
+        const int j = ((gid - d) % n + n) % n;
+        const double w = c->W[static_cast<size_t>(gid) * n + j];
+        if (w == 0.0) continue;
+        if (cnt >= kMaxS)
+            return fail(BF_ERR_UNSUPPORTED, "agent %d has more than %d in-neighbours in the static topology", gid,
+                        kMaxS);
+        tab.src[a][cnt] = static_cast<unsigned char>(j);
+        tab.coef[a][cnt] = static_cast<float>(w);
+        ++cnt;
+    }
+    tab.nsrc[a] = static_cast<unsigned char>(cnt);
+    return BF_OK;
+}
+
+bf_status fill_weights(bf_ctx *c, const bf_weights *weights, ExchParams &p) {
+    memset(&p.tab, 0, sizeof(p.tab));
+    memset(&p.dyn, 0, sizeof(p.dyn));
+    p.check = c->topo_check;
+    if (!weights) {
+        if (c->sched_kind == 1) {
+            p.wmode = kWSchedule;
+            return BF_OK;
+        }
+        p.wmode = kWStatic;
+        for (int a = 0; a < c->k; ++a) {
+            bf_status s = static_row(c, a, p.tab);
+            if (s) return s;
+        }
+        return BF_OK;
+    }
+    p.wmode = kWDynamic;
+    for (int a = 0; a < c->k; ++a) {
+        const int gid = c->proc * c->k + a;
+        const bf_weights &w = weights[a];
+        bf_status s = validate_view(c, gid, w, true, true, c->n);
+        if (s) return s;
+        p.tab.self_w[a] = static_cast<float>(w.self_weight);
+        p.dyn.has_src[a] = w.n_src >= 0;
+        p.dyn.has_dst[a] = w.n_dst >= 0;
+        if (w.n_src > 0) {
+            for (int q = 0; q < w.n_src; ++q) {
+                p.tab.src[a][q] = static_cast<unsigned char>(w.src_ranks[q]);
+                p.tab.coef[a][q] = static_cast<float>(w.src_weights[q]);
+            }
+            p.tab.nsrc[a] = static_cast<unsigned char>(w.n_src);
+        }
+        if (w.n_dst > 0) {
+            for (int q = 0; q < w.n_dst; ++q) {
+                p.dyn.dst[a][q] = static_cast<unsigned char>(w.dst_ranks[q]);
+                p.dyn.s[a][q] = static_cast<float>(w.dst_weights[q]);
+            }
+            p.dyn.ndst[a] = static_cast<unsigned char>(w.n_dst);
+        }
+    }
+    return BF_OK;
+}
+
+bool is_host_ptr(const void *p) {
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeUnregistered;
+}
+
+bf_status ensure_stage(void **buf, size_t *have, size_t need) {
+    if (*have >= need) return BF_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *have = 0;
+    CU(cudaMalloc(buf, need));
+    *have = need;
+    return BF_OK;
+}
+
+std::vector<int> in_list(const bf_ctx *c, int i) {
+    std::vector<int> v;
+    for (int j = 0; j < c->n; ++j)
+        if (j != i && c->W[static_cast<size_t>(i) * c->n + j] != 0.0) v.push_back(j);
+    return v;
+}
+std::vector<int> out_list(const bf_ctx *c, int i) {
+    std::vector<int> v;
+    for (int j = 0; j < c->n; ++j)
+        if (j != i && c->W[static_cast<size_t>(j) * c->n + i] != 0.0) v.push_back(j);
+    return v;
+}
+
+int ceil_log2(int n) {
+    int t = 0;
+    while ((1 << t) < n) ++t;
+    return t;
+}
+
+void topology_fill(int kind, int n, uint64_t k, double *W) {
+    std::fill(W, W + static_cast<size_t>(n) * n, 0.0);
+    if (n == 1) {
+        W[0] = 1.0;
+        return;
+    }
+    if (kind == 0) {                       // ring
+        if (n == 2) {
+            for (int q = 0; q < 4; ++q) W[q] = 0.5;
+            return;
+        }
+        for (int i = 0; i < n; ++i)
+            for (int d : {-1, 0, 1}) W[static_cast<size_t>(i) * n + ((i + d) % n + n) % n] = 1.0 / 3.0;
+    } else if (kind == 1) {                // exponential-2 (R4)
+        int deg = 0;
+        for (int off = 1; off <= n - 1; off *= 2) ++deg;
+        for (int i = 0; i < n; ++i) {
+            W[static_cast<size_t>(i) * n + i] = 1.0 / (deg + 1);
+            for (int off = 1; off <= n - 1; off *= 2)
+                W[static_cast<size_t>(i) * n + ((i - off) % n + n) % n] += 1.0 / (deg + 1);
+        }
+    } else if (kind == 2) {                // fully connected
+        for (size_t q = 0; q < static_cast<size_t>(n) * n; ++q) W[q] = 1.0 / n;
+    } else {                               // one-peer exp-2 at round k (R5)
+        const int off = 1 << static_cast<int>(k % static_cast<uint64_t>(ceil_log2(n)));
+        for (int i = 0; i < n; ++i) {
+            W[static_cast<size_t>(i) * n + i] = 0.5;
+            W[static_cast<size_t>(i) * n + ((i - off) % n + n) % n] += 0.5;
+        }
+    }
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char *bf_last_error(void) { return g_last_error.c_str(); }
+
+const char *bf_status_string(bf_status s) {
+    switch (s) {
+        case BF_OK: return "BF_OK";
+        case BF_ERR_ARG: return "BF_ERR_ARG";
+        case BF_ERR_STATE: return "BF_ERR_STATE";
+        case BF_ERR_TOPOLOGY: return "BF_ERR_TOPOLOGY";
+        case BF_ERR_CUDA: return "BF_ERR_CUDA";
+        case BF_ERR_TIMEOUT: return "BF_ERR_TIMEOUT";
+        case BF_ERR_NOMEM: return "BF_ERR_NOMEM";
+        case BF_ERR_UNSUPPORTED: return "BF_ERR_UNSUPPORTED";
+        case BF_ERR_WINDOW: return "BF_ERR_WINDOW";
+    }
+    return "BF_ERR_UNKNOWN";
+}
+
+size_t bf_ipc_blob_size(void) { return sizeof(Blob); }
+
+bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_device, size_t heap_bytes,
+                  bf_ctx **out) {
+    if (!out) return fail(BF_ERR_ARG, "null out");
+    *out = nullptr;
+    if (n_procs < 1 || n_procs > kMaxP) return fail(BF_ERR_UNSUPPORTED, "n_procs must be in [1, %d]", kMaxP);
+    if (proc_rank < 0 || proc_rank >= n_procs) return fail(BF_ERR_ARG, "proc_rank out of range");
+    if (agents_per_proc < 1 || agents_per_proc > kMaxK)
+        return fail(BF_ERR_UNSUPPORTED, "agents_per_proc must be in [1, %d]", kMaxK);
+    if (static_cast<long long>(n_procs) * agents_per_proc > kMaxN)
+        return fail(BF_ERR_UNSUPPORTED, "at most %d agents", kMaxN);
+    if (heap_bytes < kPadBytes + (1u << 20)) return fail(BF_ERR_ARG, "heap_bytes too small");
+    CU(cudaSetDevice(cuda_device));
+    int coop = 0;
+    CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cuda_device));
+    if (!coop) return fail(BF_ERR_UNSUPPORTED, "device does not support cooperative launch");
+    bf_ctx *c = new bf_ctx();
+    c->proc = proc_rank;
+    c->nprocs = n_procs;
+    c->k = agents_per_proc;
+    c->n = n_procs * agents_per_proc;
+    c->device = cuda_device;
+    c->heap_bytes = heap_bytes;
+    if (const char *t = getenv("BF_TIMEOUT_MS")) c->timeout_ns = strtoull(t, nullptr, 10) * 1000000ull;
+    cudaError_t e = cudaMalloc(&c->heap, heap_bytes);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(BF_ERR_NOMEM, "cudaMalloc(%zu) failed: %s", heap_bytes, cudaGetErrorString(e));
+    }
+    cudaMemset(c->heap, 0, kPadBytes);
+    c->heap_used = kPadBytes;
+    void *h = nullptr;
+    e = cudaHostAlloc(&h, 64, cudaHostAllocMapped);
+    if (e != cudaSuccess) {
+        cudaFree(c->heap);
+        delete c;
+        return fail(BF_ERR_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(e));
+    }
+    memset(h, 0, 64);
+    c->h_err = static_cast<volatile unsigned int *>(h);
+    cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->d_err), h, 0);
+    c->W.assign(static_cast<size_t>(c->n) * c->n, 1.0 / c->n);   // default: fully connected (R15)
+    c->peer_base[proc_rank] = reinterpret_cast<unsigned long long>(c->heap);
+    cudaDeviceSynchronize();
+    *out = c;
+    return BF_OK;
+}
+
+bf_status bf_get_ipc_blob(bf_ctx *c, void *blob, size_t *len) {
+    bf_status s = check_ctx(c, false);
+    if (s) return s;
+    if (!blob || !len || *len < sizeof(Blob)) return fail(BF_ERR_ARG, "blob buffer too small");
+    Blob b{};
+    b.magic = kBlobMagic;
+    b.proc = c->proc;
+    b.nprocs = c->nprocs;
+    b.k = c->k;
+    b.heap_bytes = c->heap_bytes;
+    if (c->nprocs > 1) CU(cudaIpcGetMemHandle(&b.handle, c->heap));
+    memcpy(blob, &b, sizeof(Blob));
+    *len = sizeof(Blob);
+    return BF_OK;
+}
+
+bf_status bf_connect_peers(bf_ctx *c, const void *blobs, size_t blob_len) {
+    bf_status s = check_ctx(c, false);
+    if (s) return s;
+    if (c->connected) return fail(BF_ERR_STATE, "already connected");
+    if (c->nprocs > 1) {
+        if (!blobs || blob_len < sizeof(Blob)) return fail(BF_ERR_ARG, "blobs required for n_procs > 1");
+        for (int q = 0; q < c->nprocs; ++q) {
+            Blob b;
+            memcpy(&b, static_cast<const char *>(blobs) + q * blob_len, sizeof(Blob));
+            if (b.magic != kBlobMagic || b.proc != q || b.nprocs != c->nprocs || b.k != c->k ||
+                b.heap_bytes != c->heap_bytes)
+                return fail(BF_ERR_ARG, "blob %d inconsistent (magic/proc/nprocs/agents/heap mismatch)", q);
+            if (q == c->proc) continue;
+            void *ptr = nullptr;
+            CU(cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess));
+            c->peer_opened[q] = static_cast<char *>(ptr);
+            c->peer_base[q] = reinterpret_cast<unsigned long long>(ptr);
+        }
+    }
+    c->connected = true;
+    return bf_barrier(c, nullptr) == BF_OK ? (cudaDeviceSynchronize() == cudaSuccess ? BF_OK
+                                                                                      : fail(BF_ERR_CUDA, "sync"))
+                                           : BF_ERR_TIMEOUT;
+}
+
+bf_status bf_finalize(bf_ctx *c) {
+    if (!c) return BF_OK;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (int q = 0; q < kMaxP; ++q)
+        if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer_opened[q]);
+    if (c->heap) cudaFree(c->heap);
+    if (c->stage_x) cudaFree(c->stage_x);
+    if (c->stage_g) cudaFree(c->stage_g);
+    if (c->h_err) cudaFreeHost(const_cast<unsigned int *>(c->h_err));
+    delete c;
+    return BF_OK;
+}
+
+int bf_size(const bf_ctx *c) { return c ? c->n : 0; }
+int bf_rank(const bf_ctx *c) { return c ? c->proc * c->k : -1; }
+int bf_local_agents(const bf_ctx *c) { return c ? c->k : 0; }
+uint64_t bf_kernel_launches(const bf_ctx *c) { return c ? c->launches : 0; }
+
+// ---- topology ------------------------------------------------------------------
+bf_status bf_topology_matrix(int kind, int n, uint64_t k, double *W) {
+    if (!W || n < 1 || n > kMaxN || kind < 0 || kind > 3) return fail(BF_ERR_ARG, "bad topology request");
+    topology_fill(kind, n, k, W);
+    return BF_OK;
+}
+
+bf_status bf_schedule_one_peer_exp2(int n, int rank, uint64_t round, int *src, int *dst) {
+    if (n < 1 || rank < 0 || rank >= n || !src || !dst) return fail(BF_ERR_ARG, "bad schedule request");
+    const int tau = ceil_log2(n);
+    if (tau == 0) {
+        *src = *dst = -1;
+        return BF_OK;
+    }
+    const int off = 1 << static_cast<int>(round % static_cast<uint64_t>(tau));
+    *src = ((rank - off) % n + n) % n;
+    *dst = (rank + off) % n;
+    return BF_OK;
+}
+
+bf_status bf_set_topology(bf_ctx *c, int n, const double *W) {
+    bf_status s = check_ctx(c, false);
+    if (s) return s;
+    if (n != c->n || !W) return fail(BF_ERR_ARG, "topology size %d != %d agents", n, c->n);
+    for (size_t q = 0; q < static_cast<size_t>(n) * n; ++q)
+        if (!is_finite_w(W[q])) return fail(BF_ERR_ARG, "non-finite weight in W");
+    for (int i = 0; i < n; ++i) {
+        int d = 0;
+        for (int j = 0; j < n; ++j) d += (j != i && W[static_cast<size_t>(i) * n + j] != 0.0);
+        if (d > kMaxS) return fail(BF_ERR_UNSUPPORTED, "agent %d has %d > %d in-neighbours", i, d, kMaxS);
+    }
+    c->W.assign(W, W + static_cast<size_t>(n) * n);
+    c->sched_kind = 0;
+    return BF_OK;
+}
+
+bf_status bf_set_machine_topology(bf_ctx *c, int local_size, int n_machines, const double *WM) {
+    bf_status s = check_ctx(c, false);
+    if (s) return s;
+    if (local_size < 1 || n_machines < 1 || local_size * n_machines != c->n || !WM)
+        return fail(BF_ERR_ARG, "machines (%d x %d) must tile the %d agents homogeneously (P:668)", n_machines,
+                    local_size, c->n);
+    for (int m = 0; m < n_machines; ++m) {
+        int d = 0;
+        for (int q = 0; q < n_machines; ++q) {
+            if (!is_finite_w(WM[m * n_machines + q])) return fail(BF_ERR_ARG, "non-finite machine weight");
+            d += (q != m && WM[m * n_machines + q] != 0.0);
+        }
+        if (d > kMaxS) return fail(BF_ERR_UNSUPPORTED, "machine %d has too many neighbours", m);
+    }
+    c->machine_L = local_size;
+    c->n_machines = n_machines;
+    c->WM.assign(WM, WM + static_cast<size_t>(n_machines) * n_machines);
+    return BF_OK;
+}
+
+bf_status bf_in_neighbors(bf_ctx *c, int agent, int *ranks, int cap, int *n_out) {
+    if (!c || agent < 0 || agent >= c->n || !n_out) return fail(BF_ERR_ARG, "bad agent");
+    auto v = in_list(c, agent);
+    *n_out = static_cast<int>(v.size());
+    for (int q = 0; q < cap && q < *n_out; ++q) ranks[q] = v[q];
+    return BF_OK;
+}
+
+bf_status bf_out_neighbors(bf_ctx *c, int agent, int *ranks, int cap, int *n_out) {
+    if (!c || agent < 0 || agent >= c->n || !n_out) return fail(BF_ERR_ARG, "bad agent");
+    auto v = out_list(c, agent);
+    *n_out = static_cast<int>(v.size());
+    for (int q = 0; q < cap && q < *n_out; ++q) ranks[q] = v[q];
+    return BF_OK;
+}
+
+bf_status bf_set_dynamic_schedule(bf_ctx *c, int kind, uint64_t round0) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (kind != 0 && kind != 1) return fail(BF_ERR_ARG, "unknown schedule kind %d", kind);
+    c->sched_kind = kind;
+    if (kind == 1) {
+        Pad *pad = reinterpret_cast<Pad *>(c->heap);
+        CU(launch_set_u64(&pad->round, round0, nullptr));
+        c->launches++;
+        CU(cudaDeviceSynchronize());
+    }
+    return BF_OK;
+}
+
+bf_status bf_set_topology_check(bf_ctx *c, int enable) {
+    if (!c) return fail(BF_ERR_ARG, "null context");
+    c->topo_check = enable ? 1 : 0;
+    return BF_OK;
+}
+
+bf_status bf_reserve(bf_ctx *c, size_t bytes_per_agent) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    return ensure_exchange(c, bytes_per_agent);
+}
+
+// ---- hot path ---------------------------------------------------------------
+static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *y, void *shadow, size_t count,
+                                 int x_kind, int g_kind, int wire_kind, int y_kind, float lr,
+                                 const bf_weights *weights, cudaStream_t st) {
+    if (count == 0) return BF_OK;
+    if (count > (1ull << 40)) return fail(BF_ERR_ARG, "count too large");
+    ExchParams p;
+    memset(&p, 0, sizeof(p));
+    bf_status s = fill_weights(c, weights, p);
+    if (s) return s;
+    const size_t wire_es = wire_kind == 0 ? 4 : 2;
+    s = ensure_exchange(c, count * wire_es);
+    if (s) return s;
+    if ((count + kTile - 1) / kTile > static_cast<size_t>(c->ready_stride))
+        return fail(BF_ERR_NOMEM, "too many tiles for the reserved exchange region");
+    p.geo = make_geo(c, count);
+    p.geo.vec_ok = (count % 4 == 0) && aligned16(x) && aligned16(y) && (!g || aligned16(g)) &&
+                   (!shadow || aligned16(shadow));
+    p.x_kind = x_kind;
+    p.wire_kind = wire_kind;
+    p.y_kind = y_kind;
+    p.x = x;
+    p.g = g;
+    p.y = y;
+    p.shadow = shadow;
+    p.lr = lr;
+    p.slot_off = c->slot_off;
+    p.slot_agent_stride = 2 * c->exch_cap;
+    p.slot_parity_stride = c->exch_cap;
+    p.ready_off = c->ready_off;
+    p.ready_stride = c->ready_stride;
+    CU(launch_exchange(p, x_kind, g_kind, wire_kind, y_kind, g != nullptr, 0, st));
+    c->launches++;
+    return BF_OK;
+}
+
+bf_status bf_neighbor_allreduce(bf_ctx *c, const void *x, void *y, size_t count, bf_dtype dtype,
+                                const bf_weights *weights, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!x || !y) return fail(BF_ERR_ARG, "null tensor");
+    if (dtype != BF_FLOAT32 && dtype != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
+    return exchange_common(c, x, nullptr, y, nullptr, count, dtype, dtype, dtype, dtype, 0.f, weights,
+                           static_cast<cudaStream_t>(stream));
+}
+
+bf_status bf_atc_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, size_t count, float lr, bf_dtype wire,
+                      void *x_bf16_shadow, const bf_weights *weights, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!x || !g) return fail(BF_ERR_ARG, "null tensor");
+    if ((g_dtype != BF_FLOAT32 && g_dtype != BF_BFLOAT16) || (wire != BF_FLOAT32 && wire != BF_BFLOAT16))
+        return fail(BF_ERR_UNSUPPORTED, "dtype");
+    if (!std::isfinite(lr)) return fail(BF_ERR_ARG, "non-finite lr");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t rows = static_cast<size_t>(c->k) * count;
+    float *xd = x;
+    const void *gd = g;
+    const bool x_host = is_host_ptr(x), g_host = is_host_ptr(g);
+    if (x_host) {   // end-to-end path: stage the host tensors through device memory
+        s = ensure_stage(&c->stage_x, &c->stage_x_bytes, rows * 4);
+        if (s) return s;
+        CU(cudaMemcpyAsync(c->stage_x, x, rows * 4, cudaMemcpyHostToDevice, st));
+        xd = static_cast<float *>(c->stage_x);
+    }
+    if (g_host) {
+        const size_t gb = rows * (g_dtype == BF_FLOAT32 ? 4 : 2);
+        s = ensure_stage(&c->stage_g, &c->stage_g_bytes, gb);
+        if (s) return s;
+        CU(cudaMemcpyAsync(c->stage_g, g, gb, cudaMemcpyHostToDevice, st));
+        gd = c->stage_g;
+    }
+    s = exchange_common(c, xd, gd, xd, x_bf16_shadow, count, 0, g_dtype, wire, 0, lr, weights, st);
+    if (s) return s;
+    if (x_host) CU(cudaMemcpyAsync(x, c->stage_x, rows * 4, cudaMemcpyDeviceToHost, st));
+    return BF_OK;
+}
+
+bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, size_t count, bf_dtype dtype,
+                                             const bf_weights *machine_weights, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!x || !y) return fail(BF_ERR_ARG, "null tensor");
+    if (dtype != BF_FLOAT32 && dtype != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
+    if (!c->machine_L) return fail(BF_ERR_STATE, "bf_set_machine_topology has not been called");
+    if (count == 0) return BF_OK;
+    const int L = c->machine_L, NM = c->n_machines;
+    HierParams p;
+    memset(&p, 0, sizeof(p));
+    for (int a = 0; a < c->k; ++a) {
+        const int gid = c->proc * c->k + a, m = gid / L;
+        if (!machine_weights) {
+            p.mtab.self_w[a] = static_cast<float>(c->WM[static_cast<size_t>(m) * NM + m]);
+            int cnt = 0;
+            for (int d = 1; d < NM; ++d) {
+                const int q = ((m - d) % NM + NM) % NM;
+                const double w = c->WM[static_cast<size_t>(m) * NM + q];
+                if (w == 0.0) continue;
+                p.mtab.src[a][cnt] = static_cast<unsigned char>(q);
+                p.mtab.coef[a][cnt] = static_cast<float>(w);
+                ++cnt;
+            }
+            p.mtab.nsrc[a] = static_cast<unsigned char>(cnt);
+        } else {
+            const bf_weights &w = machine_weights[a];
+            s = validate_view(c, m, w, true, false, NM);
+            if (s) return s;
+            p.mtab.self_w[a] = static_cast<float>(w.self_weight);
+            for (int q = 0; q < w.n_src; ++q) {
+                p.mtab.src[a][q] = static_cast<unsigned char>(w.src_ranks[q]);
+                p.mtab.coef[a][q] = static_cast<float>(w.src_weights[q]);
+            }
+            p.mtab.nsrc[a] = static_cast<unsigned char>(w.n_src > 0 ? w.n_src : 0);
+        }
+    }
+    const size_t es = dtype == BF_FLOAT32 ? 4 : 2;
+    s = ensure_exchange(c, count * es);
+    if (s) return s;
+    if (!c->hier_ready) {
+        // fp32 slice buffers sized for the largest count the exchange region admits
+        const size_t max_elems = c->exch_cap / 2;
+        const size_t bytes = max_elems * 4;
+        unsigned long long off;
+        if ((s = heap_alloc(c, static_cast<size_t>(c->k) * 2 * bytes, &off))) return s;
+        c->b_off = off;
+        if ((s = heap_alloc(c, static_cast<size_t>(c->k) * 2 * bytes, &off))) return s;
+        c->c_off = off;
+        if ((s = heap_alloc(c, static_cast<size_t>(c->k) * c->ready_stride * 8, &off))) return s;
+        c->fb_off = off;
+        if ((s = heap_alloc(c, static_cast<size_t>(c->k) * c->ready_stride * 8, &off))) return s;
+        c->fc_off = off;
+        c->bc_agent_stride = 2 * bytes;
+        c->bc_parity_stride = bytes;
+        c->hier_ready = true;
+    }
+    p.geo = make_geo(c, count);
+    p.geo.vec_ok = (count % 4 == 0) && aligned16(x) && aligned16(y);
+    p.x = x;
+    p.y = y;
+    p.L = L;
+    p.TS = (p.geo.T + L - 1) / L;
+    p.slot_off = c->slot_off;
+    p.slot_agent_stride = 2 * c->exch_cap;
+    p.slot_parity_stride = c->exch_cap;
+    p.ready_off = c->ready_off;
+    p.ready_stride = c->ready_stride;
+    p.b_off = c->b_off;
+    p.c_off = c->c_off;
+    p.fb_off = c->fb_off;
+    p.fc_off = c->fc_off;
+    p.bc_agent_stride = c->bc_agent_stride;
+    p.bc_parity_stride = c->bc_parity_stride;
+    CU(launch_hier(p, dtype, 0, static_cast<cudaStream_t>(stream)));
+    c->launches++;
+    return BF_OK;
+}
+
+// ---- windows ----------------------------------------------------------------
+static Window *find_win(bf_ctx *c, const char *name) {
+    if (!name) return nullptr;
+    auto it = c->windows.find(name);
+    return it == c->windows.end() ? nullptr : &it->second;
+}
+
+bf_status bf_win_create(bf_ctx *c, const char *name, void *x, size_t count, bf_dtype dtype, int zero_init,
+                        int with_p) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!name || !*name) return fail(BF_ERR_ARG, "window name required");
+    if (find_win(c, name)) return fail(BF_ERR_WINDOW, "window '%s' already exists", name);
+    if (!x || count == 0) return fail(BF_ERR_ARG, "window tensor must be non-empty");
+    if (dtype != BF_FLOAT32 && dtype != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
+    Window w;
+    w.name = name;
+    w.x = x;
+    w.count = count;
+    w.dtype = dtype;
+    w.with_p = with_p ? 1 : 0;
+    w.zero_init = zero_init ? 1 : 0;
+    w.side.resize(c->n);
+    for (int i = 0; i < c->n; ++i) {
+        w.side[i].in = in_list(c, i);
+        w.side[i].out = out_list(c, i);
+        w.maxdin = std::max<int>(w.maxdin, static_cast<int>(w.side[i].in.size()));
+        w.maxdout = std::max<int>(w.maxdout, static_cast<int>(w.side[i].out.size()));
+    }
+    if (w.maxdin > kMaxS || w.maxdout > kMaxS) return fail(BF_ERR_UNSUPPORTED, "window degree > %d", kMaxS);
+    const size_t es = dtype == BF_FLOAT32 ? 4 : 2;
+    const size_t K = c->k, DI = w.maxdin, DO = w.maxdout;
+    WinParams &b = w.base;
+    memset(&b, 0, sizeof(b));
+    w.alloc_begin = c->heap_used;
+    unsigned long long off;
+#define WALLOC(field, bytes)                           \
+    do {                                               \
+        if ((s = heap_alloc(c, (bytes), &off))) {      \
+            c->heap_used = w.alloc_begin;              \
+            return s;                                  \
+        }                                              \
+        b.field = off;                                 \
+    } while (0)
+    WALLOC(slot_off, K * DI * 2 * count * es);
+    WALLOC(pslot_off, K * DI * 2 * 8);
+    WALLOC(version_off, K * DI * 8);
+    WALLOC(consumed_off, K * DO * 8);
+    WALLOC(outbox_off, K * DO * count * 4);
+    WALLOC(pout_off, K * DO * 8);
+    WALLOC(delivered_off, K * DO * 8);
+    WALLOC(obvalid_off, K * DO * 4);
+    WALLOC(conslocal_off, K * DI * 8);
+    WALLOC(p_off, K * 8);
+    WALLOC(dec_off, K * DO * 8);
+    WALLOC(snap_off, K * DI * 16);
+#undef WALLOC
+    w.alloc_end = c->heap_used;
+    b.maxdin = w.maxdin;
+    b.maxdout = w.maxdout;
+    b.x = x;
+    b.out = x;
+    b.dtype = dtype;
+    b.with_p = w.with_p;
+    std::vector<double> ones(K, 1.0);
+    CU(cudaMemcpy(c->heap + b.p_off, ones.data(), K * 8, cudaMemcpyHostToDevice));
+    if (!zero_init) {
+        // slots start as a copy of the local tensor, in half 1 (R10)
+        for (int a = 0; a < c->k; ++a) {
+            const int gid = c->proc * c->k + a;
+            for (size_t q = 0; q < w.side[gid].in.size(); ++q)
+                CU(cudaMemcpy(c->heap + b.slot_off + ((a * DI + q) * 2 + 1) * count * es,
+                              static_cast<char *>(x) + a * count * es, count * es, cudaMemcpyDeviceToDevice));
+        }
+    }
+    CU(cudaDeviceSynchronize());
+    c->windows[name] = w;
+    s = bf_barrier(c, nullptr);
+    if (s) return s;
+    CU(cudaDeviceSynchronize());
+    return BF_OK;
+}
+
+bf_status bf_win_free(bf_ctx *c, const char *name) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    Window *w = find_win(c, name);
+    if (!w) return fail(BF_ERR_WINDOW, "unknown window '%s'", name ? name : "(null)");
+    CU(cudaDeviceSynchronize());
+    s = bf_barrier(c, nullptr);
+    if (s) return s;
+    CU(cudaDeviceSynchronize());
+    if (w->alloc_end == c->heap_used) c->heap_used = w->alloc_begin;   // LIFO release
+    c->windows.erase(name);
+    return BF_OK;
+}
+
+static bf_status win_setup(bf_ctx *c, Window *w, uint64_t agent_mask, WinParams &p) {
+    p = w->base;
+    p.geo = make_geo(c, w->count);
+    p.geo.vec_ok = (w->count % 4 == 0) && aligned16(w->x);
+    const uint64_t all = c->k >= 64 ? ~0ull : ((1ull << c->k) - 1);
+    p.agent_mask = agent_mask ? (agent_mask & all) : all;
+    return BF_OK;
+}
+
+static bf_status win_push(bf_ctx *c, const char *name, const bf_weights *weights, uint64_t agent_mask,
+                          int overwrite, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    Window *w = find_win(c, name);
+    if (!w) return fail(BF_ERR_WINDOW, "unknown window '%s'", name ? name : "(null)");
+    WinParams p;
+    win_setup(c, w, agent_mask, p);
+    p.overwrite = overwrite;
+    p.ef = (w->dtype == BF_BFLOAT16 && !overwrite) ? 1 : 0;
+    for (int a = 0; a < c->k; ++a) {
+        const int gid = c->proc * c->k + a;
+        const auto &outs = w->side[gid].out;
+        if (!weights) {   // Listing 3: 1/(outdegree+1) to every out-neighbour
+            const double wt = 1.0 / (outs.size() + 1.0);
+            p.self_w[a] = static_cast<float>(wt);
+            p.self_wd[a] = wt;
+            for (size_t q = 0; q < outs.size(); ++q) {
+                const int j = outs[q];
+                const auto &ins = w->side[j].in;
+                p.out_q[a][q] = static_cast<unsigned char>(q);
+                p.out_dst[a][q] = static_cast<unsigned char>(j);
+                p.out_qin[a][q] = static_cast<unsigned char>(std::find(ins.begin(), ins.end(), gid) - ins.begin());
+                p.out_s[a][q] = static_cast<float>(wt);
+                p.out_sd[a][q] = wt;
+            }
+            p.nout[a] = static_cast<unsigned char>(outs.size());
+            continue;
+        }
+        const bf_weights &v = weights[a];
+        s = validate_view(c, gid, v, false, true, c->n);
+        if (s) return s;
+        p.self_w[a] = static_cast<float>(v.self_weight);
+        p.self_wd[a] = v.self_weight;
+        for (int q = 0; q < v.n_dst; ++q) {
+            const int j = v.dst_ranks[q];
+            auto it = std::find(outs.begin(), outs.end(), j);
+            if (it == outs.end())
+                return fail(BF_ERR_WINDOW, "agent %d: dst %d is not an out-neighbour at window creation (P:398)",
+                            gid, j);
+            const auto &ins = w->side[j].in;
+            p.out_q[a][q] = static_cast<unsigned char>(it - outs.begin());
+            p.out_dst[a][q] = static_cast<unsigned char>(j);
+            p.out_qin[a][q] = static_cast<unsigned char>(std::find(ins.begin(), ins.end(), gid) - ins.begin());
+            p.out_s[a][q] = static_cast<float>(v.dst_weights[q]);
+            p.out_sd[a][q] = v.dst_weights[q];
+        }
+        p.nout[a] = static_cast<unsigned char>(v.n_dst > 0 ? v.n_dst : 0);
+    }
+    CU(launch_win_push(p, 0, static_cast<cudaStream_t>(stream)));
+    c->launches += 2;
+    return BF_OK;
+}
+
+bf_status bf_win_put(bf_ctx *c, const char *name, const bf_weights *weights, uint64_t agent_mask, void *stream) {
+    return win_push(c, name, weights, agent_mask, 1, stream);
+}
+
+bf_status bf_win_accumulate(bf_ctx *c, const char *name, const bf_weights *weights, int require_mutex,
+                            uint64_t agent_mask, void *stream) {
+    (void)require_mutex;   // the versioned SPSC slot protocol is the mutex
+    return win_push(c, name, weights, agent_mask, 0, stream);
+}
+
+static bf_status win_pull(bf_ctx *c, const char *name, const bf_weights *weights, void *out, uint64_t agent_mask,
+                          int update, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    Window *w = find_win(c, name);
+    if (!w) return fail(BF_ERR_WINDOW, "unknown window '%s'", name ? name : "(null)");
+    WinParams p;
+    win_setup(c, w, agent_mask, p);
+    if (out) {
+        p.out = out;
+        p.geo.vec_ok = p.geo.vec_ok && aligned16(out);
+    }
+    for (int b = 0; b < c->k; ++b) {
+        const int gid = c->proc * c->k + b;
+        const auto &ins = w->side[gid].in;
+        p.nin[b] = static_cast<unsigned char>(ins.size());
+        for (size_t q = 0; q < ins.size(); ++q) {
+            const int src = ins[q];
+            const auto &outs = w->side[src].out;
+            p.in_src[b][q] = static_cast<unsigned char>(src);
+            p.in_qout[b][q] = static_cast<unsigned char>(std::find(outs.begin(), outs.end(), gid) - outs.begin());
+            p.in_r[b][q] = static_cast<float>(1.0 / (ins.size() + 1.0));
+        }
+        p.self_w[b] = static_cast<float>(1.0 / (ins.size() + 1.0));
+        if (update && weights) {
+            const bf_weights &v = weights[b];
+            s = validate_view(c, gid, v, true, false, c->n);
+            if (s) return s;
+            p.self_w[b] = static_cast<float>(v.self_weight);
+            for (size_t q = 0; q < ins.size(); ++q) p.in_r[b][q] = 0.f;
+            for (int q = 0; q < v.n_src; ++q) {
+                auto it = std::find(ins.begin(), ins.end(), v.src_ranks[q]);
+                if (it == ins.end())
+                    return fail(BF_ERR_WINDOW, "agent %d: src %d is not an in-neighbour at window creation", gid,
+                                v.src_ranks[q]);
+                p.in_r[b][it - ins.begin()] = static_cast<float>(v.src_weights[q]);
+            }
+        }
+    }
+    CU(launch_win_collect(p, update, 0, static_cast<cudaStream_t>(stream)));
+    c->launches += 2;
+    return BF_OK;
+}
+
+bf_status bf_win_update(bf_ctx *c, const char *name, const bf_weights *weights, void *out, uint64_t agent_mask,
+                        void *stream) {
+    return win_pull(c, name, weights, out, agent_mask, 1, stream);
+}
+
+bf_status bf_win_update_then_collect(bf_ctx *c, const char *name, uint64_t agent_mask, void *stream) {
+    return win_pull(c, name, nullptr, nullptr, agent_mask, 0, stream);
+}
+
+bf_status bf_win_get_p(bf_ctx *c, const char *name, double *p_host, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    Window *w = find_win(c, name);
+    if (!w) return fail(BF_ERR_WINDOW, "unknown window '%s'", name ? name : "(null)");
+    if (!p_host) return fail(BF_ERR_ARG, "null p_host");
+    CU(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    CU(cudaMemcpy(p_host, c->heap + w->base.p_off, c->k * 8, cudaMemcpyDeviceToHost));
+    return BF_OK;
+}
+
+bf_status bf_win_counters(bf_ctx *c, const char *name, int dst_local, int src_rank, uint64_t *version,
+                          uint64_t *consumed) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    Window *w = find_win(c, name);
+    if (!w) return fail(BF_ERR_WINDOW, "unknown window '%s'", name ? name : "(null)");
+    if (dst_local < 0 || dst_local >= c->k || !version || !consumed) return fail(BF_ERR_ARG, "bad agent");
+    const auto &ins = w->side[c->proc * c->k + dst_local].in;
+    auto it = std::find(ins.begin(), ins.end(), src_rank);
+    if (it == ins.end()) return fail(BF_ERR_WINDOW, "rank %d is not an in-neighbour", src_rank);
+    const size_t ci = static_cast<size_t>(dst_local) * w->maxdin + (it - ins.begin());
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(version, c->heap + w->base.version_off + ci * 8, 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(consumed, c->heap + w->base.conslocal_off + ci * 8, 8, cudaMemcpyDeviceToHost));
+    return BF_OK;
+}
+
+long long bf_win_slot_offset(bf_ctx *c, const char *name, int agent, int src_rank) {
+    if (!c) return -1;
+    Window *w = find_win(c, name);
+    if (!w || agent < 0 || agent >= c->n) return -1;
+    const auto &ins = w->side[agent].in;
+    auto it = std::find(ins.begin(), ins.end(), src_rank);
+    if (it == ins.end()) return -1;
+    return static_cast<long long>(it - ins.begin()) * static_cast<long long>(w->count);
+}
+
+// ---- misc ---------------------------------------------------------------------
+bf_status bf_barrier(bf_ctx *c, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (c->nprocs == 1) return BF_OK;
+    Geometry g = make_geo(c, 0);
+    CU(launch_barrier(g, ++c->bar_epoch, static_cast<cudaStream_t>(stream)));
+    c->launches++;
+    return BF_OK;
+}
+
+bf_status bf_poll_error(bf_ctx *c) {
+    if (!c) return fail(BF_ERR_ARG, "null context");
+    if (c->h_err && *c->h_err) {
+        c->poisoned = true;
+        c->fault = static_cast<bf_status>(*c->h_err);
+    }
+    if (c->fault) return fail(c->fault, "latched device fault: %s", bf_status_string(c->fault));
+    return BF_OK;
+}
+
+bf_status bf_fill_uniform(void *dst, bf_dtype dtype, size_t count, uint64_t seed, uint64_t offset, float scale,
+                          void *stream) {
+    if (!dst && count) return fail(BF_ERR_ARG, "null dst");
+    if (dtype != BF_FLOAT32 && dtype != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
+    CU(launch_fill_uniform(dst, dtype, count, seed, offset, scale, static_cast<cudaStream_t>(stream)));
+    return BF_OK;
+}
+
+}  // extern "C"

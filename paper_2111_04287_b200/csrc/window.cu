@@ -1,0 +1,291 @@
+// window.cu -- one-sided windows for asynchronous push-sum
+// on sm_100a.
+//
+// Protocol (single producer / single consumer per slot, no remote
+// read-modify-write, no lock):
+//   producer i -> consumer j owns slot (j, q_in) in j's heap, two halves.
+//   payload m lands in half m&1 only if the consumer has consumed payload
+//   m-2 (consumed >= delivered-1); the producer then releases
+//   version = m+1 into j's heap.  Otherwise the payload stays in i's fp32
+//   outbox and later payloads accumulate onto it (sender-side accumulation).
+//   The consumer's collect sums the payloads consumed..version-1, then
+//   releases consumed = version into i's heap.
+// Decisions are snapshotted by a one-block kernel before the streaming kernel
+// so every CTA acts on the same decision.  Nothing here waits on another
+// agent, so these kernels can run on a single GPU for any number of agents.
+#include <cuda_bf16.h>
+
+#include "dev_common.cuh"
+
+namespace bf {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ unsigned long long esize(const WinParams &p) { return p.dtype == 0 ? 4 : 2; }
+
+__device__ __forceinline__ bool active(const WinParams &p, int a) {
+    return (p.agent_mask >> a) & 1ull;
+}
+
+// ---- push side ------------------------------------------------------------
+__global__ void win_push_decide(const __grid_constant__ WinParams p) {
+    const Geometry &g = p.geo;
+    const unsigned long long me = g.peer_base[g.me];
+    for (int idx = threadIdx.x; idx < g.k * kMaxS; idx += blockDim.x) {
+        const int a = idx / kMaxS, q = idx % kMaxS;
+        if (!active(p, a) || q >= p.nout[a]) continue;
+        const int qo = p.out_q[a][q];
+        const unsigned long long cons =
+            ld_acquire_sys(at<unsigned long long>(me, p.consumed_off) + a * p.maxdout + qo);
+        const unsigned long long dlv = at<unsigned long long>(me, p.delivered_off)[a * p.maxdout + qo];
+        const bool deliver = static_cast<long long>(cons) >= static_cast<long long>(dlv) - 1;
+        at<unsigned long long>(me, p.dec_off)[a * p.maxdout + qo] = deliver ? 1ull : 0ull;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) win_push_kernel(const __grid_constant__ WinParams p) {
+    const Geometry &g = p.geo;
+    const unsigned long long me = g.peer_base[g.me];
+    Pad *pad = pad_of(g, g.me);
+    const long long count = g.count;
+    const bool vec = g.vec_ok != 0;
+    const int k = g.k;
+    const unsigned long long *dec = at<unsigned long long>(me, p.dec_off);
+    const unsigned long long *dlv = at<unsigned long long>(me, p.delivered_off);
+    const unsigned int *obv = at<unsigned int>(me, p.obvalid_off);
+    const long long items = static_cast<long long>(k) * g.T;
+    for (long long w = blockIdx.x; w < items; w += gridDim.x) {
+        const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        if (!active(p, a)) continue;
+        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        T *xr = static_cast<T *>(p.x) + static_cast<long long>(a) * count + base;
+        float xv[kVecPerThread][4];
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+            Vec4<T>::load(xr + tile_elem(j), xv[j], clamp_valid(rem, tile_elem(j)), vec);
+        for (int q = 0; q < p.nout[a]; ++q) {
+            const int qo = p.out_q[a][q], dst = p.out_dst[a][q], qin = p.out_qin[a][q];
+            const float s = p.out_s[a][q];
+            const int ci = a * p.maxdout + qo;
+            const bool deliver = dec[ci] != 0;
+            const bool use_ob = obv[ci] != 0 && !p.overwrite;
+            float *ob = at<float>(me, p.outbox_off) + static_cast<long long>(ci) * count + base;
+            float pay[kVecPerThread][4];
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j) {
+                const int vl = clamp_valid(rem, tile_elem(j));
+                if (use_ob) Vec4<float>::load(ob + tile_elem(j), pay[j], vl, true);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) pay[j][i] = use_ob ? fmaf(s, xv[j][i], pay[j][i]) : s * xv[j][i];
+            }
+            if (deliver) {
+                const int half = static_cast<int>(dlv[ci] & 1ull);
+                T *slot = at<T>(g.peer_base[dst / k],
+                                p.slot_off + ((static_cast<unsigned long long>(dst % k) * p.maxdin + qin) * 2 + half) *
+                                                 count * esize(p)) + base;
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j) {
+                    const int vl = clamp_valid(rem, tile_elem(j));
+                    Vec4<T>::store(slot + tile_elem(j), pay[j], vl, vec);
+                    if (p.ef) {   // keep the wire rounding residual (bf16) in the outbox
+                        float r[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float wire = sizeof(T) == 2 ? bf2f(f2bf(pay[j][i])) : pay[j][i];
+                            r[i] = pay[j][i] - wire;
+                        }
+                        Vec4<float>::store(ob + tile_elem(j), r, vl, true);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j)
+                    Vec4<float>::store(ob + tile_elem(j), pay[j], clamp_valid(rem, tile_elem(j)), true);
+            }
+        }
+        const float sw = p.self_w[a];
+        if (sw != 1.0f) {
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) xv[j][i] *= sw;
+                Vec4<T>::store(xr + tile_elem(j), xv[j], clamp_valid(rem, tile_elem(j)), vec);
+            }
+        }
+    }
+
+    // last CTA: p lane, version release, control state
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned int prev = atomicAdd(&pad->done_ctr, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            pad->done_ctr = 0;
+            unsigned long long *dlvw = at<unsigned long long>(me, p.delivered_off);
+            unsigned int *obvw = at<unsigned int>(me, p.obvalid_off);
+            double *P = at<double>(me, p.p_off);
+            double *pout = at<double>(me, p.pout_off);
+            for (int a = 0; a < k; ++a) {
+                if (!active(p, a)) continue;
+                for (int q = 0; q < p.nout[a]; ++q) {
+                    const int qo = p.out_q[a][q], dst = p.out_dst[a][q], qin = p.out_qin[a][q];
+                    const int ci = a * p.maxdout + qo;
+                    const bool deliver = dec[ci] != 0;
+                    const bool use_ob = obvw[ci] != 0 && !p.overwrite;
+                    const double pv = (use_ob ? pout[ci] : 0.0) + p.out_sd[a][q] * P[a];
+                    if (deliver) {
+                        const unsigned long long m = dlvw[ci];
+                        const unsigned long long slot_idx =
+                            static_cast<unsigned long long>(dst % k) * p.maxdin + qin;
+                        if (p.with_p)
+                            at<double>(g.peer_base[dst / k], p.pslot_off)[slot_idx * 2 + (m & 1)] = pv;
+                        __threadfence_system();
+                        st_release_sys(at<unsigned long long>(g.peer_base[dst / k], p.version_off) + slot_idx,
+                                       m + 1);
+                        dlvw[ci] = m + 1;
+                        obvw[ci] = p.ef ? 1u : 0u;
+                        pout[ci] = 0.0;
+                    } else {
+                        pout[ci] = pv;
+                        obvw[ci] = 1u;
+                    }
+                }
+                P[a] *= p.self_wd[a];
+            }
+        }
+    }
+}
+
+// ---- consumer side ----------------------------------------------------------
+__global__ void win_collect_decide(const __grid_constant__ WinParams p) {
+    const Geometry &g = p.geo;
+    const unsigned long long me = g.peer_base[g.me];
+    for (int idx = threadIdx.x; idx < g.k * kMaxS; idx += blockDim.x) {
+        const int b = idx / kMaxS, q = idx % kMaxS;
+        if (!active(p, b) || q >= p.nin[b]) continue;
+        const int ci = b * p.maxdin + q;
+        const unsigned long long v = ld_acquire_sys(at<unsigned long long>(me, p.version_off) + ci);
+        const unsigned long long c = at<unsigned long long>(me, p.conslocal_off)[ci];
+        unsigned long long *snap = at<unsigned long long>(me, p.snap_off);
+        snap[ci * 2] = c;
+        snap[ci * 2 + 1] = v;
+    }
+}
+
+// update == 0: update_then_collect (x += sum of ready payloads, R9)
+// update == 1: win_update (out = self*x + sum r_j * latest payload, R10)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) win_collect_kernel(const __grid_constant__ WinParams p, int update) {
+    const Geometry &g = p.geo;
+    const unsigned long long me = g.peer_base[g.me];
+    Pad *pad = pad_of(g, g.me);
+    const long long count = g.count;
+    const bool vec = g.vec_ok != 0;
+    const int k = g.k;
+    const unsigned long long *snap = at<unsigned long long>(me, p.snap_off);
+    // per-CTA acquire of the producers' versions (orders the slot reads below)
+    for (int idx = threadIdx.x; idx < k * p.maxdin; idx += blockDim.x)
+        (void)ld_acquire_sys(at<unsigned long long>(me, p.version_off) + idx);
+    __syncthreads();
+    const long long items = static_cast<long long>(k) * g.T;
+    for (long long w = blockIdx.x; w < items; w += gridDim.x) {
+        const int t = static_cast<int>(w / k), b = static_cast<int>(w % k);
+        if (!active(p, b)) continue;
+        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        const T *xr = static_cast<const T *>(p.x) + static_cast<long long>(b) * count + base;
+        T *outr = static_cast<T *>(p.out) + static_cast<long long>(b) * count + base;
+        float acc[kVecPerThread][4];
+        const float sw = update ? p.self_w[b] : 1.0f;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+            Vec4<T>::load(xr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[j][i] *= sw;
+        }
+        for (int q = 0; q < p.nin[b]; ++q) {
+            const int ci = b * p.maxdin + q;
+            const unsigned long long c = snap[ci * 2], v = snap[ci * 2 + 1];
+            const float r = update ? p.in_r[b][q] : 1.0f;
+            // update: the latest complete payload v-1 (v == 0: the initial copy in half 1);
+            // collect: every delivered payload c..v-1.
+            const unsigned long long m_first = update ? v - 1 : c;
+            const unsigned long long m_end = update ? v : v;
+            for (unsigned long long m = m_first; update ? (m == m_first) : (m < m_end);
+                 m = update ? m_first + 1 : m + 1) {
+                const T *h = at<const T>(me, p.slot_off + (static_cast<unsigned long long>(ci) * 2 + (m & 1)) *
+                                                              count * esize(p)) + base;
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j) {
+                    float v4[4];
+                    Vec4<T>::load_cg(h + tile_elem(j), v4, clamp_valid(rem, tile_elem(j)), vec);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(r, v4[i], acc[j][i]);
+                }
+                if (update) break;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+            Vec4<T>::store(outr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+    }
+
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(&pad->done_ctr, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence();
+            pad->done_ctr = 0;
+            unsigned long long *cl = at<unsigned long long>(me, p.conslocal_off);
+            double *P = at<double>(me, p.p_off);
+            const double *ps = at<const double>(me, p.pslot_off);
+            for (int b = 0; b < k; ++b) {
+                if (!active(p, b)) continue;
+                for (int q = 0; q < p.nin[b]; ++q) {
+                    const int ci = b * p.maxdin + q;
+                    const unsigned long long c = snap[ci * 2], v = snap[ci * 2 + 1];
+                    if (!update && p.with_p)
+                        for (unsigned long long m = c; m < v; ++m) P[b] += ps[ci * 2 + (m & 1)];
+                    cl[ci] = v;
+                    const int src = p.in_src[b][q];
+                    st_release_sys(at<unsigned long long>(g.peer_base[src / k], p.consumed_off) +
+                                       (src % k) * p.maxdout + p.in_qout[b][q],
+                                   v);
+                }
+            }
+        }
+    }
+}
+
+static int stream_grid(long long items) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long g = static_cast<long long>(sms) * 4;
+    if (items < g) g = items;
+    return g < 1 ? 1 : static_cast<int>(g);
+}
+
+cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s) {
+    win_push_decide<<<1, 256, 0, s>>>(p);
+    if (grid <= 0) grid = stream_grid(static_cast<long long>(p.geo.k) * p.geo.T);
+    if (p.dtype == 0)
+        win_push_kernel<float><<<grid, kThreads, 0, s>>>(p);
+    else
+        win_push_kernel<bf16><<<grid, kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_win_collect(const WinParams &p, int update, int grid, cudaStream_t s) {
+    win_collect_decide<<<1, 256, 0, s>>>(p);
+    if (grid <= 0) grid = stream_grid(static_cast<long long>(p.geo.k) * p.geo.T);
+    if (p.dtype == 0)
+        win_collect_kernel<float><<<grid, kThreads, 0, s>>>(p, update);
+    else
+        win_collect_kernel<bf16><<<grid, kThreads, 0, s>>>(p, update);
+    return cudaGetLastError();
+}
+
+}  // namespace bf

@@ -1,0 +1,491 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Single GPU: n agents run as `agents_per_proc = n` virtual agents of one
+process; the exchange kernel is one cooperative launch over all of them, so
+the cross-agent waits are between co-resident CTAs of one kernel.
+Tolerance rule: |y - y_ref| <= tol * b elementwise,
+b = sum_j |w_ij| |x_j| (ATC: |x_j| + lr |g_j|), tol = 1e-6 fp32, 1e-2 bf16.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as ora
+import synthetic
+from bfutil import golden
+
+pytestmark = pytest.mark.gpu
+
+os.environ.setdefault("BF_TIMEOUT_MS", "5000")
+
+if torch.cuda.is_available():
+    import paper_2111_04287_b200 as bfp
+    from paper_2111_04287_b200 import BluefogError
+
+TOL = {torch.float32: 1e-6, torch.bfloat16: 1e-2}
+COUNTS = [1, 7, 4096, 4097, 3 * 4096 + 5, 100003]
+
+
+def _ctx(k, heap=1 << 28):
+    return bfp.Context(agents_per_proc=k, heap_bytes=heap, device=0)
+
+
+def _gpu(X, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32)).to(dtype).cuda()
+
+
+def _np(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def _inputs(n, count, dtype=torch.float32):
+    X = synthetic.agents_x0(n, count)
+    t = _gpu(X, dtype)
+    return t, _np(t)          # exact values the GPU holds (bf16-rounded if bf16)
+
+
+def assert_parity(y, ref, W, X, tol, extra=None):
+    b = np.abs(W) @ np.abs(X)
+    if extra is not None:
+        b = b + extra
+    err = np.abs(y - ref)
+    bad = err > tol * b + 1e-30
+    assert not bad.any(), f"max rel err {np.max(err / (b + 1e-30)):.3e} at {np.argwhere(bad)[:5].tolist()}"
+
+
+# ----------------------------------------------------------------- generator --
+def test_fill_uniform_matches_synthetic():
+    for dtype, scale in ((torch.float32, 1.0), (torch.float32, 2.0 ** -7), (torch.bfloat16, 1.0)):
+        t = torch.empty(100003, dtype=dtype, device="cuda")
+        bfp.Context.fill_uniform(t, seed=1234, offset=17, scale=scale)
+        ref = torch.from_numpy(synthetic.uniform(1234, 100003, scale=scale, offset=17)).to(dtype)
+        assert torch.equal(t.cpu(), ref)
+
+
+# ------------------------------------------------------ neighbor_allreduce ---
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("topo,n", [("ring", 4), ("exp2", 8), ("full", 5), ("exp2", 3), ("ring", 2), ("exp2", 16)])
+def test_nar_static(topo, n, dtype):
+    ctx = _ctx(n)
+    W = {"ring": ora.ring, "exp2": ora.exp2, "full": ora.full}[topo](n)
+    ctx.set_topology(W)
+    for count in COUNTS:
+        x, X = _inputs(n, count, dtype)
+        y = ctx.neighbor_allreduce(x)
+        torch.cuda.synchronize()
+        assert_parity(_np(y), ora.mix(W, X), W, X, TOL[dtype])
+    ctx.close()
+
+
+def test_nar_random_directed_and_inplace():
+    n = 6
+    rng = np.random.default_rng(1)
+    W = (rng.random((n, n)) < 0.5) * rng.uniform(-1, 1, (n, n))
+    np.fill_diagonal(W, rng.uniform(0.1, 1, n))
+    ctx = _ctx(n)
+    ctx.set_topology(W)
+    x, X = _inputs(n, 50001)
+    ctx.neighbor_allreduce(x, out=x)          # y aliases x
+    torch.cuda.synchronize()
+    assert_parity(_np(x), ora.mix(W, X), W, X, 1e-6)
+    ctx.close()
+
+
+def test_nar_default_topology_is_full_and_n1():
+    ctx = _ctx(4)
+    x = _gpu(np.array([[1.0], [2.0], [3.0], [4.0]]))
+    y = ctx.neighbor_allreduce(x)
+    torch.cuda.synchronize()
+    assert np.allclose(_np(y), golden("spec_scalar_examples.json")["full4_expected"], atol=1e-7)
+    ctx.close()
+    ctx1 = _ctx(1)
+    x, X = _inputs(1, 9999)
+    y = ctx1.neighbor_allreduce(x)
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(y), X)
+    ctx1.close()
+
+
+def _views(W, style):
+    n = W.shape[0]
+    sw, srcw, dstw = [], [], []
+    for i in range(n):
+        srcs = [j for j in range(n) if j != i and W[i, j] != 0]
+        dsts = [j for j in range(n) if j != i and W[j, i] != 0]
+        sw.append(W[i, i])
+        if style == "pull":
+            srcw.append({j: W[i, j] for j in srcs})
+            dstw.append(None)
+        elif style == "push":
+            srcw.append(None)
+            dstw.append({j: W[j, i] for j in dsts})
+        else:
+            srcw.append({j: 0.5 for j in srcs})
+            dstw.append({j: 2.0 * W[j, i] for j in dsts})
+    return sw, srcw, dstw
+
+
+@pytest.mark.parametrize("style", ["pull", "push", "pushpull"])
+def test_nar_dynamic_styles(style):
+    g = golden("fig2_neighbor_sets.json")
+    n = g["n"]
+    rng = np.random.default_rng(4)
+    W = np.eye(n)
+    for a, b in g["edges_1indexed"]:
+        W[b - 1, a - 1] = 1.0
+    W = W * rng.uniform(0.1, 1.0, W.shape)
+    sw, srcw, dstw = _views(W, style)
+    ctx = _ctx(n)
+    for count in (5, 8192, 40001):
+        x, X = _inputs(n, count)
+        y = ctx.neighbor_allreduce(x, self_weight=sw, src_weights=srcw, dst_weights=dstw)
+        torch.cuda.synchronize()
+        assert_parity(_np(y), ora.mix(W, X), W, X, 1e-6)
+    ctx.close()
+
+
+def test_nar_dynamic_time_varying_one_peer_push():
+    # per-call weights that change every iteration: one-peer push form
+    n = 8
+    ctx = _ctx(n)
+    x, X = _inputs(n, 20000)
+    for k in range(5):
+        dst = [{bfp.one_peer_exp2(n, i, k)[1]: 0.5} for i in range(n)]
+        x = ctx.neighbor_allreduce(x, self_weight=[0.5] * n, dst_weights=dst)
+        Wk = ora.one_peer_exp2(n, k)
+        torch.cuda.synchronize()
+        Y = _np(x)
+        assert_parity(Y, ora.mix(Wk, X), Wk, X, 1e-6)
+        X = Y
+    ctx.close()
+
+
+def test_nar_schedule_one_peer_exact_average():
+    n = 8
+    ctx = _ctx(n)
+    ctx.set_dynamic_schedule("one_peer_exp2", 0)
+    x, X0 = _inputs(n, 65537)
+    X = X0
+    for k in range(3):
+        x = ctx.neighbor_allreduce(x)
+        torch.cuda.synchronize()
+        Wk = ora.one_peer_exp2(n, k)
+        Y = _np(x)
+        assert_parity(Y, ora.mix(Wk, X), Wk, X, 1e-6)
+        X = Y
+    mean = X0.mean(axis=0)
+    assert np.abs(X - mean).max() <= 1e-6 * np.abs(X0).max()
+    ctx.close()
+
+
+# ---------------------------------------------------------------------- ATC ---
+@pytest.mark.parametrize("wire", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("gdt", [torch.float32, torch.bfloat16])
+def test_atc_step(wire, gdt):
+    n = 8
+    W = ora.exp2(n)
+    ctx = _ctx(n)
+    ctx.set_topology(W)
+    lr = 0.1
+    for count in (4096, 12345, 100000):
+        x, X = _inputs(n, count)
+        g = _gpu(synthetic.agents_grad(n, count, 3), gdt)
+        G = _np(g)
+        shadow = torch.empty(n, count, dtype=torch.bfloat16, device="cuda")
+        ctx.atc_step(x, g, lr, wire=wire, shadow=shadow)
+        torch.cuda.synchronize()
+        ref = ora.atc(W, X, G, lr, wire_bf16=(wire == torch.bfloat16))
+        extra = np.abs(W) @ (np.float32(lr) * np.abs(G))
+        assert_parity(_np(x), ref, W, X, TOL[wire], extra)
+        # the shadow is RNE(bf16) of the fp32 master
+        assert torch.equal(shadow.cpu(), x.cpu().to(torch.bfloat16))
+    ctx.close()
+
+
+def test_atc_one_peer_schedule_and_lr0():
+    n = 8
+    ctx = _ctx(n)
+    ctx.set_dynamic_schedule("one_peer_exp2", 0)
+    x, X = _inputs(n, 30000)
+    for k in range(4):
+        g = _gpu(synthetic.agents_grad(n, 30000, k))
+        G = _np(g)
+        ctx.atc_step(x, g, 0.05)
+        torch.cuda.synchronize()
+        Wk = ora.one_peer_exp2(n, k)
+        Y = _np(x)
+        assert_parity(Y, ora.atc(Wk, X, G, 0.05), Wk, X, 1e-6, np.abs(Wk) @ (0.05 * np.abs(G)))
+        X = Y
+    ctx.close()
+
+
+def test_atc_host_pointers_end_to_end():
+    n = 4
+    W = ora.ring(n)
+    ctx = _ctx(n)
+    ctx.set_topology(W)
+    X = synthetic.agents_x0(n, 10000)
+    G = synthetic.agents_grad(n, 10000, 0)
+    xh = torch.from_numpy(X.copy()).pin_memory()
+    gh = torch.from_numpy(G.copy()).pin_memory()
+    ctx.atc_step(xh, gh, 0.1)
+    torch.cuda.synchronize()
+    ref = ora.atc(W, X.astype(np.float64), G.astype(np.float64), 0.1)
+    assert_parity(xh.numpy().astype(np.float64), ref, W, X.astype(np.float64), 1e-6,
+                  np.abs(W) @ (0.1 * np.abs(G.astype(np.float64))))
+    ctx.close()
+
+
+def test_c1_consensus_ring4_20_iterations():
+    # C1: n=4 ring, fp32[4096], 20 iterations; chained per-step parity and the
+    # end state against the fp64 trajectory (normalised by ||X0||_inf)
+    n = 4
+    W = ora.ring(n)
+    ctx = _ctx(n)
+    ctx.set_topology(W)
+    x, X0 = _inputs(n, 4096)
+    X = X0
+    Xf = X0
+    for _ in range(20):
+        x = ctx.neighbor_allreduce(x)
+        torch.cuda.synchronize()
+        Y = _np(x)
+        assert_parity(Y, ora.mix(W, X), W, X, 1e-6)
+        X = Y
+        Xf = ora.mix(W, Xf)
+    assert np.abs(X - Xf).max() <= 1e-6 * np.abs(X0).max()
+    ctx.close()
+
+
+# --------------------------------------------------------- topology check ---
+def test_topology_check_mismatch_is_an_error_not_a_hang():
+    os.environ["BF_TIMEOUT_MS"] = "2000"
+    ctx = _ctx(2)
+    x, _ = _inputs(2, 1000)
+    # agent 0 pushes to 1; agent 1 declares no source
+    with pytest.raises(BluefogError):
+        ctx.neighbor_allreduce(x, self_weight=[0.5, 1.0], src_weights=[None, {}], dst_weights=[{1: 0.5}, {}])
+        torch.cuda.synchronize()
+        ctx.poll_error()
+    with pytest.raises(BluefogError) as e:
+        ctx.neighbor_allreduce(x)
+    assert e.value.name == "BF_ERR_STATE"
+    ctx.close()
+    os.environ["BF_TIMEOUT_MS"] = "5000"
+
+
+def test_invalid_configurations_rejected_on_host():
+    ctx = _ctx(2)
+    x, _ = _inputs(2, 100)
+    bad = [dict(self_weight=None, src_weights=[{1: 0.5}, {0: 0.5}]),          # no self weight
+           dict(self_weight=[0.5, 0.5]),                                       # self only
+           dict(self_weight=[0.5, 0.5], src_weights=[{0: 0.5}, {0: 0.5}]),     # self rank
+           dict(self_weight=[0.5, 0.5], src_weights=[{5: 0.5}, {0: 0.5}]),     # out of range
+           dict(self_weight=[float("nan"), 0.5], src_weights=[{1: 0.5}, {0: 0.5}])]
+    for kw in bad:
+        with pytest.raises(BluefogError) as e:
+            ctx.neighbor_allreduce(x, **kw)
+        assert e.value.name == "BF_ERR_ARG"
+    ctx.neighbor_allreduce(x)                    # context still healthy
+    torch.cuda.synchronize()
+    ctx.close()
+
+
+# ------------------------------------------------------------- hierarchical ---
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("nm,L", [(4, 2), (2, 4), (1, 8), (8, 1), (2, 2)])
+def test_hierarchical(nm, L, dtype):
+    n = nm * L
+    WM = ora.exp2(nm)
+    ctx = _ctx(n)
+    ctx.set_machine_topology(WM, L)
+    K = np.kron(WM, np.full((L, L), 1.0 / L))
+    for count in (3, 4096 * 3 + 1, 50000):
+        x, X = _inputs(n, count, dtype)
+        y = ctx.hierarchical_neighbor_allreduce(x)
+        torch.cuda.synchronize()
+        assert_parity(_np(y), ora.hier(WM, L, X), K, X, TOL[dtype])
+    ctx.close()
+
+
+def test_hierarchical_spec_example():
+    gd = golden("hier_2x2_example.json")
+    ctx = _ctx(4)
+    ctx.set_machine_topology(np.array(gd["machine_W"]), gd["local_size"])
+    x = _gpu(np.array(gd["inputs"]).reshape(4, 1))
+    y = ctx.hierarchical_neighbor_allreduce(x)
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(y).ravel(), np.array(gd["expected"]))
+    ctx.close()
+
+
+# ------------------------------------------------------------------ windows ---
+def _fig2_static():
+    g = golden("fig2_neighbor_sets.json")
+    W = np.eye(g["n"])
+    for a, b in g["edges_1indexed"]:
+        W[b - 1, a - 1] = 1.0
+    return W
+
+
+def test_window_slot_layout_p388():
+    gd = golden("window_layout_p388.json")
+    n = 6                                   # nodes 0..5, paper node ids used directly
+    W = np.eye(n)
+    for s in gd["in_neighbors"]:
+        W[gd["owner"], s] = 1.0
+    ctx = _ctx(n)
+    ctx.set_topology(W)
+    numel = int(np.prod(gd["shape"]))
+    x = torch.zeros(n, numel, device="cuda")
+    ctx.win_create(x, "w")
+    offs = [ctx.win_slot_offset("w", gd["owner"], s) for s in gd["slot_order"]]
+    assert offs == [0, numel]
+    assert numel * len(gd["in_neighbors"]) == gd["logical_elements"]
+    ctx.win_free("w")
+    ctx.close()
+
+
+def test_window_sync_pushsum_matches_oracle():
+    Wst = _fig2_static()
+    n = Wst.shape[0]
+    count = 9000
+    X0 = synthetic.agents_x0(n, count).astype(np.float64)
+    ctx = _ctx(n)
+    ctx.set_topology(Wst)
+    x = _gpu(X0)
+    ctx.win_create(x, "ps", zero_init=True, with_p=True)
+    ext = np.concatenate([X0, np.ones((n, 1))], axis=1)
+    win = ora.Window(Wst, ext, zero_init=True)
+    for _ in range(6):
+        ctx.win_accumulate("ps")                 # Listing 3 weights 1/(outdeg+1)
+        ctx.win_update_then_collect("ps")
+        for i in range(n):
+            outs = ora.out_neighbors(Wst, i)
+            w = 1.0 / (len(outs) + 1)
+            win.accumulate(i, w, {j: w for j in outs})
+        for i in range(n):
+            win.collect(i)
+    torch.cuda.synchronize()
+    ref = win.x()
+    assert np.abs(_np(x) - ref[:, :-1]).max() < 1e-5
+    assert np.allclose(ctx.win_p("ps"), ref[:, -1], rtol=0, atol=1e-12)
+    ctx.win_free("ps")
+    ctx.close()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_window_async_event_model(dtype):
+    # random per-agent interleaving of accumulate / collect (agent_mask selects
+    # the acting agent); the GPU follows the oracle's state machine event by event
+    Wst = _fig2_static()
+    n = Wst.shape[0]
+    count = 4099
+    ctx = _ctx(n)
+    ctx.set_topology(Wst)
+    x = _gpu(synthetic.agents_x0(n, count), dtype)
+    X0 = _np(x)
+    ctx.win_create(x, "a", zero_init=True, with_p=True)
+    win = ora.Window(Wst, np.concatenate([X0, np.ones((n, 1))], axis=1), zero_init=True)
+    rng = np.random.default_rng(7)
+    mass0 = X0.sum(axis=0)
+    for _ in range(150):
+        i = int(rng.integers(n))
+        if rng.random() < 0.5:
+            ctx.win_accumulate("a", agent_mask=1 << i)
+            outs = ora.out_neighbors(Wst, i)
+            w = 1.0 / (len(outs) + 1)
+            win.accumulate(i, w, {j: w for j in outs})
+        else:
+            ctx.win_update_then_collect("a", agent_mask=1 << i)
+            win.collect(i)
+    torch.cuda.synchronize()
+    for i in range(n):
+        for j in ora.out_neighbors(Wst, i):
+            v, c = ctx.win_counters("a", j, i)
+            assert (v, c) == win.counters(j, i)
+    ref = win.x()
+    assert np.allclose(ctx.win_p("a"), ref[:, -1], rtol=0, atol=1e-12)
+    tol = 3e-5 if dtype == torch.float32 else 2e-2
+    assert np.abs(_np(x) - ref[:, :-1]).max() < tol
+    # flush: every agent pushes its outbox and collects, twice -> mass conserved
+    for _ in range(3):
+        ctx.win_accumulate("a", self_weight=[1.0] * n, dst_weights=[{j: 0.0 for j in ora.out_neighbors(Wst, i)}
+                                                                   for i in range(n)])
+        ctx.win_update_then_collect("a")
+    torch.cuda.synchronize()
+    mass = _np(x).sum(axis=0)
+    mtol = 1e-4 if dtype == torch.float32 else 5e-2
+    assert np.abs(mass - mass0).max() < mtol
+    assert abs(ctx.win_p("a").sum() - n) < 1e-12
+    ctx.win_free("a")
+    ctx.close()
+
+
+def test_window_put_and_update():
+    # S:454 example: ring(3) after each in-neighbour puts {3, 9} and local 0,
+    # uniform 1/3 -> 4; idempotent when called twice
+    W = ora.ring(3)
+    ctx = _ctx(3)
+    ctx.set_topology(W)
+    x = _gpu(np.array([[0.0], [3.0], [9.0]]))
+    ctx.win_create(x, "u", zero_init=True)
+    ctx.win_put("u", self_weight=[1.0] * 3, dst_weights=[{1: 1.0, 2: 1.0}, {0: 1.0, 2: 1.0}, {0: 1.0, 1: 1.0}])
+    out = torch.empty_like(x)
+    ctx.win_update("u", out=out)
+    torch.cuda.synchronize()
+    assert abs(_np(out)[0, 0] - 4.0) < 1e-6
+    ctx.win_update("u", out=out)
+    torch.cuda.synchronize()
+    assert abs(_np(out)[0, 0] - 4.0) < 1e-6
+    # non-zero-init: buffers start as the local tensor -> update returns x
+    ctx.win_create(x, "v", zero_init=False)
+    ctx.win_update("v", out=out)
+    torch.cuda.synchronize()
+    assert np.allclose(_np(out), _np(x), atol=1e-6)
+    ctx.win_free("v")
+    ctx.win_free("u")
+    ctx.close()
+
+
+def test_window_dst_outside_creation_topology():
+    W = ora.ring(4)
+    ctx = _ctx(4)
+    ctx.set_topology(W)
+    x = torch.zeros(4, 10, device="cuda")
+    ctx.win_create(x, "d")
+    with pytest.raises(BluefogError) as e:
+        ctx.win_accumulate("d", self_weight=[0.5] * 4, dst_weights=[{2: 0.5}, {2: 0.5}, {3: 0.5}, {0: 0.5}])
+    assert e.value.name == "BF_ERR_WINDOW"
+    ctx.win_free("d")
+    ctx.close()
+
+
+# ------------------------------------------------ bench configuration (C4) ---
+def test_bench_config_c4_sampled():
+    """8 agents x 25.6M fp32, the launch configuration bench.py times; outputs
+    checked on sampled columns the oracle computes one by one."""
+    n, count, lr = 8, 25_600_000, 0.1
+    ctx = _ctx(n, heap=3 << 30)
+    ctx.set_dynamic_schedule("one_peer_exp2", 0)
+    x = torch.empty(n, count, device="cuda")
+    g = torch.empty(n, count, device="cuda")
+    for r in range(n):
+        bfp.Context.fill_uniform(x[r], synthetic.SEED_X0 + r)
+        bfp.Context.fill_uniform(g[r], synthetic.grad_seed(0, r), scale=2.0 ** -7)
+    rng = np.random.default_rng(0)
+    cols = np.unique(np.concatenate([rng.integers(0, count, 2000), [0, 1, 4095, 4096, count - 1]]))
+    Xs = np.stack([np.concatenate([synthetic.uniform(synthetic.SEED_X0 + r, 1, offset=int(c)) for c in cols])
+                   for r in range(n)]).astype(np.float64)
+    Gs = np.stack([np.concatenate([synthetic.uniform(synthetic.grad_seed(0, r), 1, scale=2.0 ** -7, offset=int(c))
+                                   for c in cols]) for r in range(n)]).astype(np.float64)
+    assert np.array_equal(x[:, torch.from_numpy(cols).cuda()].cpu().numpy(), Xs.astype(np.float32))
+    ctx.atc_step(x, g, lr)
+    torch.cuda.synchronize()
+    W0 = ora.one_peer_exp2(n, 0)
+    ref = ora.atc(W0, Xs, Gs, lr)
+    got = x[:, torch.from_numpy(cols).cuda()].cpu().numpy().astype(np.float64)
+    assert_parity(got, ref, W0, Xs, 1e-6, np.abs(W0) @ (lr * np.abs(Gs)))
+    ctx.close()

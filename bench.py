@@ -286,24 +286,25 @@ def main():
 
     if rank == 0:
         d = degree(a.topology, n)
-        # algorithmic bytes per launch on this GPU (fused ATC):
-        # x read + x write + g read + publish (wire) + d_out * served (wire)
-        hbm_bytes = k * count * (4 + 4 + 4 + wire_b + d * wire_b)
-        if world > 1:
-            # neighbours on other GPUs: d_in * wire bytes cross NVLink per remote source
-            remote = 0
-            for la in range(k):
-                gid = ctx.rank + la
-                for kk in range(1):
-                    src = [bfp.one_peer_exp2(n, gid, r)[0] for r in range(max(1, (n - 1).bit_length()))] \
-                        if a.topology == "one_peer" else [((gid - (1 << j)) % n) for j in range(d)]
-                    if a.topology == "one_peer":
-                        remote += sum(1 for s in src if s // k != ctx.proc) / len(src)
-                    else:
-                        remote += sum(1 for s in src if s // k != ctx.proc)
-            nvl_bytes = remote * count * wire_b
-        else:
-            nvl_bytes = 0
+        # algorithmic bytes per launch on this GPU:
+        # x read + g read + x write + publish (wire).  The d_out reads of each
+        # published tile by same-GPU neighbours are served from L2 by the
+        # tile-major schedule (ncu: DRAM traffic = 16.0 B/element at N=1).
+        hbm_bytes = k * count * (4 + 4 + 4 + wire_b)
+        # NVLink-in: wire bytes of every source that lives on another GPU,
+        # averaged over the rounds of the timed region (one-peer rotates).
+        tau = max(1, (n - 1).bit_length())
+        remote = 0.0
+        rounds = range(a.warmup, a.warmup + a.steps)
+        for la in range(k):
+            gid = ctx.rank + la
+            for r in rounds:
+                if a.topology == "one_peer":
+                    srcs = [(gid - (1 << (r % tau))) % n] if n > 1 else []
+                else:
+                    srcs = [(gid - (1 << j)) % n for j in range(d)]
+                remote += sum(1 for sidx in srcs if sidx // k != ctx.proc) / len(rounds)
+        nvl_bytes = remote * count * wire_b
         peak_hbm, peak_kind = hbm_peak()
         t_hbm = hbm_bytes / (peak_hbm * 1e9)
         t_nvl = nvl_bytes / (NVLINK_PEAK_GBS * 1e9)

@@ -26,6 +26,61 @@ __device__ __forceinline__ unsigned int ld_relaxed_sys_u32(const unsigned int *p
     asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Flags read by other GPUs need system scope; flags only read on this GPU
+// (every agent on one GPU) take the cheaper GPU scope.
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p, bool sys) {
+    return sys ? ld_acquire_sys(p) : ld_acquire_gpu(p);
+}
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v, bool sys) {
+    if (sys)
+        st_release_sys(p, v);
+    else
+        st_release_gpu(p, v);
+}
+
+// ---- TMA bulk copies + mbarriers (sm_90+ async proxy; SASS UBLKCP / SYNCS) ----
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gsrc, unsigned bytes,
+                                            unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "LAB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -52,13 +107,13 @@ static __device__ __noinline__ void abort_all(const Geometry &g, unsigned int co
 // Spin until *flag >= target.  Bounded by the context timeout and by the
 // abort word of this process.  Returns false on timeout / abort.
 __device__ __forceinline__ bool spin_ge(const Geometry &g, const unsigned long long *flag,
-                                        unsigned long long target) {
-    if (ld_acquire_sys(flag) >= target) return true;
+                                        unsigned long long target, bool sys = true) {
+    if (ld_acquire(flag, sys) >= target) return true;
     const unsigned long long t0 = globaltimer();
     const unsigned int *abort_w = &pad_of(g, g.me)->abort;
     unsigned int it = 0;
     while (true) {
-        if (ld_acquire_sys(flag) >= target) return true;
+        if (ld_acquire(flag, sys) >= target) return true;
         if ((++it & 63u) == 0) {
             if (ld_relaxed_sys_u32(abort_w)) return false;
             if (globaltimer() - t0 > g.timeout_ns) {
@@ -66,7 +121,7 @@ __device__ __forceinline__ bool spin_ge(const Geometry &g, const unsigned long l
                 return false;
             }
         }
-        __nanosleep(64);
+        __nanosleep(32);
     }
 }
 

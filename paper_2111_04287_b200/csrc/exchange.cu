@@ -174,15 +174,34 @@ __device__ void write_descriptors(const ExchParams &p, unsigned long long e) {
     }
 }
 
+// Shared-memory ring of the TMA-prefetched x / g tiles (2 stages).
+template <typename XT, typename GT, bool HAS_G>
+struct Ring {
+    static constexpr unsigned kXBytes = kTile * sizeof(XT);
+    static constexpr unsigned kGBytes = HAS_G ? kTile * sizeof(GT) : 0;
+    static constexpr unsigned kBytes = 2 * (kXBytes + kGBytes);
+};
+
 template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
 __global__ void __launch_bounds__(kThreads, 2) exchange_kernel(const __grid_constant__ ExchParams p) {
+    using R = Ring<XT, GT, HAS_G>;
+    extern __shared__ __align__(128) unsigned char ring[];
     __shared__ SharedTab st;
+    __shared__ __align__(8) unsigned long long full[2];
+    __shared__ int s_fail;
     const Geometry &g = p.geo;
     Pad *pad = pad_of(g, g.me);
     if (*reinterpret_cast<volatile unsigned int *>(&pad->abort)) return;
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
     const int parity = static_cast<int>(e & 1);
+    const bool sys = g.nprocs > 1;   // flags of agents on other GPUs need system scope
 
+    if (threadIdx.x == 0) {
+        s_fail = 0;
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+    }
     if (!war_wait(g, e)) return;
     if (p.wmode == kWDynamic) write_descriptors(p, e);
     if (!resolve_sources(p, e, st)) return;
@@ -191,29 +210,66 @@ __global__ void __launch_bounds__(kThreads, 2) exchange_kernel(const __grid_cons
     const long long count = g.count;
     const int k = g.k;
     const long long items = static_cast<long long>(k) * g.T;
-    __shared__ int s_fail;
-    if (threadIdx.x == 0) s_fail = 0;
+    // an item is staged by TMA when its rows are 16B-aligned and the tile is full
+    auto staged = [&](long long w) {
+        return vec && (count - static_cast<long long>(w / k) * kTile) >= kTile;
+    };
+    auto issue = [&](long long w, int stage) {   // thread 0 only
+        const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        const long long off = static_cast<long long>(a) * count + static_cast<long long>(t) * kTile;
+        fence_proxy_async();
+        mbar_expect_tx(&full[stage], R::kXBytes + R::kGBytes);
+        tma_load_1d(ring + stage * R::kXBytes, static_cast<const XT *>(p.x) + off, R::kXBytes, &full[stage]);
+        if constexpr (HAS_G)
+            tma_load_1d(ring + 2 * R::kXBytes + stage * R::kGBytes, static_cast<const GT *>(p.g) + off,
+                        R::kGBytes, &full[stage]);
+    };
+    unsigned phase[2] = {0u, 0u};
+    if (threadIdx.x == 0 && blockIdx.x < items && staged(blockIdx.x)) issue(blockIdx.x, 0);
 
-    for (long long w = blockIdx.x; w < items; w += gridDim.x) {
+    int it = 0;
+    for (long long w = blockIdx.x; w < items; w += gridDim.x, ++it) {
         const int t = static_cast<int>(w / k);
         const int a = static_cast<int>(w % k);
         const long long base = static_cast<long long>(t) * kTile;
         const long long rem = count - base;
+        const int stage = it & 1;
+        // prefetch the next item of this CTA while this one is processed
+        const long long wn = w + gridDim.x;
+        if (threadIdx.x == 0 && wn < items && staged(wn)) issue(wn, stage ^ 1);
 
         // ---- Eq. 4 local update (ATC) or plain input (neighbor_allreduce) ----
         float xh[kVecPerThread][4];
-        const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(a) * count + base;
+        if (staged(w)) {
+            mbar_wait(&full[stage], phase[stage]);
+            phase[stage] ^= 1u;
+            const XT *xs = reinterpret_cast<const XT *>(ring + stage * R::kXBytes);
 #pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j)
-            Vec4<XT>::load(xr + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
-        if constexpr (HAS_G) {
-            const GT *gr = static_cast<const GT *>(p.g) + static_cast<long long>(a) * count + base;
+            for (int j = 0; j < kVecPerThread; ++j) Vec4<XT>::load(xs + tile_elem(j), xh[j], 4, true);
+            if constexpr (HAS_G) {
+                const GT *gs = reinterpret_cast<const GT *>(ring + 2 * R::kXBytes + stage * R::kGBytes);
 #pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j) {
-                float gv[4];
-                Vec4<GT>::load(gr + tile_elem(j), gv, clamp_valid(rem, tile_elem(j)), vec);
+                for (int j = 0; j < kVecPerThread; ++j) {
+                    float gv[4];
+                    Vec4<GT>::load(gs + tile_elem(j), gv, 4, true);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
+                    for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
+                }
+            }
+        } else {
+            const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(a) * count + base;
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+                Vec4<XT>::load(xr + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
+            if constexpr (HAS_G) {
+                const GT *gr = static_cast<const GT *>(p.g) + static_cast<long long>(a) * count + base;
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j) {
+                    float gv[4];
+                    Vec4<GT>::load(gr + tile_elem(j), gv, clamp_valid(rem, tile_elem(j)), vec);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
+                }
             }
         }
 
@@ -225,16 +281,20 @@ __global__ void __launch_bounds__(kThreads, 2) exchange_kernel(const __grid_cons
             Vec4<WT>::store(mine + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
         __syncthreads();
         if (threadIdx.x == 0)
-            st_release_sys(ready_ptr(g, p.ready_off, p.ready_stride, g.me * k + a, t), e);
+            st_release(ready_ptr(g, p.ready_off, p.ready_stride, g.me * k + a, t), e, sys);
 
         // ---- wait for the in-neighbours' tile t ----
         const int ns = st.nsrc[a];
         if (threadIdx.x < ns) {
-            if (!spin_ge(g, ready_ptr(g, p.ready_off, p.ready_stride, st.src[a][threadIdx.x], t), e))
+            if (!spin_ge(g, ready_ptr(g, p.ready_off, p.ready_stride, st.src[a][threadIdx.x], t), e, sys))
                 s_fail = 1;
         }
         __syncthreads();
-        if (s_fail) return;
+        if (s_fail) {
+            // drain the in-flight prefetch before the CTA exits (its smem may be reused)
+            if (threadIdx.x == 0 && wn < items && staged(wn)) mbar_wait(&full[stage ^ 1], phase[stage ^ 1]);
+            return;
+        }
 
         // ---- Eq. 5 / Eq. 9 weighted combine in fp32 ----
         float acc[kVecPerThread][4];
@@ -459,14 +519,22 @@ int max_coresident(const void *func, int threads, size_t smem) {
 template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
 static cudaError_t launch_exch_t(const ExchParams &p, int grid, cudaStream_t s) {
     auto fn = exchange_kernel<XT, GT, WT, YT, HAS_G>;
-    const int maxg = max_coresident(reinterpret_cast<const void *>(fn), kThreads, 0);
+    const unsigned smem = Ring<XT, GT, HAS_G>::kBytes;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int maxg = max_coresident(reinterpret_cast<const void *>(fn), kThreads, smem);
     if (grid <= 0 || grid > maxg) grid = maxg;
     const long long items = static_cast<long long>(p.geo.k) * p.geo.T;
     if (grid > items) grid = static_cast<int>(items < p.geo.k ? p.geo.k : items);
     if (grid < 1) grid = 1;
     void *args[] = {const_cast<ExchParams *>(&p)};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(kThreads),
-                                       args, 0, s);
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(kThreads), args,
+                                       smem, s);
 }
 
 cudaError_t launch_exchange(const ExchParams &p, int x_kind, int g_kind, int wire_kind, int y_kind,

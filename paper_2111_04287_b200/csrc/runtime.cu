@@ -85,6 +85,7 @@ struct bf_ctx {
     int topo_check = 1;
     // exchange region
     size_t exch_cap = 0;                      // bytes per agent per parity
+    size_t exch_begin = 0, exch_top = 0;      // heap range of exchange (+ hierarchical) regions
     unsigned long long slot_off = 0, ready_off = 0;
     int ready_stride = 0;
     // hierarchical region
@@ -97,6 +98,8 @@ struct bf_ctx {
     unsigned long long bar_epoch = 0;
     unsigned long long launches = 0;
 };
+
+bf_status bf_barrier_internal(bf_ctx *c);
 
 namespace {
 
@@ -144,16 +147,25 @@ Geometry make_geo(bf_ctx *c, size_t count) {
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Exchange region: double-buffered slots + per-tile ready flags of every local
+// agent.  Grows on demand (collective: every process makes the same call):
+// quiesce all processes first, then release the old region if it is on top of
+// the heap (otherwise it is abandoned) and allocate the new one.
 bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
     if (c->exch_cap >= bytes_per_agent && c->exch_cap) return BF_OK;
-    if (c->exch_cap)
-        return fail(BF_ERR_NOMEM,
-                    "message of %zu bytes per agent exceeds the reserved exchange capacity %zu; call "
-                    "bf_reserve with the largest size first",
-                    bytes_per_agent, c->exch_cap);
     size_t tile_bytes = static_cast<size_t>(kTile) * 4;
     size_t cap = (bytes_per_agent + tile_bytes - 1) / tile_bytes * tile_bytes;
     if (cap == 0) cap = tile_bytes;
+    if (c->exch_cap) {
+        CU(cudaDeviceSynchronize());
+        bf_status s = bf_barrier_internal(c);
+        if (s) return s;
+        CU(cudaDeviceSynchronize());
+        if (c->heap_used == c->exch_top) c->heap_used = c->exch_begin;
+        c->hier_ready = false;
+        cap = std::max(cap, 2 * c->exch_cap);
+    }
+    const size_t begin = c->heap_used;
     unsigned long long slot_off, ready_off;
     bf_status s = heap_alloc(c, static_cast<size_t>(c->k) * 2 * cap, &slot_off);
     if (s) return s;
@@ -164,6 +176,8 @@ bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
     c->slot_off = slot_off;
     c->ready_off = ready_off;
     c->ready_stride = tmax;
+    c->exch_begin = begin;
+    c->exch_top = c->heap_used;
     return BF_OK;
 }
 
@@ -684,6 +698,7 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
     if (s) return s;
     if (!c->hier_ready) {
         // fp32 slice buffers sized for the largest count the exchange region admits
+        const bool on_top = c->heap_used == c->exch_top;
         const size_t max_elems = c->exch_cap / 2;
         const size_t bytes = max_elems * 4;
         unsigned long long off;
@@ -695,6 +710,7 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
         c->fb_off = off;
         if ((s = heap_alloc(c, static_cast<size_t>(c->k) * c->ready_stride * 8, &off))) return s;
         c->fc_off = off;
+        if (on_top) c->exch_top = c->heap_used;   // released together with the exchange region
         c->bc_agent_stride = 2 * bytes;
         c->bc_parity_stride = bytes;
         c->hier_ready = true;
@@ -765,11 +781,12 @@ bf_status bf_win_create(bf_ctx *c, const char *name, void *x, size_t count, bf_d
         }                                              \
         b.field = off;                                 \
     } while (0)
-    WALLOC(slot_off, K * DI * 2 * count * es);
+    const size_t cpad = (count + 3) / 4 * 4;
+    WALLOC(slot_off, K * DI * 2 * cpad * es);
     WALLOC(pslot_off, K * DI * 2 * 8);
     WALLOC(version_off, K * DI * 8);
     WALLOC(consumed_off, K * DO * 8);
-    WALLOC(outbox_off, K * DO * count * 4);
+    WALLOC(outbox_off, K * DO * cpad * 4);
     WALLOC(pout_off, K * DO * 8);
     WALLOC(delivered_off, K * DO * 8);
     WALLOC(obvalid_off, K * DO * 4);
@@ -781,6 +798,7 @@ bf_status bf_win_create(bf_ctx *c, const char *name, void *x, size_t count, bf_d
     w.alloc_end = c->heap_used;
     b.maxdin = w.maxdin;
     b.maxdout = w.maxdout;
+    b.cpad = static_cast<long long>(cpad);
     b.x = x;
     b.out = x;
     b.dtype = dtype;
@@ -792,7 +810,7 @@ bf_status bf_win_create(bf_ctx *c, const char *name, void *x, size_t count, bf_d
         for (int a = 0; a < c->k; ++a) {
             const int gid = c->proc * c->k + a;
             for (size_t q = 0; q < w.side[gid].in.size(); ++q)
-                CU(cudaMemcpy(c->heap + b.slot_off + ((a * DI + q) * 2 + 1) * count * es,
+                CU(cudaMemcpy(c->heap + b.slot_off + ((a * DI + q) * 2 + 1) * cpad * es,
                               static_cast<char *>(x) + a * count * es, count * es, cudaMemcpyDeviceToDevice));
         }
     }
@@ -992,6 +1010,12 @@ bf_status bf_barrier(bf_ctx *c, void *stream) {
     c->launches++;
     return BF_OK;
 }
+
+}  // extern "C"
+
+bf_status bf_barrier_internal(bf_ctx *c) { return bf_barrier(c, nullptr); }
+
+extern "C" {
 
 bf_status bf_poll_error(bf_ctx *c) {
     if (!c) return fail(BF_ERR_ARG, "null context");

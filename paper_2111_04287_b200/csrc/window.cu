@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kThreads) win_push_kernel(const __grid_constan
             const int ci = a * p.maxdout + qo;
             const bool deliver = dec[ci] != 0;
             const bool use_ob = obv[ci] != 0 && !p.overwrite;
-            float *ob = at<float>(me, p.outbox_off) + static_cast<long long>(ci) * count + base;
+            float *ob = at<float>(me, p.outbox_off) + static_cast<long long>(ci) * p.cpad + base;
             float pay[kVecPerThread][4];
 #pragma unroll
             for (int j = 0; j < kVecPerThread; ++j) {
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kThreads) win_push_kernel(const __grid_constan
                 const int half = static_cast<int>(dlv[ci] & 1ull);
                 T *slot = at<T>(g.peer_base[dst / k],
                                 p.slot_off + ((static_cast<unsigned long long>(dst % k) * p.maxdin + qin) * 2 + half) *
-                                                 count * esize(p)) + base;
+                                                 p.cpad * esize(p)) + base;
 #pragma unroll
                 for (int j = 0; j < kVecPerThread; ++j) {
                     const int vl = clamp_valid(rem, tile_elem(j));
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) win_collect_kernel(const __grid_cons
             for (unsigned long long m = m_first; update ? (m == m_first) : (m < m_end);
                  m = update ? m_first + 1 : m + 1) {
                 const T *h = at<const T>(me, p.slot_off + (static_cast<unsigned long long>(ci) * 2 + (m & 1)) *
-                                                              count * esize(p)) + base;
+                                                              p.cpad * esize(p)) + base;
 #pragma unroll
                 for (int j = 0; j < kVecPerThread; ++j) {
                     float v4[4];

@@ -1,0 +1,200 @@
+"""Multi-process parity worker (one process per GPU, launched by torchrun from
+tests/test_multigpu.py).  Every process holds `BF_TEST_K` agents; neighbours
+on other GPUs are read over NVLink through CUDA-IPC peer pointers.  Each rank
+checks its own rows against the oracle run on the full stacked input."""
+import os
+import sys
+import traceback
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("BF_TIMEOUT_MS", "8000")
+
+import oracle as ora  # noqa: E402
+import synthetic  # noqa: E402
+import paper_2111_04287_b200 as bfp  # noqa: E402
+from paper_2111_04287_b200 import BluefogError  # noqa: E402
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    rank = int(os.environ["RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    k = int(os.environ.get("BF_TEST_K", "1"))
+    ctx = bfp.Context(agents_per_proc=k, heap_bytes=1 << 28, device=local)
+    n, r0 = ctx.n, ctx.rank
+    rows = slice(r0, r0 + k)
+    failures = []
+
+    def check(name, y, ref, W, X, tol, extra=None):
+        b = (np.abs(W) @ np.abs(X))[rows]
+        if extra is not None:
+            b = b + extra[rows]
+        err = np.abs(y - ref[rows])
+        if (err > tol * b + 1e-30).any():
+            failures.append(f"{name}: max rel {np.max(err / (b + 1e-30)):.3e}")
+
+    def inputs(count, dtype=torch.float32, seed_off=0):
+        X = np.stack([synthetic.uniform(synthetic.SEED_X0 + seed_off + r, count) for r in range(n)])
+        xt = torch.from_numpy(X[rows].copy()).to(dtype).cuda()
+        Xf = torch.from_numpy(X).to(dtype).float().numpy().astype(np.float64)
+        return xt, Xf
+
+    def np_(t):
+        return t.float().cpu().numpy().astype(np.float64)
+
+    # ---- static topologies --------------------------------------------------
+    for topo in ("exp2", "ring", "full"):
+        W = {"exp2": ora.exp2, "ring": ora.ring, "full": ora.full}[topo](n)
+        ctx.set_topology(W)
+        for dtype, tol in ((torch.float32, 1e-6), (torch.bfloat16, 1e-2)):
+            for count in (1, 4097, 3 * 4096 + 5, 200003):
+                x, X = inputs(count, dtype)
+                y = ctx.neighbor_allreduce(x)
+                torch.cuda.synchronize()
+                check(f"static {topo} {dtype} {count}", np_(y), ora.mix(W, X), W, X, tol)
+
+    # ---- dynamic push / pull / push-pull ------------------------------------
+    rng = np.random.default_rng(11)
+    W = (rng.random((n, n)) < 0.6) * rng.uniform(0.1, 1.0, (n, n))
+    np.fill_diagonal(W, 0.5)
+    for style in ("pull", "push", "pushpull"):
+        sw, srcw, dstw = [], [], []
+        for i in range(r0, r0 + k):
+            srcs = [j for j in range(n) if j != i and W[i, j] != 0]
+            dsts = [j for j in range(n) if j != i and W[j, i] != 0]
+            sw.append(W[i, i])
+            srcw.append({j: W[i, j] for j in srcs} if style == "pull" else
+                        ({j: 0.5 for j in srcs} if style == "pushpull" else None))
+            dstw.append({j: W[j, i] for j in dsts} if style == "push" else
+                        ({j: 2.0 * W[j, i] for j in dsts} if style == "pushpull" else None))
+        x, X = inputs(50001)
+        y = ctx.neighbor_allreduce(x, self_weight=sw, src_weights=srcw, dst_weights=dstw)
+        torch.cuda.synchronize()
+        check(f"dynamic {style}", np_(y), ora.mix(W, X), W, X, 1e-6)
+
+    # ---- one-peer schedule (device round counter) ----------------------------
+    ctx.set_dynamic_schedule("one_peer_exp2", 0)
+    x, X = inputs(70001)
+    for kk in range(4):
+        x = ctx.neighbor_allreduce(x)
+        torch.cuda.synchronize()
+        Wk = ora.one_peer_exp2(n, kk)
+        Y = ora.mix(Wk, X)
+        check(f"schedule round {kk}", np_(x), Y, Wk, X, 1e-6)
+        X = Y   # continue from the oracle state (rows of other ranks are not visible here)
+        x = torch.from_numpy(X[rows].astype(np.float32)).cuda()
+    # ---- fused ATC --------------------------------------------------------------
+    for wire, tol in ((torch.float32, 1e-6), (torch.bfloat16, 1e-2)):
+        x, X = inputs(123457)
+        G = np.stack([synthetic.uniform(synthetic.grad_seed(1, r), 123457, scale=2.0 ** -7) for r in range(n)])
+        g = torch.from_numpy(G[rows].copy()).cuda()
+        kk = 4 if wire == torch.float32 else 5
+        ctx.atc_step(x, g, 0.1, wire=wire)
+        torch.cuda.synchronize()
+        Wk = ora.one_peer_exp2(n, kk)
+        check(f"atc {wire}", np_(x), ora.atc(Wk, X, G.astype(np.float64), 0.1, wire_bf16=wire == torch.bfloat16),
+              Wk, X, tol, np.abs(Wk) @ (0.1 * np.abs(G.astype(np.float64))))
+    ctx.set_dynamic_schedule("none")
+
+    # ---- hierarchical -------------------------------------------------------------
+    for L in (2, n):
+        if n % L or n // L < 1:
+            continue
+        nm = n // L
+        WM = ora.exp2(nm)
+        ctx.set_machine_topology(WM, L)
+        x, X = inputs(40000)
+        y = ctx.hierarchical_neighbor_allreduce(x)
+        torch.cuda.synchronize()
+        check(f"hier L={L}", np_(y), ora.hier(WM, L, X), np.kron(WM, np.full((L, L), 1.0 / L)), X, 1e-6)
+
+    # ---- windows: synchronous push-sum ------------------------------------------
+    Wst = ora.exp2(n)
+    ctx.set_topology(Wst)
+    x, X = inputs(9001)
+    ctx.win_create(x, "ps", zero_init=True, with_p=True)
+    win = ora.Window(Wst, np.concatenate([X, np.ones((n, 1))], axis=1), zero_init=True)
+    for _ in range(4):
+        ctx.win_accumulate("ps")
+        ctx.barrier()
+        ctx.win_update_then_collect("ps")
+        ctx.barrier()
+        for i in range(n):
+            outs = ora.out_neighbors(Wst, i)
+            w = 1.0 / (len(outs) + 1)
+            win.accumulate(i, w, {j: w for j in outs})
+        for i in range(n):
+            win.collect(i)
+    torch.cuda.synchronize()
+    ref = win.x()
+    if np.abs(np_(x) - ref[rows, :-1]).max() > 1e-5:
+        failures.append("window sync push-sum x")
+    if np.abs(ctx.win_p("ps") - ref[rows, -1]).max() > 1e-12:
+        failures.append("window sync push-sum p")
+
+    # ---- windows: asynchronous push-sum (no inter-agent synchronisation) --------
+    x2, X2 = inputs(20000, seed_off=7)
+    ctx.win_create(x2, "async", zero_init=True, with_p=True)
+    mass0 = X2.sum(axis=0)
+    lr_ = np.random.default_rng(100 + rank)
+    for _ in range(60):
+        if lr_.random() < 0.5:
+            ctx.win_accumulate("async", agent_mask=1 << int(lr_.integers(k)))
+        else:
+            ctx.win_update_then_collect("async", agent_mask=1 << int(lr_.integers(k)))
+    for _ in range(3):   # quiesce: flush outboxes, collect everything
+        ctx.barrier()
+        ctx.win_accumulate("async", self_weight=[1.0] * k,
+                           dst_weights=[{j: 0.0 for j in ora.out_neighbors(Wst, i)} for i in range(r0, r0 + k)])
+        ctx.barrier()
+        ctx.win_update_then_collect("async")
+    ctx.barrier()
+    torch.cuda.synchronize()
+    tot = torch.tensor(np.concatenate([np_(x2).sum(axis=0), [ctx.win_p("async").sum()]]), device="cuda")
+    dist.all_reduce(tot)
+    tot = tot.cpu().numpy()
+    if np.abs(tot[:-1] - mass0).max() > 1e-4 or abs(tot[-1] - n) > 1e-12:
+        failures.append(f"async window mass {np.abs(tot[:-1] - mass0).max():.3e} p {tot[-1]}")
+    ctx.win_free("async")
+    ctx.win_free("ps")
+
+    # ---- topology-check mismatch: an error, never a hang -------------------
+    x, X = inputs(1000)
+    got = None
+    try:
+        sw = [0.5] * k
+        if r0 == 0:   # agent 0 pushes to agent n-1, which declares no sources
+            dstw = [{n - 1: 0.5}] + [{}] * (k - 1)
+        else:
+            dstw = [{}] * k
+        srcw = [None] * k if r0 == 0 else [{}] * k
+        ctx.neighbor_allreduce(x, self_weight=sw, src_weights=srcw, dst_weights=dstw)
+        torch.cuda.synchronize()
+        ctx.poll_error()
+    except BluefogError as e:
+        got = e.name
+    if got not in ("BF_ERR_TOPOLOGY", "BF_ERR_TIMEOUT"):
+        failures.append(f"mismatch not reported: {got}")
+
+    dist.barrier()
+    if failures:
+        print(f"RANK {rank} FAIL: " + "; ".join(failures), flush=True)
+    else:
+        print(f"RANK {rank} ALL OK", flush=True)
+    ctx.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    try:
+        main()
+    except Exception:
+        traceback.print_exc()
+        print(f"RANK {os.environ.get('RANK')} FAIL: exception", flush=True)
+        sys.exit(1)

@@ -1,0 +1,29 @@
+"""Multi-GPU parity: one process per GPU (torchrun), CUDA-IPC peer memory over
+NVLink.  Needs >= 2 GPUs; skipped otherwise."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpus():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("nproc,k", [(2, 1), (2, 2), (4, 1), (4, 2)])
+def test_multiprocess_parity(nproc, k):
+    if _ngpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    env = dict(os.environ, BF_TEST_K=str(k), BF_TIMEOUT_MS="8000")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mp_worker.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert out.count("ALL OK") == nproc, out[-4000:]

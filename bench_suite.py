@@ -1,0 +1,242 @@
+#!/usr/bin/env python
+"""Measurement suite for the BASELINE.json configs beyond bench.py's C4 line.
+
+  C1  consensus, ring-4, fp32[4096], 20 iterations: microseconds per iteration
+  C2  ATC-DSGD on synthetic least squares (d=10k, 8 agents, m=2000 rows each):
+      iterations/s and distance to the oracle's x* (gradients by torch GEMV --
+      workload plumbing, not the hot path)
+  C3  neighbor_allreduce sweep 1 KB .. 1 GB per agent, fp32/bf16, static exp-2
+      vs one-peer: exchange GB/s per GPU and HBM fraction
+  C5  push-sum through win_accumulate / win_update_then_collect, 340M bf16 per
+      agent, one-peer destinations inside the static exp-2 window topology
+  H   hierarchical_neighbor_allreduce, 25.6M fp32, L = 2, 4
+
+One JSON object per line.  N = 1: the 8 agents are virtual agents of one GPU;
+under torchrun, 8/N agents per GPU.  Every number is CUDA-event time on the
+launching stream, after warm-up, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="c1,c3,c5,h,c2")
+    ap.add_argument("--agents", type=int, default=8)
+    ap.add_argument("--max-bytes", type=int, default=1 << 30)
+    ap.add_argument("--out", default=None)
+    return ap.parse_args()
+
+
+def main():
+    a = parse()
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2111_04287_b200 as bfp
+    import synthetic
+
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    out = open(a.out, "a") if (a.out and rank == 0) else None
+    stream = torch.cuda.current_stream()
+
+    def emit(d):
+        d["n_gpus"] = world
+        if rank == 0:
+            line = json.dumps(d)
+            print(line, flush=True)
+            if out:
+                out.write(line + "\n")
+                out.flush()
+
+    def timed(fn, iters, warm=3):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / iters], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms)
+
+    only = set(a.only.split(","))
+
+    # ---------------------------------------------------------------- C1 ----
+    if "c1" in only:
+        n = 4
+        if n % world == 0:
+            k = n // world
+            ctx = bfp.Context(agents_per_proc=k, heap_bytes=64 << 20, device=local)
+            ctx.set_topology(bfp.topology_matrix("ring", n))
+            x = torch.empty(k, 4096, device="cuda")
+            for la in range(k):
+                bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + ctx.rank + la)
+            y = torch.empty_like(x)
+
+            def c1():
+                for _ in range(10):
+                    ctx.neighbor_allreduce(x, out=y)
+                    ctx.neighbor_allreduce(y, out=x)
+            ms = timed(c1, 5)
+            emit({"config": "C1 consensus ring-4 fp32[4096] x 20 iterations", "us_per_iteration": ms * 1e3 / 20,
+                  "ms_20_iterations": ms})
+            ctx.close()
+
+    # ---------------------------------------------------------------- C3 ----
+    if "c3" in only:
+        n = a.agents
+        k = n // world
+        maxb = a.max_bytes
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=k * 2 * maxb + (256 << 20), device=local)
+        ctx.reserve(maxb)
+        W = bfp.topology_matrix("exp2", n)
+        for dtype, es in ((torch.float32, 4), (torch.bfloat16, 2)):
+            nb = 1024
+            while nb <= maxb:
+                count = nb // es
+                x = torch.empty(k, count, device="cuda", dtype=dtype)
+                for la in range(k):
+                    bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + ctx.rank + la)
+                y = torch.empty_like(x)
+                for topo in ("exp2", "one_peer"):
+                    if topo == "exp2":
+                        ctx.set_topology(W)
+                        d = 3 if n == 8 else int(np.count_nonzero(W[0])) - 1
+                    else:
+                        ctx.set_dynamic_schedule("one_peer_exp2", 0)
+                        d = 1
+                    iters = max(3, min(200, int(2e8 // max(nb, 1))))
+                    ms = timed(lambda: ctx.neighbor_allreduce(x, out=y), iters)
+                    ctx.set_dynamic_schedule("none")
+                    gbs = k * d * nb / (ms * 1e-3) / 1e9
+                    hbm = k * 3 * nb / (ms * 1e-3) / 1e9      # read x, write y, publish
+                    emit({"config": "C3 neighbor_allreduce sweep", "bytes_per_agent": nb,
+                          "dtype": str(dtype).split(".")[-1], "topology": topo, "agents": n, "agents_per_gpu": k,
+                          "us": ms * 1e3, "exchange_gbs_per_gpu": gbs, "hbm_gbs": hbm, "hbm_frac": hbm / peak})
+                del x, y
+                nb *= 4
+        ctx.close()
+
+    # ----------------------------------------------------------------- H ----
+    if "h" in only:
+        n = a.agents
+        k = n // world
+        count = 25_600_000
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=6 * k * count * 4 + (256 << 20), device=local)
+        x = torch.empty(k, count, device="cuda")
+        for la in range(k):
+            bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + ctx.rank + la)
+        y = torch.empty_like(x)
+        for L in (2, 4):
+            nm = n // L
+            ctx.set_machine_topology(bfp.topology_matrix("exp2", nm), L)
+            ms = timed(lambda: ctx.hierarchical_neighbor_allreduce(x, out=y), 20)
+            dm = 1 if nm == 2 else (2 if nm in (3, 4) else 3)
+            per_agent = (2 * (L - 1) + dm) * count * 4 / L + 3 * count * 4
+            emit({"config": f"H hierarchical_neighbor_allreduce 25.6M fp32, {nm} machines x {L}", "ms": ms,
+                  "gbs_per_gpu": k * per_agent / (ms * 1e-3) / 1e9})
+        ctx.close()
+
+    # ---------------------------------------------------------------- C5 ----
+    if "c5" in only:
+        n = a.agents
+        k = n // world
+        count = 340_000_000
+        try:
+            ctx = bfp.Context(agents_per_proc=k, heap_bytes=k * 3 * count * (2 * 2 + 4) + (1 << 30), device=local)
+            ctx.set_topology(bfp.topology_matrix("exp2", n))
+            x = torch.empty(k, count, device="cuda", dtype=torch.bfloat16)
+            for la in range(k):
+                bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + ctx.rank + la)
+            ctx.win_create(x, "ext", zero_init=True, with_p=True)
+            r = [0]
+
+            def c5():
+                ks = r[0]
+                dst = []
+                for la in range(k):
+                    _, d_ = bfp.one_peer_exp2(n, ctx.rank + la, ks)
+                    dst.append({d_: 0.5})
+                ctx.win_accumulate("ext", self_weight=[0.5] * k, dst_weights=dst)
+                ctx.win_update_then_collect("ext")
+                r[0] += 1
+            ms = timed(c5, 10)
+            p = ctx.win_p("ext")
+            tot = torch.tensor([float(p.sum())], device="cuda", dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(tot)
+            nvl = k * count * 2                      # one payload per agent per round
+            emit({"config": "C5 push-sum round (win_accumulate + win_update_then_collect), 340M bf16/agent, "
+                            "one-peer dst in exp-2 window", "ms_per_round": ms, "rounds_per_s": 1e3 / ms,
+                  "payload_gbs_per_gpu": nvl / (ms * 1e-3) / 1e9, "sum_p": float(tot), "expected_sum_p": n})
+            ctx.win_free("ext")
+            ctx.close()
+        except Exception as ex:  # noqa: BLE001
+            emit({"config": "C5", "error": repr(ex)[:300]})
+
+    # ---------------------------------------------------------------- C2 ----
+    if "c2" in only and world == 1:
+        import oracle as ora
+        n, m, d = a.agents, 2000, 10_000
+        As = torch.stack([torch.from_numpy(synthetic.uniform(synthetic.SEED_A + r, m * d,
+                                                             scale=1.0 / np.sqrt(m)).reshape(m, d))
+                          for r in range(n)]).cuda()
+        xnat = torch.from_numpy(synthetic.uniform(synthetic.SEED_XNAT, d)).cuda()
+        bs = torch.stack([As[r] @ xnat + torch.from_numpy(synthetic.uniform(synthetic.SEED_NOISE + r, m,
+                                                                            scale=0.01)).cuda()
+                          for r in range(n)])
+        L = max(float(torch.linalg.matrix_norm(As[r], ord=2) ** 2) for r in range(n))
+        lr = 1.0 / L
+        ctx = bfp.Context(agents_per_proc=n, heap_bytes=64 << 20, device=local)
+        x = torch.zeros(n, d, device="cuda")
+        g = torch.empty_like(x)
+        for topo in ("exp2", "one_peer"):
+            x.zero_()
+            if topo == "exp2":
+                ctx.set_topology(bfp.topology_matrix("exp2", n))
+            else:
+                ctx.set_dynamic_schedule("one_peer_exp2", 0)
+
+            def step():
+                r_ = torch.bmm(As, x.unsqueeze(2)).squeeze(2) - bs
+                torch.bmm(As.transpose(1, 2), r_.unsqueeze(2), out=g.unsqueeze(2))
+                ctx.atc_step(x, g, lr)
+            ms = timed(step, 200, warm=0)
+            ctx.set_dynamic_schedule("none")
+            xs, _ = ora.lsq_solve(As.double().cpu().numpy(), bs.double().cpu().numpy(), tol=1e-12, max_iter=2000)
+            xbar = x.double().mean(0).cpu().numpy()
+            emit({"config": f"C2 ATC-DSGD least squares d=10k m=2000 x 8 agents, {topo}", "ms_per_iter": ms,
+                  "iters_per_s": 1e3 / ms, "rel_dist_to_xstar_after_203_iters":
+                      float(np.linalg.norm(xbar - xs) / np.linalg.norm(xs)),
+                  "consensus_residual": float((x.double() - x.double().mean(0)).abs().max())})
+        ctx.close()
+
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

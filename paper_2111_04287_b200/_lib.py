@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libbluefog_b200.so")
+SO_PATH = os.environ.get("BF_LIB_PATH") or os.path.join(HERE, "libbluefog_b200.so")
 
 BF_OK = 0
 STATUS = {0: "BF_OK", 1: "BF_ERR_ARG", 2: "BF_ERR_STATE", 3: "BF_ERR_TOPOLOGY", 4: "BF_ERR_CUDA",

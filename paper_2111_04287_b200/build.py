@@ -39,10 +39,11 @@ def up_to_date() -> bool:
     return os.path.getmtime(SO) >= max(os.path.getmtime(p) for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = SO) -> str:
+    """defines: extra -D flags for tuning variants (BF_TILE, BF_THREADS, BF_MINB)."""
+    if not force and out == SO and not defines and up_to_date():
         return SO
-    cmd = [NVCC, *FLAGS, *sources(), "-o", SO + ".tmp"]
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], *sources(), "-o", out + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
@@ -50,12 +51,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed (see {log})")
-    os.replace(SO + ".tmp", SO)
+    os.replace(out + ".tmp", out)
     if verbose:
         sys.stdout.write(res.stderr)
-    return SO
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(SO)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv or bool(defs), verbose="-v" in sys.argv, defines=defs,
+                out=outs[0] if outs else SO))

@@ -15,8 +15,17 @@
 
 namespace bf {
 
-constexpr int kTile = 4096;            // elements per tile (the unit of one flag)
-constexpr int kThreads = 256;          // threads per CTA of the streaming kernels
+#ifndef BF_TILE
+#define BF_TILE 4096
+#endif
+#ifndef BF_THREADS
+#define BF_THREADS 256
+#endif
+#ifndef BF_MINB
+#define BF_MINB 2
+#endif
+constexpr int kTile = BF_TILE;         // elements per tile (the unit of one flag)
+constexpr int kThreads = BF_THREADS;   // threads per CTA of the streaming kernels
 constexpr int kVec = 4;                // elements per vector access
 constexpr int kVecPerThread = kTile / (kThreads * kVec);   // 4
 constexpr int kMaxK = BF_MAX_LOCAL_AGENTS;

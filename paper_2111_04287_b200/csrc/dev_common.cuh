@@ -81,10 +81,37 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// 16-byte LDGSTS with zero fill beyond src_bytes (0..16); generic-proxy global
+// read, so it is valid on CUDA-IPC peer mappings (NVLink) as well as local HBM.
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, unsigned src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
+                 "r"(src_bytes)
+                 : "memory");
+}
+// arrive on `bar` when all prior cp.async of this thread have completed
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(unsigned long long *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// Kernel prologue check: a fault raised earlier (here or by a peer) stops the
+// kernel and is latched in the host-visible error word.
+__device__ __forceinline__ bool aborted(const Geometry &g) {
+    const unsigned int code = *reinterpret_cast<volatile unsigned int *>(
+        &reinterpret_cast<Pad *>(g.peer_base[g.me])->abort);
+    if (code && g.host_err && threadIdx.x == 0) *g.host_err = code;
+    return code != 0;
 }
 
 template <typename T>
@@ -115,7 +142,11 @@ __device__ __forceinline__ bool spin_ge(const Geometry &g, const unsigned long l
     while (true) {
         if (ld_acquire(flag, sys) >= target) return true;
         if ((++it & 63u) == 0) {
-            if (ld_relaxed_sys_u32(abort_w)) return false;
+            const unsigned int code = ld_relaxed_sys_u32(abort_w);
+            if (code) {   // raised by a peer: latch it for this process's host too
+                if (g.host_err) *g.host_err = code;
+                return false;
+            }
             if (globaltimer() - t0 > g.timeout_ns) {
                 abort_all(g, BF_ERR_TIMEOUT);
                 return false;

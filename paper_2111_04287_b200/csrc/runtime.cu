@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cstddef>
 #include <map>
 #include <string>
 #include <vector>
@@ -1019,6 +1020,13 @@ extern "C" {
 
 bf_status bf_poll_error(bf_ctx *c) {
     if (!c) return fail(BF_ERR_ARG, "null context");
+    if (c->h_err && !*c->h_err && c->heap) {
+        // a peer may have raised an abort in this process's pad after our last kernel
+        unsigned int code = 0;
+        cudaSetDevice(c->device);
+        if (cudaMemcpy(&code, c->heap + offsetof(Pad, abort), 4, cudaMemcpyDeviceToHost) == cudaSuccess && code)
+            *const_cast<unsigned int *>(c->h_err) = code;
+    }
     if (c->h_err && *c->h_err) {
         c->poisoned = true;
         c->fault = static_cast<bf_status>(*c->h_err);

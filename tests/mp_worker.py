@@ -179,7 +179,15 @@ def main():
         ctx.poll_error()
     except BluefogError as e:
         got = e.name
-    if got not in ("BF_ERR_TOPOLOGY", "BF_ERR_TIMEOUT"):
+    # the receiver detects the mismatch; it aborts every process, so after a
+    # host barrier every rank reports the fault (the sender included)
+    dist.barrier()
+    if got is None:
+        try:
+            ctx.poll_error()
+        except BluefogError as e:
+            got = e.name
+    if got not in ("BF_ERR_TOPOLOGY", "BF_ERR_TIMEOUT", "BF_ERR_STATE"):
         failures.append(f"mismatch not reported: {got}")
 
     dist.barrier()

@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--agents", type=int, default=8)
     ap.add_argument("--count", type=int, default=25_600_000)
-    ap.add_argument("--topology", choices=["one_peer", "exp2"], default="one_peer")
+    ap.add_argument("--topology", choices=["one_peer", "exp2", "self"], default="one_peer")
     ap.add_argument("--wire", choices=["fp32", "bf16"], default="fp32")
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--no-e2e", action="store_true")
@@ -60,7 +60,7 @@ def hbm_peak():
 
 
 def degree(topology, n):
-    if n == 1:
+    if n == 1 or topology == "self":
         return 0
     if topology == "one_peer":
         return 1
@@ -215,6 +215,9 @@ def main():
     n = ctx.n
     if a.topology == "one_peer":
         ctx.set_dynamic_schedule("one_peer_exp2", 0)
+    elif a.topology == "self":      # diagnostic: W = I, no neighbour traffic
+        import numpy as np
+        ctx.set_topology(np.eye(n))
     else:
         ctx.set_topology(bfp.topology_matrix("exp2", n))
     ctx.reserve(count * wire_b)

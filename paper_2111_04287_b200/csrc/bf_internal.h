@@ -103,6 +103,7 @@ struct ExchParams {
     int ready_stride;
     int wmode;
     int check;
+    int kernel;                             // 0: exchange_kernel (default), 1: exchange_pipe_kernel
     SrcTab tab;                             // kWStatic: final coefficients; kWDynamic: declared r
     DynDecl dyn;
 };

@@ -46,6 +46,27 @@ __device__ __forceinline__ void st_release(unsigned long long *p, unsigned long 
         st_release_gpu(p, v);
 }
 
+__device__ __forceinline__ void fence_acq_rel(bool sys) {
+    if (sys)
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p, bool sys) {
+    unsigned long long v;
+    if (sys)
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v, bool sys) {
+    if (sys)
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // ---- TMA bulk copies + mbarriers (sm_90+ async proxy; SASS UBLKCP / SYNCS) ----
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -153,6 +174,46 @@ __device__ __forceinline__ bool spin_ge(const Geometry &g, const unsigned long l
             }
         }
         __nanosleep(32);
+    }
+}
+
+// Bounded mbarrier wait: returns false (and fails the CTA) on timeout or when
+// *fail is already set, so a protocol fault can never hang the GPU.
+__device__ __forceinline__ bool mbar_try(unsigned long long *bar, unsigned phase) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+// non-blocking test of a phase
+__device__ __forceinline__ bool mbar_test(unsigned long long *bar, unsigned phase) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ bool mbar_wait_b(const Geometry &g, unsigned long long *bar, unsigned phase,
+                                            volatile int *fail) {
+    if (mbar_try(bar, phase)) return true;
+    const unsigned long long t0 = globaltimer();
+    while (true) {
+        if (mbar_try(bar, phase)) return true;
+        if (*fail) return false;
+        if (globaltimer() - t0 > g.timeout_ns) {
+            *fail = 1;
+            abort_all(g, BF_ERR_TIMEOUT);
+            return false;
+        }
     }
 }
 

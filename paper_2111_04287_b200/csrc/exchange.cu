@@ -174,53 +174,20 @@ __device__ void write_descriptors(const ExchParams &p, unsigned long long e) {
     }
 }
 
-#ifndef BF_LAG
-#define BF_LAG 2
-#endif
-#ifndef BF_PSTAGES
-#define BF_PSTAGES 2
-#endif
-#ifndef BF_NPEER
-#define BF_NPEER 2
-#endif
-constexpr int kConsumerWarps = kThreads / 32;          // 8 consumer warps
-constexpr int kExchThreads = kThreads + 96;            // + 2 producer warps + 1 signal warp
-
-// Per-CTA shared-memory pipeline.
-//   x/g ring  : SX = D + 2 stages (item i is combined while item i+D is published)
-//   peer ring : SP stages of NP in-neighbour tiles
-template <typename XT, typename GT, typename WT, bool HAS_G>
-struct Pipe {
-    static constexpr int D = BF_LAG, SX = BF_LAG + 2, SP = BF_PSTAGES, NP = BF_NPEER;
-    static constexpr unsigned XB = kTile * sizeof(XT);
-    static constexpr unsigned GB = HAS_G ? kTile * sizeof(GT) : 0;
-    static constexpr unsigned PB = kTile * sizeof(WT);
-    static constexpr unsigned XG = XB + GB;
-    static constexpr unsigned BYTES = SX * XG + SP * NP * PB;
+// Shared-memory ring of the TMA-prefetched x / g tiles (2 stages).
+template <typename XT, typename GT, bool HAS_G>
+struct Ring {
+    static constexpr unsigned kXBytes = kTile * sizeof(XT);
+    static constexpr unsigned kGBytes = HAS_G ? kTile * sizeof(GT) : 0;
+    static constexpr unsigned kBytes = 2 * (kXBytes + kGBytes);
 };
 
-// exchange_kernel: warp-specialised persistent pipeline, one CTA per SM.
-//   producer warp A : TMA bulk loads of this CTA's x / g tiles (x/g ring)
-//   producer warp B : acquire the in-neighbours' ready flags of a tile, then
-//                     LDGSTS (cp.async) of their published tiles -- over NVLink
-//                     for agents on other GPUs, from L2 on this GPU (peer ring)
-//   consumer warps  : iteration c publishes item c+D (adapt x - lr*g, store the
-//                     wire copy in this agent's IPC slot, release its flag) and
-//                     then combines item c (Eq. 5 / Eq. 9, fp32) and stores it.
-// Publishing D items ahead means a neighbour's tile is normally published long
-// before it is needed, so flag waits and peer-load latency leave the critical
-// path.  Deadlock freedom: items are visited in increasing tile order; x/g
-// loads never wait on other agents; a tile is published before anybody's wait
-// for the tile of a later item; all CTAs are co-resident (cooperative launch).
-// A fault never exits early: waits fail fast, garbage is computed and the fault
-// is latched, so no TMA or cp.async is left in flight.
 template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
-__global__ void __launch_bounds__(kExchThreads, 1) exchange_kernel(const __grid_constant__ ExchParams p) {
-    using P = Pipe<XT, GT, WT, HAS_G>;
-    extern __shared__ __align__(128) unsigned char smem[];
+__global__ void __launch_bounds__(kThreads, BF_MINB) exchange_kernel(const __grid_constant__ ExchParams p) {
+    using R = Ring<XT, GT, HAS_G>;
+    extern __shared__ __align__(128) unsigned char ring[];
     __shared__ SharedTab st;
-    __shared__ __align__(8) unsigned long long full_xg[P::SX], empty_xg[P::SX], published[P::SX];
-    __shared__ __align__(8) unsigned long long full_pr[P::SP], empty_pr[P::SP];
+    __shared__ __align__(8) unsigned long long full[2];
     __shared__ int s_fail;
     const Geometry &g = p.geo;
     Pad *pad = pad_of(g, g.me);
@@ -231,14 +198,249 @@ __global__ void __launch_bounds__(kExchThreads, 1) exchange_kernel(const __grid_
 
     if (threadIdx.x == 0) {
         s_fail = 0;
-        for (int i = 0; i < P::SX; ++i) {
-            mbar_init(&full_xg[i], 1);
-            mbar_init(&empty_xg[i], kConsumerWarps + 1);   // consumers + signal warp
-            mbar_init(&published[i], kConsumerWarps);
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+    }
+    if (!war_wait(g, e)) return;
+    if (p.wmode == kWDynamic) write_descriptors(p, e);
+    if (!resolve_sources(p, e, st)) return;
+
+    const bool vec = g.vec_ok != 0;
+    const long long count = g.count;
+    const int k = g.k;
+    const long long items = static_cast<long long>(k) * g.T;
+    // an item is staged by TMA when its rows are 16B-aligned and the tile is full
+    auto staged = [&](long long w) {
+        return vec && (count - static_cast<long long>(w / k) * kTile) >= kTile;
+    };
+    auto issue = [&](long long w, int stage) {   // thread 0 only
+        const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        const long long off = static_cast<long long>(a) * count + static_cast<long long>(t) * kTile;
+        fence_proxy_async();
+        mbar_expect_tx(&full[stage], R::kXBytes + R::kGBytes);
+        tma_load_1d(ring + stage * R::kXBytes, static_cast<const XT *>(p.x) + off, R::kXBytes, &full[stage]);
+        if constexpr (HAS_G)
+            tma_load_1d(ring + 2 * R::kXBytes + stage * R::kGBytes, static_cast<const GT *>(p.g) + off,
+                        R::kGBytes, &full[stage]);
+    };
+    unsigned phase[2] = {0u, 0u};
+    if (threadIdx.x == 0 && blockIdx.x < items && staged(blockIdx.x)) issue(blockIdx.x, 0);
+
+    int it = 0;
+    for (long long w = blockIdx.x; w < items; w += gridDim.x, ++it) {
+        const int t = static_cast<int>(w / k);
+        const int a = static_cast<int>(w % k);
+        const long long base = static_cast<long long>(t) * kTile;
+        const long long rem = count - base;
+        const int stage = it & 1;
+        // prefetch the next item of this CTA while this one is processed
+        const long long wn = w + gridDim.x;
+        if (threadIdx.x == 0 && wn < items && staged(wn)) issue(wn, stage ^ 1);
+
+        // ---- Eq. 4 local update (ATC) or plain input (neighbor_allreduce) ----
+        float xh[kVecPerThread][4];
+        if (staged(w)) {
+            mbar_wait(&full[stage], phase[stage]);
+            phase[stage] ^= 1u;
+            const XT *xs = reinterpret_cast<const XT *>(ring + stage * R::kXBytes);
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j) Vec4<XT>::load(xs + tile_elem(j), xh[j], 4, true);
+            if constexpr (HAS_G) {
+                const GT *gs = reinterpret_cast<const GT *>(ring + 2 * R::kXBytes + stage * R::kGBytes);
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j) {
+                    float gv[4];
+                    Vec4<GT>::load(gs + tile_elem(j), gv, 4, true);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
+                }
+            }
+        } else {
+            const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(a) * count + base;
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+                Vec4<XT>::load(xr + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
+            if constexpr (HAS_G) {
+                const GT *gr = static_cast<const GT *>(p.g) + static_cast<long long>(a) * count + base;
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j) {
+                    float gv[4];
+                    Vec4<GT>::load(gr + tile_elem(j), gv, clamp_valid(rem, tile_elem(j)), vec);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
+                }
+            }
         }
-        for (int i = 0; i < P::SP; ++i) {
-            mbar_init(&full_pr[i], 32);
-            mbar_init(&empty_pr[i], kConsumerWarps);
+
+        // ---- publish the wire copy into this agent's slot, release flag ----
+        WT *mine = at<WT>(g.peer_base[g.me], p.slot_off + a * p.slot_agent_stride +
+                                                 parity * p.slot_parity_stride) + base;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+            Vec4<WT>::store(mine + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            st_release(ready_ptr(g, p.ready_off, p.ready_stride, g.me * k + a, t), e, sys);
+
+        // ---- wait for the in-neighbours' tile t ----
+        const int ns = st.nsrc[a];
+        if (threadIdx.x < ns) {
+            if (!spin_ge(g, ready_ptr(g, p.ready_off, p.ready_stride, st.src[a][threadIdx.x], t), e, sys))
+                s_fail = 1;
+        }
+        __syncthreads();
+        if (s_fail) {
+            // drain the in-flight prefetch before the CTA exits (its smem may be reused)
+            if (threadIdx.x == 0 && wn < items && staged(wn)) mbar_wait(&full[stage ^ 1], phase[stage ^ 1]);
+            return;
+        }
+
+        // ---- Eq. 5 / Eq. 9 weighted combine in fp32 ----
+        float acc[kVecPerThread][4];
+        const float cs = st.self_w[a];
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[j][i] = cs * xh[j][i];
+        for (int q = 0; q < ns; ++q) {
+            const int src = st.src[a][q];
+            const float c = st.coef[a][q];
+            const WT *sp = at<const WT>(g.peer_base[src / k],
+                                        p.slot_off + (src % k) * p.slot_agent_stride +
+                                            parity * p.slot_parity_stride) + base;
+            float v[kVecPerThread][4];
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+                Vec4<WT>::load_cg(sp + tile_elem(j), v[j], clamp_valid(rem, tile_elem(j)), vec);
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(c, v[j][i], acc[j][i]);
+        }
+
+        // ---- store (cast) ----
+        YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+            Vec4<YT>::store(yr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+        if (p.shadow) {
+            bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base;
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+                Vec4<bf16>::store(sr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+        }
+    }
+
+    last_cta(pad, [&] {
+        pad->epoch = e;
+        if (p.wmode == kWSchedule) pad->round = pad->round + 1;
+        publish_done(g, e);
+    });
+}
+
+#ifndef BF_LAG
+#define BF_LAG 3
+#endif
+#ifndef BF_PSTAGES
+#define BF_PSTAGES 3
+#endif
+#ifndef BF_CSTAGES
+#define BF_CSTAGES 2
+#endif
+#ifndef BF_NPEER
+#define BF_NPEER 2
+#endif
+constexpr int kConsumerWarps = kThreads / 32;          // 8 consumer warps
+constexpr int kExchThreads = kThreads + 96;            // + 2 producer warps + 1 signal warp
+constexpr int kPub = 16;                               // ring of "published" notifications
+
+// Walks the items w = first, first + stride, ... as (tile t, local agent a)
+// with w = t*k + a, without integer division in the loop.
+struct ItemIt {
+    int t, a, dt, da, k;
+    __device__ ItemIt(int first, int stride, int k_) : t(first / k_), a(first % k_), dt(stride / k_),
+                                                          da(stride % k_), k(k_) {}
+    __device__ __forceinline__ void next() {
+        t += dt;
+        a += da;
+        if (a >= k) {
+            a -= k;
+            ++t;
+        }
+    }
+};
+
+// Per-CTA shared-memory pipelines.
+//   publish ring (PS stages): x / g tile of an item to publish (DRAM reads in flight)
+//   combine ring (CS stages): the tiles combined for an item.  When the wire copy
+//   IS the fp32 x_half (fp32 wire, or neighbor_allreduce) the self term is the
+//   agent's own published tile, staged like a neighbour's (an L2 hit); for ATC
+//   with a bf16 wire the stage re-reads x / g to recompute the fp32 x_half (R18).
+template <typename XT, typename GT, typename WT, bool HAS_G>
+struct Pipe {
+    static constexpr int D = BF_LAG, PS = BF_PSTAGES, CS = BF_CSTAGES, NP = BF_NPEER;
+    static constexpr bool SELF_XG = HAS_G && sizeof(WT) < 4;
+    static constexpr unsigned XB = kTile * sizeof(XT);
+    static constexpr unsigned GB = HAS_G ? kTile * sizeof(GT) : 0;
+    static constexpr unsigned PB = kTile * sizeof(WT);
+    static constexpr unsigned XG = XB + GB;
+    static constexpr int NT = NP + (SELF_XG ? 0 : 1);               // staged tiles per combine stage
+    static constexpr unsigned CST = (SELF_XG ? XG : 0) + NT * PB;
+    static constexpr unsigned BYTES = PS * XG + CS * CST;
+};
+
+// exchange_pipe_kernel: warp-specialised persistent pipeline, one CTA per SM
+// (alternative to exchange_kernel, selected with BF_EXCH=pipe).
+//   producer A : TMA bulk loads of the x / g tiles of items to publish
+//   producer B : TMA bulk loads of the x / g tiles of items to combine (L2 hits,
+//                they were published D items earlier), then acquire the
+//                in-neighbours' ready flags of the tile and LDGSTS (cp.async)
+//                their published tiles -- over NVLink for agents on other GPUs,
+//                from L2 for agents on this GPU
+//   signal     : releases the ready flag of every published tile (the release
+//                fence runs off the consumers' critical path)
+//   consumers  : iteration c publishes item c+D (Eq. 4 adapt, wire copy into
+//                this agent's IPC slot) and combines item c (Eq. 5 / Eq. 9,
+//                fp32) from shared memory.
+// Publishing D items ahead means a neighbour's tile is normally published long
+// before anybody needs it.  Deadlock freedom: items are visited in increasing
+// tile order; publish-side loads never wait on other agents; a tile is
+// published before its owner waits on the tile of any later item; all CTAs are
+// co-resident (cooperative launch) and grid >= local agents.  A fault never
+// exits early: waits fail fast, garbage is computed, the fault is latched, and
+// no TMA or cp.async is left in flight.
+template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
+__global__ void __launch_bounds__(kExchThreads, 1) exchange_pipe_kernel(const __grid_constant__ ExchParams p) {
+    using P = Pipe<XT, GT, WT, HAS_G>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ SharedTab st;
+    __shared__ __align__(8) unsigned long long fullP[P::PS], emptyP[P::PS];
+    __shared__ __align__(8) unsigned long long published[kPub], signaled[kPub];
+    __shared__ __align__(8) unsigned long long fullC[P::CS], emptyC[P::CS];
+    __shared__ int s_fail, drain_fail;
+    volatile int *const fail = &s_fail;
+    const Geometry &g = p.geo;
+    Pad *pad = pad_of(g, g.me);
+    if (aborted(g)) return;
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
+    const int parity = static_cast<int>(e & 1);
+    const bool sys = g.nprocs > 1;   // flags of agents on other GPUs need system scope
+
+    if (threadIdx.x == 0) {
+        s_fail = 0;
+        drain_fail = 0;
+        for (int i = 0; i < P::PS; ++i) {
+            mbar_init(&fullP[i], 1);
+            mbar_init(&emptyP[i], kConsumerWarps);
+        }
+        for (int i = 0; i < kPub; ++i) {
+            mbar_init(&published[i], kConsumerWarps);
+            mbar_init(&signaled[i], 1);
+        }
+        for (int i = 0; i < P::CS; ++i) {
+            mbar_init(&fullC[i], 1 + 32);                 // TMA / plain arrive + 32 cp.async lanes
+            mbar_init(&emptyC[i], kConsumerWarps);
         }
         fence_mbar_init();
     }
@@ -251,60 +453,90 @@ __global__ void __launch_bounds__(kExchThreads, 1) exchange_kernel(const __grid_
     const bool vec = g.vec_ok != 0;
     const long long count = g.count;
     const int k = g.k;
-    const long long items = static_cast<long long>(k) * g.T;
-    const int nmine = blockIdx.x < items ? static_cast<int>((items - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
-    auto item = [&](int c) { return blockIdx.x + static_cast<long long>(c) * gridDim.x; };
-    auto staged = [&](long long w) {   // TMA needs 16B-aligned rows and a full tile
-        return vec && (count - static_cast<long long>(w / k) * kTile) >= kTile;
-    };
-    auto xs = [&](int s) { return smem + s * P::XG; };
-    auto gs = [&](int s) { return smem + s * P::XG + P::XB; };
-    auto ps = [&](int s, int q) { return smem + P::SX * P::XG + (s * P::NP + q) * P::PB; };
+    const int items = k * g.T;
+    const int nfull = static_cast<int>(count / kTile);   // tiles that are full
+    const int nmine = static_cast<int>(blockIdx.x) < items
+                          ? (items - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                                static_cast<int>(gridDim.x)
+                          : 0;
+    auto staged = [&](int t) { return vec && t < nfull; };   // TMA needs 16B-aligned rows and a full tile
+    unsigned char *const ringP = smem;
+    unsigned char *const ringC = smem + P::PS * P::XG;
+    auto xP = [&](int s) { return ringP + s * P::XG; };
+    auto xC = [&](int s) { return ringC + s * P::CST; };
+    auto tC = [&](int s, int q) { return ringC + s * P::CST + (P::SELF_XG ? P::XG : 0) + q * P::PB; };
     auto slot_of = [&](int agent) {
         return at<WT>(g.peer_base[agent / k],
                       p.slot_off + (agent % k) * p.slot_agent_stride + parity * p.slot_parity_stride);
     };
     auto failed = [&]() { return *reinterpret_cast<volatile int *>(&s_fail) != 0; };
+    auto tma_xg = [&](int t, int a, unsigned char *dst, unsigned long long *bar) {   // lane 0 only
+        const long long off = static_cast<long long>(a) * count + static_cast<long long>(t) * kTile;
+        fence_proxy_async();
+        mbar_expect_tx(bar, P::XG);
+        tma_load_1d(dst, static_cast<const XT *>(p.x) + off, P::XB, bar);
+        if constexpr (HAS_G) tma_load_1d(dst + P::XB, static_cast<const GT *>(p.g) + off, P::GB, bar);
+    };
+    // agent whose published tile is staged in tile slot q of a combine stage
+    auto staged_agent = [&](int a, int q) {
+        if constexpr (P::SELF_XG) return static_cast<int>(st.src[a][q]);
+        return q == 0 ? g.me * k + a : static_cast<int>(st.src[a][q - 1]);
+    };
+    auto n_staged = [&](int a) { return min(st.nsrc[a], P::NP) + (P::SELF_XG ? 0 : 1); };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (warp == kConsumerWarps) {
-        // ===================== producer A: x / g tiles (TMA) =====================
-        for (int c = 0; c < nmine; ++c) {
-            const int s = c % P::SX;
-            if (c >= P::SX) mbar_wait(&empty_xg[s], static_cast<unsigned>(c / P::SX - 1) & 1u);
+        // ====================== producer A: publish-side x / g ======================
+        ItemIt it(blockIdx.x, gridDim.x, k);
+        int issued = 0;
+        for (int c = 0; c < nmine; ++c, it.next()) {
+            const int s = c % P::PS;
+            bool okw = true;   // lane 0 waits, the warp follows its verdict (no divergent break)
+            if (c >= P::PS && lane == 0) okw = mbar_wait_b(g, &emptyP[s], static_cast<unsigned>(c / P::PS - 1) & 1u, fail);
+            if (!__shfl_sync(0xffffffffu, okw, 0)) break;
+            issued = c + 1;
             if (lane == 0) {
-                const long long w = item(c);
-                if (staged(w)) {
-                    const long long off = static_cast<long long>(w % k) * count + (w / k) * kTile;
-                    fence_proxy_async();
-                    mbar_expect_tx(&full_xg[s], P::XG);
-                    tma_load_1d(xs(s), static_cast<const XT *>(p.x) + off, P::XB, &full_xg[s]);
-                    if constexpr (HAS_G) tma_load_1d(gs(s), static_cast<const GT *>(p.g) + off, P::GB, &full_xg[s]);
-                } else {
-                    mbar_arrive(&full_xg[s]);
-                }
+                if (staged(it.t))
+                    tma_xg(it.t, it.a, xP(s), &fullP[s]);
+                else
+                    mbar_arrive(&fullP[s]);
             }
             __syncwarp();
         }
+        // drain: every armed phase completes before the CTA can exit
+        if (lane == 0)
+            for (int c = max(0, issued - P::PS); c < issued; ++c)
+                mbar_wait_b(g, &fullP[c % P::PS], static_cast<unsigned>(c / P::PS) & 1u, &drain_fail);
     } else if (warp == kConsumerWarps + 1) {
-        // ============ producer B: in-neighbour tiles (flag-gated cp.async) ============
-        for (int c = 0; c < nmine; ++c) {
-            const int s = c % P::SP;
-            if (c >= P::SP) mbar_wait(&empty_pr[s], static_cast<unsigned>(c / P::SP - 1) & 1u);
-            const long long w = item(c);
-            const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        // ========== producer B: the published tiles combined for each item ==========
+        ItemIt it(blockIdx.x, gridDim.x, k);
+        int issued = 0;
+        for (int c = 0; c < nmine; ++c, it.next()) {
+            const int s = c % P::CS;
+            bool okw = true;
+            if (c >= P::CS && lane == 0) okw = mbar_wait_b(g, &emptyC[s], static_cast<unsigned>(c / P::CS - 1) & 1u, fail);
+            if (!__shfl_sync(0xffffffffu, okw, 0)) break;
+            issued = c + 1;
+            const int t = it.t, a = it.a;
             const long long base = static_cast<long long>(t) * kTile;
-            const int np = min(st.nsrc[a], P::NP);
+            if (lane == 0) {
+                if (P::SELF_XG && staged(t))
+                    tma_xg(t, a, xC(s), &fullC[s]);
+                else
+                    mbar_arrive(&fullC[s]);
+            }
+            const int nt = n_staged(a);
             bool good = true;
-            if (lane < np && !failed())
-                good = spin_ge(g, ready_ptr(g, p.ready_off, p.ready_stride, st.src[a][lane], t), e, sys);
+            if (lane < nt && !failed())
+                good = spin_ge(g, ready_ptr(g, p.ready_off, p.ready_stride, staged_agent(a, lane), t), e, sys);
             if (!__all_sync(0xffffffffu, good) && lane == 0) s_fail = 1;
             __syncwarp();
             if (!failed()) {
                 const long long rem_bytes = (count - base) * static_cast<long long>(sizeof(WT));
-                for (int q = 0; q < np; ++q) {
-                    const unsigned char *src = reinterpret_cast<const unsigned char *>(slot_of(st.src[a][q]) + base);
-                    unsigned char *dst = ps(s, q);
+                for (int q = 0; q < nt; ++q) {
+                    const unsigned char *src =
+                        reinterpret_cast<const unsigned char *>(slot_of(staged_agent(a, q)) + base);
+                    unsigned char *dst = tC(s, q);
 #pragma unroll 4
                     for (int ch = lane; ch < static_cast<int>(P::PB / 16); ch += 32) {
                         const long long left = rem_bytes - 16ll * ch;
@@ -313,37 +545,44 @@ __global__ void __launch_bounds__(kExchThreads, 1) exchange_kernel(const __grid_
                     }
                 }
             }
-            cp_async_mbar_arrive_noinc(&full_pr[s]);
+            cp_async_mbar_arrive_noinc(&fullC[s]);
         }
+        if (lane == 0)
+            for (int c = max(0, issued - P::CS); c < issued; ++c)
+                mbar_wait_b(g, &fullC[c % P::CS], static_cast<unsigned>(c / P::CS) & 1u, &drain_fail);
     } else if (warp == kConsumerWarps + 2) {
-        // ======== signal warp: release the ready flag of every published tile ========
-        // (the release fence runs here, off the consumers' critical path)
-        for (int c = 0; c < nmine; ++c) {
-            const int s = c % P::SX;
-            mbar_wait(&published[s], static_cast<unsigned>(c / P::SX) & 1u);
-            if (lane == 0) {
-                const long long w = item(c);
-                st_release(ready_ptr(g, p.ready_off, p.ready_stride, g.me * k + static_cast<int>(w % k),
-                                     static_cast<int>(w / k)),
-                           e, sys);
-                mbar_arrive(&empty_xg[s]);
+        // ======== signal warp: release the ready flags of published tiles ========
+        // One release fence covers every tile already published (batch), so the
+        // fence cost is paid per batch, not per tile, and never by the consumers.
+        if (lane == 0) {
+            ItemIt it(blockIdx.x, gridDim.x, k);
+            int c = 0;
+            while (c < nmine) {
+                const bool okp = mbar_wait_b(g, &published[c % kPub], static_cast<unsigned>(c / kPub) & 1u, fail);
+                int c_end = c + 1;
+                while (okp && c_end < nmine && c_end - c < kPub / 2 &&
+                       mbar_test(&published[c_end % kPub], static_cast<unsigned>(c_end / kPub) & 1u))
+                    ++c_end;
+                if (okp) fence_acq_rel(sys);
+                for (int i = c; i < c_end; ++i, it.next()) {
+                    if (okp) st_relaxed(ready_ptr(g, p.ready_off, p.ready_stride, g.me * k + it.a, it.t), e, sys);
+                    mbar_arrive(&signaled[i % kPub]);
+                }
+                c = c_end;
             }
-            __syncwarp();
         }
+        __syncwarp();
     } else {
         // =============================== consumers ===============================
-        // x_half of item c, from the staged tiles or straight from global memory
-        auto adapt = [&](int c, float (&xh)[kVecPerThread][4]) {
-            const long long w = item(c);
-            const int sx = c % P::SX;
-            const int a = static_cast<int>(w % k);
-            const long long base = (w / k) * kTile, rem = count - base;
-            if (staged(w)) {
-                const XT *xsm = reinterpret_cast<const XT *>(xs(sx));
+        // x_half of item (t, a) from a staged x/g tile, or straight from global memory
+        auto adapt = [&](int t, int a, const unsigned char *stage, float (&xh)[kVecPerThread][4]) {
+            const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+            if (staged(t)) {
+                const XT *xsm = reinterpret_cast<const XT *>(stage);
 #pragma unroll
                 for (int j = 0; j < kVecPerThread; ++j) Vec4<XT>::load(xsm + tile_elem(j), xh[j], 4, true);
                 if constexpr (HAS_G) {
-                    const GT *gsm = reinterpret_cast<const GT *>(gs(sx));
+                    const GT *gsm = reinterpret_cast<const GT *>(stage + P::XB);
 #pragma unroll
                     for (int j = 0; j < kVecPerThread; ++j) {
                         float gv[4];
@@ -369,42 +608,63 @@ __global__ void __launch_bounds__(kExchThreads, 1) exchange_kernel(const __grid_
                 }
             }
         };
+        ItemIt itP(blockIdx.x, gridDim.x, k);   // next item to publish
+        ItemIt itC(blockIdx.x, gridDim.x, k);   // next item to combine
         for (int c = -P::D; c < nmine; ++c) {
-            // ---- publish item c + D: Eq. 4 local update, wire copy, release flag ----
+            // ---- publish item c + D: Eq. 4 local update, wire copy into the slot ----
             const int cp = c + P::D;
-            if (cp < nmine) {
-                const long long w = item(cp);
-                const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+            if (cp >= 0 && cp < nmine) {
+                const int s = cp % P::PS;
+                const int t = itP.t, a = itP.a;
                 const long long base = static_cast<long long>(t) * kTile, rem = count - base;
-                mbar_wait(&full_xg[cp % P::SX], static_cast<unsigned>(cp / P::SX) & 1u);
+                mbar_wait_b(g, &fullP[s], static_cast<unsigned>(cp / P::PS) & 1u, fail);
                 float xh[kVecPerThread][4];
-                adapt(cp, xh);
+                adapt(t, a, xP(s), xh);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyP[s]);   // x / g consumed: producer A may refill
                 WT *mine = slot_of(g.me * k + a) + base;
 #pragma unroll
                 for (int j = 0; j < kVecPerThread; ++j)
                     Vec4<WT>::store(mine + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), true);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&published[cp % P::SX]);   // the signal warp releases the flag
-                (void)t;
+                if (lane == 0) {
+                    if (cp >= kPub)   // the signal warp has consumed the notification kPub items back
+                        mbar_wait_b(g, &signaled[cp % kPub], static_cast<unsigned>(cp / kPub - 1) & 1u, fail);
+                    mbar_arrive(&published[cp % kPub]);   // the signal warp releases the flag
+                }
+                itP.next();
             }
             if (c < 0) continue;
             // ---- combine item c: Eq. 5 / Eq. 9 in fp32 ----
-            const long long w = item(c);
-            const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+            const int t = itC.t, a = itC.a;
+            itC.next();
             const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+            const int s = c % P::CS;
+            mbar_wait_b(g, &fullC[s], static_cast<unsigned>(c / P::CS) & 1u, fail);
             float acc[kVecPerThread][4];
-            adapt(c, acc);   // x_half again (self term uses the fp32 x_half, R18)
             const float cs = st.self_w[a];
+            int q0 = 0;
+            if constexpr (P::SELF_XG) {
+                adapt(t, a, xC(s), acc);   // fp32 x_half for the self term (R18)
 #pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j)
+                for (int j = 0; j < kVecPerThread; ++j)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) acc[j][i] *= cs;
+                    for (int i = 0; i < 4; ++i) acc[j][i] *= cs;
+            } else {
+                // own published tile == the fp32 x_half (fp32 wire) or x itself
+                const WT *sm0 = reinterpret_cast<const WT *>(tC(s, 0));
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j) {
+                    Vec4<WT>::load(sm0 + tile_elem(j), acc[j], 4, true);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[j][i] *= cs;
+                }
+                q0 = 1;
+            }
             const int ns = st.nsrc[a];
             const int np = min(ns, P::NP);
-            const int sp = c % P::SP;
-            mbar_wait(&full_pr[sp], static_cast<unsigned>(c / P::SP) & 1u);
             for (int q = 0; q < np; ++q) {
-                const WT *psm = reinterpret_cast<const WT *>(ps(sp, q));
+                const WT *psm = reinterpret_cast<const WT *>(tC(s, q0 + q));
                 const float cq = st.coef[a][q];
 #pragma unroll
                 for (int j = 0; j < kVecPerThread; ++j) {
@@ -434,10 +694,7 @@ __global__ void __launch_bounds__(kExchThreads, 1) exchange_kernel(const __grid_
                 }
             }
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&empty_xg[c % P::SX]);
-                mbar_arrive(&empty_pr[sp]);
-            }
+            if (lane == 0) mbar_arrive(&emptyC[s]);
             YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base;
 #pragma unroll
             for (int j = 0; j < kVecPerThread; ++j)
@@ -639,23 +896,24 @@ int max_coresident(const void *func, int threads, size_t smem) {
 
 template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
 static cudaError_t launch_exch_t(const ExchParams &p, int grid, cudaStream_t s) {
-    auto fn = exchange_kernel<XT, GT, WT, YT, HAS_G>;
-    const unsigned smem = Pipe<XT, GT, WT, HAS_G>::BYTES;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const bool pipe = p.kernel == 1;
+    const void *fn = pipe ? reinterpret_cast<const void *>(exchange_pipe_kernel<XT, GT, WT, YT, HAS_G>)
+                          : reinterpret_cast<const void *>(exchange_kernel<XT, GT, WT, YT, HAS_G>);
+    const unsigned smem = pipe ? Pipe<XT, GT, WT, HAS_G>::BYTES : Ring<XT, GT, HAS_G>::kBytes;
+    const int threads = pipe ? kExchThreads : kThreads;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[pipe]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set[pipe] = true;
     }
-    const int maxg = max_coresident(reinterpret_cast<const void *>(fn), kExchThreads, smem);
+    const int maxg = max_coresident(fn, threads, smem);
     if (grid <= 0 || grid > maxg) grid = maxg;
     const long long items = static_cast<long long>(p.geo.k) * p.geo.T;
     if (grid > items) grid = static_cast<int>(items < p.geo.k ? p.geo.k : items);
     if (grid < 1) grid = 1;
     void *args[] = {const_cast<ExchParams *>(&p)};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(kExchThreads), args,
-                                       smem, s);
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, s);
 }
 
 cudaError_t launch_exchange(const ExchParams &p, int x_kind, int g_kind, int wire_kind, int y_kind,

@@ -84,6 +84,7 @@ struct bf_ctx {
     std::vector<double> WM;
     int sched_kind = 0;
     int topo_check = 1;
+    int exch_kernel = 0;                      // BF_EXCH=pipe selects the warp-specialised pipeline
     // exchange region
     size_t exch_cap = 0;                      // bytes per agent per parity
     size_t exch_begin = 0, exch_top = 0;      // heap range of exchange (+ hierarchical) regions
@@ -397,6 +398,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     c->device = cuda_device;
     c->heap_bytes = heap_bytes;
     if (const char *t = getenv("BF_TIMEOUT_MS")) c->timeout_ns = strtoull(t, nullptr, 10) * 1000000ull;
+    if (const char *x = getenv("BF_EXCH")) c->exch_kernel = strcmp(x, "pipe") == 0 ? 1 : 0;
     cudaError_t e = cudaMalloc(&c->heap, heap_bytes);
     if (e != cudaSuccess) {
         delete c;
@@ -610,6 +612,7 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     p.slot_parity_stride = c->exch_cap;
     p.ready_off = c->ready_off;
     p.ready_stride = c->ready_stride;
+    p.kernel = c->exch_kernel;
     CU(launch_exchange(p, x_kind, g_kind, wire_kind, y_kind, g != nullptr, 0, st));
     c->launches++;
     return BF_OK;

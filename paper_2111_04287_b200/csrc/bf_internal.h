@@ -103,7 +103,10 @@ struct ExchParams {
     int ready_stride;
     int wmode;
     int check;
-    int kernel;                             // 0: exchange_kernel (default), 1: exchange_pipe_kernel
+    int kernel;                             // 0: per-tile flags, 1: warp-specialised pipeline, 2: chunked
+    int chunk_tiles;                        // kernel 2: tiles per chunk
+    unsigned long long ccnt_off;            // kernel 2: u32 [tmax] per-chunk CTA counters (local)
+    unsigned long long cflag_off;           // kernel 2: u64 [tmax] per-chunk release flags
     SrcTab tab;                             // kWStatic: final coefficients; kWDynamic: declared r
     DynDecl dyn;
 };

@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, BF_MINB) exchange_kernel(const __gri
         // ---- Eq. 4 local update (ATC) or plain input (neighbor_allreduce) ----
         float xh[kVecPerThread][4];
         if (staged(w)) {
-            mbar_wait(&full[stage], phase[stage]);
+            mbar_wait_b(g, &full[stage], phase[stage], &s_fail);
             phase[stage] ^= 1u;
             const XT *xs = reinterpret_cast<const XT *>(ring + stage * R::kXBytes);
 #pragma unroll
@@ -292,7 +292,10 @@ __global__ void __launch_bounds__(kThreads, BF_MINB) exchange_kernel(const __gri
         __syncthreads();
         if (s_fail) {
             // drain the in-flight prefetch before the CTA exits (its smem may be reused)
-            if (threadIdx.x == 0 && wn < items && staged(wn)) mbar_wait(&full[stage ^ 1], phase[stage ^ 1]);
+            if (threadIdx.x == 0 && wn < items && staged(wn)) {
+                volatile int no_fail = 0;
+                mbar_wait_b(g, &full[stage ^ 1], phase[stage ^ 1], &no_fail);
+            }
             return;
         }
 
@@ -718,6 +721,214 @@ __global__ void __launch_bounds__(kExchThreads, 1) exchange_pipe_kernel(const __
 }
 
 // --------------------------------------------------------------------------
+// exchange_chunk_kernel (kernel 2, default): chunk-granular synchronisation.
+// The tiles are grouped into chunks of CT tiles (per agent).  Every CTA walks
+// its items (grid-stride, tile-major) twice: it PUBLISHES them (Eq. 4 adapt,
+// wire copy into the IPC slot) and COMBINES them (Eq. 5 / Eq. 9), the combine
+// of chunk c running after the CTA has published everything up to chunk c+1.
+// A CTA that has published all its items of a chunk bumps the chunk's counter;
+// the CTA that completes the count releases the chunk flag once (system scope
+// if other GPUs read it).  A combine waits once per chunk for the chunk flags
+// of every process -- no per-tile flag traffic, no per-tile fences, and the
+// one-chunk lag means the flags are normally already set.
+// Deadlock freedom: a CTA never waits while holding an un-counted chunk that a
+// waiter needs (it publishes chunk c+1 before waiting for chunk c), and all CTAs
+// are co-resident (cooperative launch).
+template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
+__global__ void __launch_bounds__(kThreads, BF_MINB) exchange_chunk_kernel(const __grid_constant__ ExchParams p) {
+    using R = Ring<XT, GT, HAS_G>;
+    extern __shared__ __align__(128) unsigned char ring[];
+    __shared__ SharedTab st;
+    __shared__ __align__(8) unsigned long long full[2];
+    __shared__ int s_fail;
+    const Geometry &g = p.geo;
+    Pad *pad = pad_of(g, g.me);
+    if (aborted(g)) return;
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
+    const int parity = static_cast<int>(e & 1);
+    const bool sys = g.nprocs > 1;
+    if (threadIdx.x == 0) {
+        s_fail = 0;
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+    }
+    bool ok = war_wait(g, e);
+    if (p.wmode == kWDynamic) write_descriptors(p, e);
+    ok = resolve_sources(p, e, st) && ok;
+    if (!ok) return;   // fault latched; nothing in flight yet
+
+    const bool vec = g.vec_ok != 0;
+    const long long count = g.count;
+    const int k = g.k, G = gridDim.x;
+    const int items = k * g.T;
+    const int CT = p.chunk_tiles;
+    const int NC = (g.T + CT - 1) / CT;
+    const int nfull = static_cast<int>(count / kTile);
+    const int nmine = static_cast<int>(blockIdx.x) < items ? (items - static_cast<int>(blockIdx.x) + G - 1) / G : 0;
+    unsigned *cnt = at<unsigned>(g.peer_base[g.me], p.ccnt_off);
+    unsigned long long *cflag = at<unsigned long long>(g.peer_base[g.me], p.cflag_off);
+    auto staged = [&](int t) { return vec && t < nfull; };
+    auto slot_of = [&](int agent) {
+        return at<WT>(g.peer_base[agent / k],
+                      p.slot_off + (agent % k) * p.slot_agent_stride + parity * p.slot_parity_stride);
+    };
+    auto issue = [&](const ItemIt &it, int stage) {   // thread 0: TMA of the x / g tiles of a publish item
+        const long long off = static_cast<long long>(it.a) * count + static_cast<long long>(it.t) * kTile;
+        fence_proxy_async();
+        mbar_expect_tx(&full[stage], R::kXBytes + R::kGBytes);
+        tma_load_1d(ring + stage * R::kXBytes, static_cast<const XT *>(p.x) + off, R::kXBytes, &full[stage]);
+        if constexpr (HAS_G)
+            tma_load_1d(ring + 2 * R::kXBytes + stage * R::kGBytes, static_cast<const GT *>(p.g) + off, R::kGBytes,
+                        &full[stage]);
+    };
+    // x_half of (t, a) from global memory (unstaged publish items, bf16-wire self terms)
+    auto adapt_global = [&](int t, int a, float (&xh)[kVecPerThread][4]) {
+        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(a) * count + base;
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j)
+            Vec4<XT>::load(xr + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
+        if constexpr (HAS_G) {
+            const GT *gr = static_cast<const GT *>(p.g) + static_cast<long long>(a) * count + base;
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j) {
+                float gv[4];
+                Vec4<GT>::load(gr + tile_elem(j), gv, clamp_valid(rem, tile_elem(j)), vec);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
+            }
+        }
+    };
+
+    int counted = 0;   // this CTA has counted chunks [0, counted)
+    auto count_upto = [&](int c_excl) {   // uniform
+        __syncthreads();   // every slot store of this CTA for those chunks is issued (CTA scope)
+        if (threadIdx.x == 0) {
+            __threadfence();   // ... and visible at GPU scope before the counters
+            for (int c = counted; c < c_excl; ++c) {
+                const unsigned old = atomicAdd(&cnt[c], 1u);
+                if (old == static_cast<unsigned>(G) - 1) {   // last CTA of this GPU for chunk c
+                    cnt[c] = 0;
+                    fence_acq_rel(sys);
+                    st_relaxed(&cflag[c], e, sys);
+                }
+            }
+        }
+        counted = c_excl;
+    };
+
+    ItemIt pub(blockIdx.x, G, k), comb(blockIdx.x, G, k);
+    int mp = 0, mc = 0, waited = -1, it_pub = 0;
+    unsigned phase[2] = {0u, 0u};
+    if (threadIdx.x == 0 && nmine > 0 && staged(pub.t)) issue(pub, 0);
+    if (nmine == 0) count_upto(NC);
+    bool failed = false;
+    while (mp < nmine || mc < nmine) {
+        const bool do_pub = mp < nmine && (mc >= nmine || pub.t / CT <= comb.t / CT + 1);
+        if (do_pub) {
+            // ---- publish item mp ----
+            const int t = pub.t, a = pub.a;
+            const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+            const int stage = it_pub & 1;
+            ItemIt nxt = pub;
+            nxt.next();
+            // every warp has finished reading stage^1 (item mp-1) and has waited on its
+            // phase before thread 0 re-arms it: a barrier can never run two phases ahead
+            __syncthreads();
+            if (threadIdx.x == 0 && mp + 1 < nmine && staged(nxt.t)) issue(nxt, stage ^ 1);
+            float xh[kVecPerThread][4];
+            if (staged(t)) {
+                mbar_wait_b(g, &full[stage], phase[stage], &s_fail);
+                phase[stage] ^= 1u;
+                const XT *xs = reinterpret_cast<const XT *>(ring + stage * R::kXBytes);
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j) Vec4<XT>::load(xs + tile_elem(j), xh[j], 4, true);
+                if constexpr (HAS_G) {
+                    const GT *gs = reinterpret_cast<const GT *>(ring + 2 * R::kXBytes + stage * R::kGBytes);
+#pragma unroll
+                    for (int j = 0; j < kVecPerThread; ++j) {
+                        float gv[4];
+                        Vec4<GT>::load(gs + tile_elem(j), gv, 4, true);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
+                    }
+                }
+            } else {
+                adapt_global(t, a, xh);
+            }
+            WT *mine = slot_of(g.me * k + a) + base;
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+                Vec4<WT>::store(mine + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), true);
+            ++it_pub;
+            ++mp;
+            pub = nxt;
+            const int next_chunk = mp < nmine ? pub.t / CT : NC;
+            if (next_chunk > counted) count_upto(next_chunk);
+        } else {
+            // ---- combine item mc (its chunk's flags: once per chunk) ----
+            const int t = comb.t, a = comb.a;
+            const int cc = t / CT;
+            if (cc != waited) {
+                bool good = true;
+                if (threadIdx.x < g.nprocs && !failed)
+                    good = spin_ge(g, at<unsigned long long>(g.peer_base[threadIdx.x], p.cflag_off) + cc, e, sys);
+                failed = !__syncthreads_and(good) || failed;
+                waited = cc;
+            }
+            const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+            float acc[kVecPerThread][4];
+            const float cs = st.self_w[a];
+            if constexpr (HAS_G && sizeof(WT) < 4) {
+                adapt_global(t, a, acc);   // fp32 x_half for the self term (R18); L2 hit
+            } else {
+                const WT *own = slot_of(g.me * k + a) + base;   // == fp32 x_half (or x)
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j)
+                    Vec4<WT>::load_cg(own + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), true);
+            }
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[j][i] *= cs;
+            const int ns = st.nsrc[a];
+            for (int q = 0; q < ns; ++q) {
+                const WT *sp = slot_of(st.src[a][q]) + base;
+                const float c = st.coef[a][q];
+                float v[kVecPerThread][4];
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j)
+                    Vec4<WT>::load_cg(sp + tile_elem(j), v[j], clamp_valid(rem, tile_elem(j)), true);
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(c, v[j][i], acc[j][i]);
+            }
+            YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base;
+#pragma unroll
+            for (int j = 0; j < kVecPerThread; ++j)
+                Vec4<YT>::store(yr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+            if (p.shadow) {
+                bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base;
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j)
+                    Vec4<bf16>::store(sr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+            }
+            comb.next();
+            ++mc;
+        }
+    }
+    if (counted < NC) count_upto(NC);
+    if (failed) return;
+    last_cta(pad, [&] {
+        pad->epoch = e;
+        if (p.wmode == kWSchedule) pad->round = pad->round + 1;
+        publish_done(g, e);
+    });
+}
+
+// --------------------------------------------------------------------------
 // Hierarchical neighbour allreduce: leader-free, sliced.
 //   A: publish x tile t -> slot, flag
 //   B: agent (m,l) averages slice l over its machine's L agents (1/L, R12)
@@ -896,16 +1107,18 @@ int max_coresident(const void *func, int threads, size_t smem) {
 
 template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
 static cudaError_t launch_exch_t(const ExchParams &p, int grid, cudaStream_t s) {
-    const bool pipe = p.kernel == 1;
+    const int kind = p.kernel;
+    const bool pipe = kind == 1;
     const void *fn = pipe ? reinterpret_cast<const void *>(exchange_pipe_kernel<XT, GT, WT, YT, HAS_G>)
-                          : reinterpret_cast<const void *>(exchange_kernel<XT, GT, WT, YT, HAS_G>);
+                          : (kind == 2 ? reinterpret_cast<const void *>(exchange_chunk_kernel<XT, GT, WT, YT, HAS_G>)
+                                       : reinterpret_cast<const void *>(exchange_kernel<XT, GT, WT, YT, HAS_G>));
     const unsigned smem = pipe ? Pipe<XT, GT, WT, HAS_G>::BYTES : Ring<XT, GT, HAS_G>::kBytes;
     const int threads = pipe ? kExchThreads : kThreads;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[pipe]) {
+    static bool attr_set[3] = {false, false, false};
+    if (!attr_set[kind]) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr_set[pipe] = true;
+        attr_set[kind] = true;
     }
     const int maxg = max_coresident(fn, threads, smem);
     if (grid <= 0 || grid > maxg) grid = maxg;

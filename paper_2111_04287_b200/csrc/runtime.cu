@@ -84,7 +84,9 @@ struct bf_ctx {
     std::vector<double> WM;
     int sched_kind = 0;
     int topo_check = 1;
-    int exch_kernel = 0;                      // BF_EXCH=pipe selects the warp-specialised pipeline
+    int exch_kernel = 2;                      // BF_EXCH: tile | pipe | chunk (default)
+    int chunk_tiles = 128;                    // BF_CHUNK_TILES
+    unsigned long long ccnt_off = 0, cflag_off = 0;
     // exchange region
     size_t exch_cap = 0;                      // bytes per agent per parity
     size_t exch_begin = 0, exch_top = 0;      // heap range of exchange (+ hierarchical) regions
@@ -174,6 +176,11 @@ bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
     const int tmax = static_cast<int>(cap / (static_cast<size_t>(kTile) * 2));
     s = heap_alloc(c, static_cast<size_t>(c->k) * tmax * 8, &ready_off);
     if (s) return s;
+    unsigned long long ccnt_off, cflag_off;
+    if ((s = heap_alloc(c, static_cast<size_t>(tmax) * 4, &ccnt_off))) return s;
+    if ((s = heap_alloc(c, static_cast<size_t>(tmax) * 8, &cflag_off))) return s;
+    c->ccnt_off = ccnt_off;
+    c->cflag_off = cflag_off;
     c->exch_cap = cap;
     c->slot_off = slot_off;
     c->ready_off = ready_off;
@@ -398,7 +405,9 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     c->device = cuda_device;
     c->heap_bytes = heap_bytes;
     if (const char *t = getenv("BF_TIMEOUT_MS")) c->timeout_ns = strtoull(t, nullptr, 10) * 1000000ull;
-    if (const char *x = getenv("BF_EXCH")) c->exch_kernel = strcmp(x, "pipe") == 0 ? 1 : 0;
+    if (const char *x = getenv("BF_EXCH"))
+        c->exch_kernel = strcmp(x, "pipe") == 0 ? 1 : (strcmp(x, "tile") == 0 ? 0 : 2);
+    if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
     cudaError_t e = cudaMalloc(&c->heap, heap_bytes);
     if (e != cudaSuccess) {
         delete c;
@@ -613,6 +622,9 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     p.ready_off = c->ready_off;
     p.ready_stride = c->ready_stride;
     p.kernel = c->exch_kernel;
+    p.chunk_tiles = c->chunk_tiles;
+    p.ccnt_off = c->ccnt_off;
+    p.cflag_off = c->cflag_off;
     CU(launch_exchange(p, x_kind, g_kind, wire_kind, y_kind, g != nullptr, 0, st));
     c->launches++;
     return BF_OK;

@@ -22,7 +22,7 @@ namespace bf {
 #define BF_THREADS 256
 #endif
 #ifndef BF_MINB
-#define BF_MINB 2
+#define BF_MINB 3
 #endif
 constexpr int kTile = BF_TILE;         // elements per tile (the unit of one flag)
 constexpr int kThreads = BF_THREADS;   // threads per CTA of the streaming kernels

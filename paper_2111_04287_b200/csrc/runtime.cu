@@ -85,7 +85,7 @@ struct bf_ctx {
     int sched_kind = 0;
     int topo_check = 1;
     int exch_kernel = 2;                      // BF_EXCH: tile | pipe | chunk (default)
-    int chunk_tiles = 128;                    // BF_CHUNK_TILES
+    int chunk_tiles = 0;                      // BF_CHUNK_TILES; 0 = 256 on one GPU, 1024 across GPUs
     unsigned long long ccnt_off = 0, cflag_off = 0;
     // exchange region
     size_t exch_cap = 0;                      // bytes per agent per parity
@@ -622,7 +622,7 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     p.ready_off = c->ready_off;
     p.ready_stride = c->ready_stride;
     p.kernel = c->exch_kernel;
-    p.chunk_tiles = c->chunk_tiles;
+    p.chunk_tiles = c->chunk_tiles ? c->chunk_tiles : (c->nprocs > 1 ? 1024 : 256);
     p.ccnt_off = c->ccnt_off;
     p.cflag_off = c->cflag_off;
     CU(launch_exchange(p, x_kind, g_kind, wire_kind, y_kind, g != nullptr, 0, st));

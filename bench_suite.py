@@ -145,7 +145,7 @@ def main():
         n = a.agents
         k = n // world
         count = 25_600_000
-        ctx = bfp.Context(agents_per_proc=k, heap_bytes=6 * k * count * 4 + (256 << 20), device=local)
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=5 * k * count * 4 + (512 << 20), device=local)
         x = torch.empty(k, count, device="cuda")
         for la in range(k):
             bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + ctx.rank + la)
@@ -226,7 +226,7 @@ def main():
                 ctx.atc_step(x, g, lr)
             ms = timed(step, 200, warm=0)
             ctx.set_dynamic_schedule("none")
-            xs, _ = ora.lsq_solve(As.double().cpu().numpy(), bs.double().cpu().numpy(), tol=1e-12, max_iter=2000)
+            xs, _ = ora.lsq_solve(As.double().cpu().numpy(), bs.double().cpu().numpy(), tol=1e-10, max_iter=500)
             xbar = x.double().mean(0).cpu().numpy()
             emit({"config": f"C2 ATC-DSGD least squares d=10k m=2000 x 8 agents, {topo}", "ms_per_iter": ms,
                   "iters_per_s": 1e3 / ms, "rel_dist_to_xstar_after_203_iters":

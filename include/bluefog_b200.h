@@ -144,6 +144,12 @@ bf_status bf_neighbor_allreduce(bf_ctx *ctx, const void *x, void *y, size_t coun
 bf_status bf_atc_step(bf_ctx *ctx, float *x, const void *g, bf_dtype g_dtype, size_t count,
                       float lr, bf_dtype wire, void *x_bf16_shadow,
                       const bf_weights *weights, void *stream);
+/* bf_awc_step: fused adapt-while-communicate DSGD step (Eq. 16; R6):
+ * x_i <- sum_j w_ij x_j - lr * g_i, in place on the fp32 master x (device
+ * tensors).  The neighbours exchange x itself, so in a training loop the
+ * exchange does not depend on this step's gradient. */
+bf_status bf_awc_step(bf_ctx *ctx, float *x, const void *g, bf_dtype g_dtype, size_t count, float lr,
+                      const bf_weights *weights, void *stream);
 /* bf_hierarchical_neighbor_allreduce (R12): y = (W_M kron J_L/L) x:
  * intra-machine average, machine-level neighbour averaging, broadcast.
  * machine_weights: NULL (static machine topology) or an array of

@@ -211,6 +211,41 @@ class Context:
                                    v.ptr() if v else None, _stream_ptr(stream)))
         return x
 
+    def awc_step(self, x: torch.Tensor, g: torch.Tensor, lr: float, self_weight=None, src_weights=None,
+                 dst_weights=None, stream=None) -> torch.Tensor:
+        """Fused AWC-DSGD step (Eq. 16): x <- W x - lr*g, in place on the fp32 master x."""
+        if x.dtype != torch.float32:
+            raise ValueError("x must be the fp32 master copy")
+        count = self._rows(x)
+        v = self._views(self_weight, src_weights, dst_weights)
+        check(self.lib.bf_awc_step(self.h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()), _DT[g.dtype],
+                                   count, float(lr), v.ptr() if v else None, _stream_ptr(stream)))
+        return x
+
+    # ---- non-blocking form (P:635-645) -------------------------------------------
+    def neighbor_allreduce_nonblocking(self, tensor: torch.Tensor, self_weight=None, src_weights=None,
+                                       dst_weights=None):
+        """Launch neighbor_allreduce on the context's side stream and return a
+        handle immediately; the caller's stream keeps running
+        computation.  `wait(handle)` returns the result."""
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        cur = torch.cuda.current_stream()
+        self._side.wait_stream(cur)             # the input is complete before the exchange reads it
+        out = torch.empty_like(tensor)
+        tensor.record_stream(self._side)
+        out.record_stream(self._side)
+        self.neighbor_allreduce(tensor, self_weight, src_weights, dst_weights, out=out, stream=self._side)
+        ev = torch.cuda.Event()
+        ev.record(self._side)
+        return (out, ev)
+
+    @staticmethod
+    def wait(handle) -> torch.Tensor:
+        out, ev = handle
+        torch.cuda.current_stream().wait_event(ev)
+        return out
+
     def hierarchical_neighbor_allreduce(self, tensor: torch.Tensor, self_weight=None, src_machine_weights=None,
                                         out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         """P:660-675 (machine-level neighbour averaging of machine averages)."""

@@ -97,6 +97,8 @@ struct ExchParams {
     void *y;
     void *shadow;                           // bf16 copy of y (nullable)
     float lr;
+    int awc;                                // AWC (Eq. 16): combine x, then subtract lr * g_self (kernel 2)
+    int g_bf16;                             // AWC: dtype of g
     // exchange region (offsets into every heap)
     unsigned long long slot_off, slot_agent_stride, slot_parity_stride;
     unsigned long long ready_off;           // u64 [k][ready_stride]

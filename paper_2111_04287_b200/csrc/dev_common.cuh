@@ -92,6 +92,41 @@ __device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gsrc, un
         "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// L2 cache policies (createpolicy): streaming data evict-first, published
+// tiles evict-last so that the neighbours' re-reads hit L2.
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ unsigned long long policy_evict_normal() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_1d_hint(void *smem_dst, const void *gsrc, unsigned bytes,
+                                                 unsigned long long *bar, unsigned long long pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void st_hint_v4f(float *p, const float v[4], unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st_hint_v2u(void *p, unsigned a, unsigned b, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol)
+                 : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -253,6 +288,8 @@ struct Vec4<float> {
                 if (i < valid) p[i] = v[i];
         }
     }
+    static __device__ __forceinline__ void store_hint(float *p, const float v[4], int valid, bool vec,
+                                                      unsigned long long pol);
 };
 
 __device__ __forceinline__ unsigned short f2bf(float f) {
@@ -300,7 +337,27 @@ struct Vec4<__nv_bfloat16> {
                 if (i < valid) q[i] = f2bf(v[i]);
         }
     }
+    static __device__ __forceinline__ void store_hint(__nv_bfloat16 *p, const float v[4], int valid, bool vec,
+                                                      unsigned long long pol);
 };
+
+__device__ __forceinline__ void Vec4<float>::store_hint(float *p, const float v[4], int valid, bool vec,
+                                                        unsigned long long pol) {
+    if (vec && valid == 4)
+        st_hint_v4f(p, v, pol);
+    else
+        store(p, v, valid, vec);
+}
+__device__ __forceinline__ void Vec4<__nv_bfloat16>::store_hint(__nv_bfloat16 *p, const float v[4], int valid,
+                                                                bool vec, unsigned long long pol) {
+    if (vec && valid == 4) {
+        const unsigned a = static_cast<unsigned>(f2bf(v[0])) | (static_cast<unsigned>(f2bf(v[1])) << 16);
+        const unsigned b = static_cast<unsigned>(f2bf(v[2])) | (static_cast<unsigned>(f2bf(v[3])) << 16);
+        st_hint_v2u(p, a, b, pol);
+    } else {
+        store(p, v, valid, vec);
+    }
+}
 
 // Element index of vector j (0..kVecPerThread-1) of this thread inside a tile:
 // consecutive threads touch consecutive 4-element vectors (coalesced).

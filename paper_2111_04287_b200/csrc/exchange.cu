@@ -773,14 +773,21 @@ __global__ void __launch_bounds__(kThreads, BF_MINB) exchange_chunk_kernel(const
         return at<WT>(g.peer_base[agent / k],
                       p.slot_off + (agent % k) * p.slot_agent_stride + parity * p.slot_parity_stride);
     };
+#ifndef BF_HINTS
+#define BF_HINTS 1
+#endif
+    // BF_HINTS: 0 none, 1 streaming data evict-first, 2 + published tiles evict-last
+    const unsigned long long pol_stream = BF_HINTS >= 1 ? policy_evict_first() : policy_evict_normal();
+    const unsigned long long pol_keep = BF_HINTS >= 2 ? policy_evict_last() : policy_evict_normal();
     auto issue = [&](const ItemIt &it, int stage) {   // thread 0: TMA of the x / g tiles of a publish item
         const long long off = static_cast<long long>(it.a) * count + static_cast<long long>(it.t) * kTile;
         fence_proxy_async();
         mbar_expect_tx(&full[stage], R::kXBytes + R::kGBytes);
-        tma_load_1d(ring + stage * R::kXBytes, static_cast<const XT *>(p.x) + off, R::kXBytes, &full[stage]);
+        tma_load_1d_hint(ring + stage * R::kXBytes, static_cast<const XT *>(p.x) + off, R::kXBytes, &full[stage],
+                         pol_stream);
         if constexpr (HAS_G)
-            tma_load_1d(ring + 2 * R::kXBytes + stage * R::kGBytes, static_cast<const GT *>(p.g) + off, R::kGBytes,
-                        &full[stage]);
+            tma_load_1d_hint(ring + 2 * R::kXBytes + stage * R::kGBytes, static_cast<const GT *>(p.g) + off,
+                             R::kGBytes, &full[stage], pol_stream);
     };
     // x_half of (t, a) from global memory (unstaged publish items, bf16-wire self terms)
     auto adapt_global = [&](int t, int a, float (&xh)[kVecPerThread][4]) {
@@ -860,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, BF_MINB) exchange_chunk_kernel(const
             WT *mine = slot_of(g.me * k + a) + base;
 #pragma unroll
             for (int j = 0; j < kVecPerThread; ++j)
-                Vec4<WT>::store(mine + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), true);
+                Vec4<WT>::store_hint(mine + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), true, pol_keep);
             ++it_pub;
             ++mp;
             pub = nxt;
@@ -905,15 +912,29 @@ __global__ void __launch_bounds__(kThreads, BF_MINB) exchange_chunk_kernel(const
 #pragma unroll
                     for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(c, v[j][i], acc[j][i]);
             }
+            if (p.awc) {   // AWC (Eq. 16): x_i <- sum_j w_ij x_j - lr * g_i
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j) {
+                    float gv[4];
+                    const long long off = static_cast<long long>(a) * count + base + tile_elem(j);
+                    if (p.g_bf16)
+                        Vec4<bf16>::load(static_cast<const bf16 *>(p.g) + off, gv, clamp_valid(rem, tile_elem(j)), vec);
+                    else
+                        Vec4<float>::load(static_cast<const float *>(p.g) + off, gv, clamp_valid(rem, tile_elem(j)),
+                                          vec);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(-p.lr, gv[i], acc[j][i]);
+                }
+            }
             YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base;
 #pragma unroll
             for (int j = 0; j < kVecPerThread; ++j)
-                Vec4<YT>::store(yr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+                Vec4<YT>::store_hint(yr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec, pol_stream);
             if (p.shadow) {
                 bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base;
 #pragma unroll
                 for (int j = 0; j < kVecPerThread; ++j)
-                    Vec4<bf16>::store(sr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+                    Vec4<bf16>::store_hint(sr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec, pol_stream);
             }
             comb.next();
             ++mc;

@@ -94,6 +94,8 @@ struct bf_ctx {
     int ready_stride = 0;
     // hierarchical region
     bool hier_ready = false;
+    int hier_L = 0;
+    size_t hier_begin = 0, hier_top = 0;
     unsigned long long b_off = 0, c_off = 0, fb_off = 0, fc_off = 0, bc_agent_stride = 0, bc_parity_stride = 0;
     // staging for host pointers
     void *stage_x = nullptr, *stage_g = nullptr;
@@ -593,7 +595,7 @@ bf_status bf_reserve(bf_ctx *c, size_t bytes_per_agent) {
 // ---- hot path ---------------------------------------------------------------
 static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *y, void *shadow, size_t count,
                                  int x_kind, int g_kind, int wire_kind, int y_kind, float lr,
-                                 const bf_weights *weights, cudaStream_t st) {
+                                 const bf_weights *weights, cudaStream_t st, const void *awc_g = nullptr) {
     if (count == 0) return BF_OK;
     if (count > (1ull << 40)) return fail(BF_ERR_ARG, "count too large");
     ExchParams p;
@@ -622,10 +624,18 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     p.ready_off = c->ready_off;
     p.ready_stride = c->ready_stride;
     p.kernel = c->exch_kernel;
+    if (awc_g) {
+        if (p.kernel != 2) return fail(BF_ERR_UNSUPPORTED, "AWC is fused in the chunked exchange kernel only");
+        p.awc = 1;
+        p.g = awc_g;
+        p.g_bf16 = g_kind == 1;
+        p.lr = lr;
+        p.geo.vec_ok = p.geo.vec_ok && aligned16(awc_g);
+    }
     p.chunk_tiles = c->chunk_tiles ? c->chunk_tiles : (c->nprocs > 1 ? 1024 : 256);
     p.ccnt_off = c->ccnt_off;
     p.cflag_off = c->cflag_off;
-    CU(launch_exchange(p, x_kind, g_kind, wire_kind, y_kind, g != nullptr, 0, st));
+    CU(launch_exchange(p, x_kind, awc_g ? x_kind : g_kind, wire_kind, y_kind, g != nullptr, 0, st));
     c->launches++;
     return BF_OK;
 }
@@ -672,6 +682,18 @@ bf_status bf_atc_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, size
     return BF_OK;
 }
 
+bf_status bf_awc_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, size_t count, float lr,
+                      const bf_weights *weights, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!x || !g) return fail(BF_ERR_ARG, "null tensor");
+    if (g_dtype != BF_FLOAT32 && g_dtype != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
+    if (!std::isfinite(lr)) return fail(BF_ERR_ARG, "non-finite lr");
+    if (is_host_ptr(x) || is_host_ptr(g)) return fail(BF_ERR_ARG, "bf_awc_step takes device tensors");
+    return exchange_common(c, x, nullptr, x, nullptr, count, 0, g_dtype, 0, 0, lr, weights,
+                           static_cast<cudaStream_t>(stream), g);
+}
+
 bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, size_t count, bf_dtype dtype,
                                              const bf_weights *machine_weights, void *stream) {
     bf_status s = check_ctx(c);
@@ -712,11 +734,19 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
     const size_t es = dtype == BF_FLOAT32 ? 4 : 2;
     s = ensure_exchange(c, count * es);
     if (s) return s;
+    if (c->hier_ready && c->hier_L != L) {   // slices are sized per machine size: reallocate
+        CU(cudaDeviceSynchronize());
+        if ((s = bf_barrier_internal(c))) return s;
+        CU(cudaDeviceSynchronize());
+        if (c->heap_used == c->hier_top) c->heap_used = c->hier_begin;
+        c->hier_ready = false;
+    }
     if (!c->hier_ready) {
-        // fp32 slice buffers sized for the largest count the exchange region admits
+        // fp32 slice buffers: each agent averages / combines ceil(tiles / L) tiles
         const bool on_top = c->heap_used == c->exch_top;
-        const size_t max_elems = c->exch_cap / 2;
-        const size_t bytes = max_elems * 4;
+        c->hier_begin = c->heap_used;
+        const size_t slice_tiles = (static_cast<size_t>(c->ready_stride) + L - 1) / L;
+        const size_t bytes = slice_tiles * kTile * 4;
         unsigned long long off;
         if ((s = heap_alloc(c, static_cast<size_t>(c->k) * 2 * bytes, &off))) return s;
         c->b_off = off;
@@ -727,6 +757,8 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
         if ((s = heap_alloc(c, static_cast<size_t>(c->k) * c->ready_stride * 8, &off))) return s;
         c->fc_off = off;
         if (on_top) c->exch_top = c->heap_used;   // released together with the exchange region
+        c->hier_top = c->heap_used;
+        c->hier_L = L;
         c->bc_agent_stride = 2 * bytes;
         c->bc_parity_stride = bytes;
         c->hier_ready = true;

@@ -489,3 +489,50 @@ def test_bench_config_c4_sampled():
     got = x[:, torch.from_numpy(cols).cuda()].cpu().numpy().astype(np.float64)
     assert_parity(got, ref, W0, Xs, 1e-6, np.abs(W0) @ (lr * np.abs(Gs)))
     ctx.close()
+
+
+# ------------------------------------------------------- AWC / non-blocking ---
+@pytest.mark.parametrize("gdt", [torch.float32, torch.bfloat16])
+def test_awc_step(gdt):
+    # Eq. 16: x_i <- sum_j w_ij x_j - lr * g_i
+    n, lr = 8, 0.1
+    W = ora.exp2(n)
+    ctx = _ctx(n)
+    ctx.set_topology(W)
+    for count in (4096, 50001):
+        x, X = _inputs(n, count)
+        g = _gpu(synthetic.agents_grad(n, count, 7), gdt)
+        G = _np(g)
+        ctx.awc_step(x, g, lr)
+        torch.cuda.synchronize()
+        assert_parity(_np(x), ora.awc(W, X, G, lr), W, X, 1e-6, np.float32(lr) * np.abs(G))
+    ctx.close()
+
+
+def test_nonblocking_equals_blocking():
+    # neighbor_allreduce_nonblocking + wait == the blocking call
+    n = 4
+    ctx = _ctx(n)
+    ctx.set_topology(ora.ring(n))
+    x, X = _inputs(n, 30001)
+    h = ctx.neighbor_allreduce_nonblocking(x)
+    z = torch.ones(1000, device="cuda").sum()      # computation overlapping the exchange
+    y1 = bfp.Context.wait(h)
+    y2 = ctx.neighbor_allreduce(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and float(z) == 1000.0
+    assert_parity(_np(y1), ora.mix(ora.ring(n), X), ora.ring(n), X, 1e-6)
+    ctx.close()
+
+
+def test_hierarchical_machine_size_change():
+    n = 8
+    ctx = _ctx(n)
+    x, X = _inputs(n, 20000)
+    for L in (2, 4, 2):
+        WM = ora.exp2(n // L)
+        ctx.set_machine_topology(WM, L)
+        y = ctx.hierarchical_neighbor_allreduce(x)
+        torch.cuda.synchronize()
+        assert_parity(_np(y), ora.hier(WM, L, X), np.kron(WM, np.full((L, L), 1.0 / L)), X, 1e-6)
+    ctx.close()

@@ -256,7 +256,12 @@ def main():
     barrier()
     launches = ctx.kernel_launches() - l0
     total_ms = t_begin.elapsed_time(t_end)
-    kern_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / a.steps
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kern_ms = sum(step_ms) / a.steps
+    # one-peer rotates through tau = ceil(log2 n) graphs: mean step time per graph
+    tau_r = max(1, (ctx.n - 1).bit_length()) if a.topology == "one_peer" else 1
+    by_round = [statistics.mean(step_ms[i] for i in range(a.steps) if (a.warmup + i) % tau_r == r)
+                for r in range(min(tau_r, a.steps))]
     ctx.poll_error()
 
     # ---- end to end through the public API: host gradients in, sample out ----
@@ -281,34 +286,53 @@ def main():
     ctx.poll_error()
 
     # ---- max over ranks ----
-    vals = torch.tensor([total_ms / a.steps, kern_ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64,
+    vals = torch.tensor([total_ms / a.steps, kern_ms, e2e["ms"] if e2e else 0.0] + by_round, dtype=torch.float64,
                         device="cuda")
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms_step, ms_kern, ms_e2e = [float(v) for v in vals.cpu()]
+    vals = [float(v) for v in vals.cpu()]
+    ms_step, ms_kern, ms_e2e = vals[:3]
+    ms_by_round = vals[3:]
 
     if rank == 0:
         d = degree(a.topology, n)
-        # algorithmic bytes per launch on this GPU:
-        # x read + g read + x write + publish (wire).  The d_out reads of each
-        # published tile by same-GPU neighbours are served from L2 by the
-        # tile-major schedule (ncu: DRAM traffic = 16.0 B/element at N=1).
-        hbm_bytes = k * count * (4 + 4 + 4 + wire_b)
-        # NVLink-in: wire bytes of every source that lives on another GPU,
-        # averaged over the rounds of the timed region (one-peer rotates).
+        # algorithmic bytes per launch on this GPU, for the
+        # default local-agent fused kernel: every local agent reads x and g and
+        # writes x (12 B per element); an agent whose x_half is read by another
+        # process also publishes its wire copy (w B per element).  Local sources
+        # are combined in registers, remote sources cross NVLink (d_in remote x w).
         tau = max(1, (n - 1).bit_length())
-        remote = 0.0
         rounds = range(a.warmup, a.warmup + a.steps)
-        for la in range(k):
-            gid = ctx.rank + la
-            for r in rounds:
-                if a.topology == "one_peer":
-                    srcs = [(gid - (1 << (r % tau))) % n] if n > 1 else []
-                else:
-                    srcs = [(gid - (1 << j)) % n for j in range(d)]
-                remote += sum(1 for sidx in srcs if sidx // k != ctx.proc) / len(rounds)
-        nvl_bytes = remote * count * wire_b
+
+        def sources(gid, r):
+            if n == 1 or a.topology == "self":
+                return []
+            if a.topology == "one_peer":
+                return [(gid - (1 << (r % tau))) % n]
+            return [(gid - (1 << j)) % n for j in range(d)]
+
+        def dests(gid, r):
+            if n == 1 or a.topology == "self":
+                return []
+            if a.topology == "one_peer":
+                return [(gid + (1 << (r % tau))) % n]
+            return [(gid + (1 << j)) % n for j in range(d)]
+
         peak_hbm, peak_kind = hbm_peak()
+        remote, publishers, t_roof = 0.0, 0.0, 0.0
+        roof_by_round = {}
+        for r in rounds:
+            rem_r = sum(1 for la in range(k) for sidx in sources(ctx.rank + la, r) if sidx // k != ctx.proc)
+            pub_r = sum(1 for la in range(k) if any(didx // k != ctx.proc for didx in dests(ctx.rank + la, r)))
+            remote += rem_r / len(rounds)
+            publishers += pub_r / len(rounds)
+            # per-round roofline time: the slower of HBM and NVLink-in for this round's graph
+            t_r = max((k * 12 + pub_r * wire_b) * count / (peak_hbm * 1e9),
+                      rem_r * count * wire_b / (NVLINK_PEAK_GBS * 1e9))
+            t_roof += t_r / len(rounds)
+            roof_by_round[r % tau_r] = t_r
+        hbm_bytes = k * count * (4 + 4 + 4) + publishers * count * wire_b
+        nvl_bytes = remote * count * wire_b
         t_hbm = hbm_bytes / (peak_hbm * 1e9)
         t_nvl = nvl_bytes / (NVLINK_PEAK_GBS * 1e9)
         if t_nvl > t_hbm:
@@ -318,6 +342,12 @@ def main():
             roof = {"bound": "hbm", "achieved": hbm_bytes / (ms_kern * 1e-3) / 1e9, "peak": peak_hbm,
                     "unit": "GB/s", "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
         roof["frac"] = roof["achieved"] / roof["peak"]
+        # one-peer rounds alternate between HBM- and NVLink-bound on N > 1: the
+        # mean over rounds of max(HBM time, NVLink time) at the peaks, / measured
+        roof["t_roof_ms"] = t_roof * 1e3
+        roof["frac_per_round_bound"] = t_roof * 1e3 / ms_kern
+        roof["by_round"] = [{"ms": m, "t_roof_ms": roof_by_round[r] * 1e3, "frac": roof_by_round[r] * 1e3 / m}
+                            for r, m in enumerate(ms_by_round)]
         roof["traffic"] = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
@@ -329,7 +359,8 @@ def main():
             except Exception:
                 pass
         roof["algorithmic_bytes_per_launch"] = hbm_bytes if roof["bound"] == "hbm" else nvl_bytes
-        roof["kernel"] = "bf::exchange_kernel (fused ATC adapt+publish+exchange+combine)"
+        roof["kernel"] = ("bf::exchange_fused_kernel (ATC adapt + local-agent combine in registers + "
+                          "publish / NVLink pull of remote sources)")
         value = 1e3 / ms_step
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": a.steps,

@@ -40,20 +40,49 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str = SO) -> str:
-    """defines: extra -D flags for tuning variants (BF_TILE, BF_THREADS, BF_MINB)."""
+    """Compile every csrc/*.cu to an object in parallel (one nvcc per file),
+    then link the shared library.  defines: extra -D flags for tuning variants."""
     if not force and out == SO and not defines and up_to_date():
         return SO
-    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], *sources(), "-o", out + ".tmp"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
+
+    obj_dir = tempfile.mkdtemp(prefix="bf_build_")
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+    dflags = [f"-D{d}" for d in defines]
+
+    def compile_one(src):
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *compile_flags, *dflags, "-c", src, "-o", obj]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, res
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, sources()))
+    log_text = ""
+    failed = False
+    for src, obj, cmd, res in results:
+        log_text += " ".join(cmd) + "\n" + res.stdout + res.stderr
+        failed |= res.returncode != 0
+    if not failed:
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+               *[obj for _, obj, _, _ in results], "-o", out + ".tmp"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        log_text += " ".join(cmd) + "\n" + res.stdout + res.stderr
+        failed = res.returncode != 0
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+        f.write(log_text)
+    for _, obj, _, _ in results:
+        if os.path.exists(obj):
+            os.unlink(obj)
+    os.rmdir(obj_dir)
+    if failed:
+        sys.stderr.write(log_text[-8000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     os.replace(out + ".tmp", out)
     if verbose:
-        sys.stdout.write(res.stderr)
+        sys.stdout.write(log_text)
     return out
 
 

@@ -34,6 +34,7 @@ constexpr int kMaxN = BF_MAX_AGENTS;
 constexpr int kMaxP = BF_MAX_PROCS;
 constexpr size_t kPadBytes = 64 * 1024;
 constexpr size_t kAlign = 4096;
+constexpr int kMaxGrid = 4096;         // CTAs of one exchange launch (progress counters per process)
 
 // Per-agent, per-parity descriptor of a dynamic call (push side of Eq. 9):
 // which agents this agent pushes to and with which s (sender-side weight).
@@ -97,7 +98,7 @@ struct ExchParams {
     void *y;
     void *shadow;                           // bf16 copy of y (nullable)
     float lr;
-    int awc;                                // AWC (Eq. 16): combine x, then subtract lr * g_self (kernel 2)
+    int awc;                                // AWC (Eq. 16): combine x, then subtract lr * g_self
     int g_bf16;                             // AWC: dtype of g
     // exchange region (offsets into every heap)
     unsigned long long slot_off, slot_agent_stride, slot_parity_stride;
@@ -105,10 +106,12 @@ struct ExchParams {
     int ready_stride;
     int wmode;
     int check;
-    int kernel;                             // 0: per-tile flags, 1: warp-specialised pipeline, 2: chunked
-    int chunk_tiles;                        // kernel 2: tiles per chunk
-    unsigned long long ccnt_off;            // kernel 2: u32 [tmax] per-chunk CTA counters (local)
-    unsigned long long cflag_off;           // kernel 2: u64 [tmax] per-chunk release flags
+    int kernel;                             // 2: chunked (any k); 3: local-agent fused (default, fused_supported)
+    int chunk_tiles;                        // kernels 2, 3: tiles per chunk
+    unsigned long long ccnt_off;            // kernels 2, 3: u32 [tmax] per-chunk CTA counters (local)
+    unsigned long long cflag_off;           // kernels 2, 3: u64 [tmax] per-chunk release flags
+    unsigned pub_mask;                      // kernel 3, kWStatic: local agents read by another process
+    unsigned long long prog_off;            // kernel 3: u64 [kMaxGrid] per-CTA publish progress
     SrcTab tab;                             // kWStatic: final coefficients; kWDynamic: declared r
     DynDecl dyn;
 };
@@ -181,5 +184,6 @@ cudaError_t launch_fill_uniform(void *dst, int kind, size_t count, unsigned long
                                 unsigned long long offset, float scale, cudaStream_t s);
 cudaError_t launch_set_u64(unsigned long long *dst, unsigned long long v, cudaStream_t s);
 int max_coresident(const void *func, int threads, size_t smem);
+bool fused_supported(int k, int nprocs);   // kernel 3 is instantiated for this configuration
 
 }  // namespace bf

@@ -80,6 +80,11 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// order generic-proxy accesses (e.g. an acquire of a peer's flag) before later
+// async-proxy (TMA) accesses of global memory
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -125,6 +130,21 @@ __device__ __forceinline__ void st_hint_v4f(float *p, const float v[4], unsigned
 __device__ __forceinline__ void st_hint_v2u(void *p, unsigned a, unsigned b, unsigned long long pol) {
     asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol)
                  : "memory");
+}
+// 128-bit / 64-bit loads with an L2 eviction policy, bypassing L1 (streamed once)
+__device__ __forceinline__ float4 ld_hint_v4f(const float *p, unsigned long long pol) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_hint_v2u(const void *p, unsigned long long pol) {
+    uint2 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
 }
 
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
@@ -290,6 +310,17 @@ struct Vec4<float> {
     }
     static __device__ __forceinline__ void store_hint(float *p, const float v[4], int valid, bool vec,
                                                       unsigned long long pol);
+    static __device__ __forceinline__ void load_hint(const float *p, float v[4], int valid, bool vec,
+                                                     unsigned long long pol) {
+        if (vec && valid == 4) {
+            float4 q = ld_hint_v4f(p, pol);
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
+            load(p, v, valid, vec);
+        }
+    }
+    // value as it travels on a wire of this dtype
+    static __device__ __forceinline__ float wire(float f) { return f; }
 };
 
 __device__ __forceinline__ unsigned short f2bf(float f) {
@@ -339,6 +370,18 @@ struct Vec4<__nv_bfloat16> {
     }
     static __device__ __forceinline__ void store_hint(__nv_bfloat16 *p, const float v[4], int valid, bool vec,
                                                       unsigned long long pol);
+    static __device__ __forceinline__ void load_hint(const __nv_bfloat16 *p, float v[4], int valid, bool vec,
+                                                     unsigned long long pol) {
+        if (vec && valid == 4) {
+            uint2 w = ld_hint_v2u(p, pol);
+            v[0] = __uint_as_float(w.x << 16); v[1] = __uint_as_float(w.x & 0xFFFF0000u);
+            v[2] = __uint_as_float(w.y << 16); v[3] = __uint_as_float(w.y & 0xFFFF0000u);
+        } else {
+            load(p, v, valid, vec);
+        }
+    }
+    // value as it travels on a bf16 wire: round to nearest even (R17)
+    static __device__ __forceinline__ float wire(float f) { return bf2f(f2bf(f)); }
 };
 
 __device__ __forceinline__ void Vec4<float>::store_hint(float *p, const float v[4], int valid, bool vec,

@@ -1,178 +1,32 @@
-// exchange.cu -- the partial-averaging hot path on sm_100a.
+// exchange.cu -- the partial-averaging hot path on sm_100a: the chunked
+// exchange kernel (kernel 2, any number of local agents), the dispatch to the
+// local-agent fused kernel (kernel 3, exchange_fused.cuh), the hierarchical
+// kernel and the device barrier.
 //
-// exchange_kernel: ONE persistent, cooperative launch per call that fuses
+// Every exchange is ONE persistent, cooperative launch per call that fuses
 //   Eq. 4 local update (ATC)      x_half = x - lr*g          (registers)
 //   publish + signal                      wire(x_half) -> own IPC slot, release flag
-//   neighbour exchange (Eq. 5 / Eq. 9)    acquire peers' flags, 128-bit loads over
+//   neighbour exchange (Eq. 5 / Eq. 9)    acquire peers' flags, loads over
 //                                         NVLink (other GPU) or L2 (same GPU)
 //   weighted combine + store              y = w_ii x_half + sum_j w_ij wire_j (fp32 FMA)
-// tile by tile (kTile elements per flag), so HBM traffic, NVLink traffic and
-// the wait for the slowest neighbour overlap across the CTAs of the grid.
+// chunk by chunk, so HBM traffic, NVLink traffic and the wait for the slowest
+// neighbour overlap across the CTAs of the grid.
 //
 // Deadlock freedom: all CTAs are co-resident (cooperative launch), every CTA
-// walks its items in increasing tile order and publishes tile t before it
-// waits for anybody's tile t, and grid >= local agents; every wait is bounded
-// by the context timeout.  WAR safety: slots are double-buffered by epoch
-// parity and a writer overwrites parity (e&1) only after every process has
-// reported (done_from) that it finished reading epoch e-2.
-#include <cooperative_groups.h>
+// walks its items in increasing tile order and publishes chunk c+1 before it
+// waits for anybody's chunk c; every wait is bounded by the context timeout.
+// WAR safety: slots are double-buffered by epoch parity and a writer
+// overwrites parity (e&1) only after every process has reported (done_from)
+// that it finished reading epoch e-2.
 #include <cuda_bf16.h>
 
-#include "dev_common.cuh"
+#include "exchange_common.cuh"
 
 namespace bf {
 
-using bf16 = __nv_bfloat16;
-
-__device__ __forceinline__ unsigned long long *ready_ptr(const Geometry &g, unsigned long long off,
-                                                         int stride, int agent, int t) {
-    return at<unsigned long long>(g.peer_base[agent / g.k], off) +
-           static_cast<long long>(agent % g.k) * stride + t;
-}
-
-// Wait until every process finished reading epoch e-2 (so parity e&1 is free).
-__device__ __forceinline__ bool war_wait(const Geometry &g, unsigned long long e) {
-    bool ok = true;
-    if (g.nprocs > 1 && e > 2 && threadIdx.x < g.nprocs)
-        ok = spin_ge(g, &pad_of(g, g.me)->done_from[threadIdx.x], e - 2);
-    return __syncthreads_and(ok);
-}
-
-// Broadcast "this process finished reading epoch e" to every process.
-__device__ __forceinline__ void publish_done(const Geometry &g, unsigned long long e) {
-    for (int q = 0; q < g.nprocs; ++q) st_release_sys(&pad_of(g, q)->done_from[g.me], e);
-}
-
-// --------------------------------------------------------------------------
-// Source resolution for one call: fills the shared table of every local agent.
-//   static   : coefficients from the host's W row (Eq. 5)
-//   schedule : one-peer exp-2 from the device round counter (R5)
-//   dynamic  : declared r (Eq. 11) times the senders' s (Eq. 10) read from their
-//              descriptors; push-only receivers discover their sources there;
-//              topology check on mismatches.
-struct SharedTab {
-    float self_w[kMaxK];
-    float coef[kMaxK][kMaxN];
-    unsigned char src[kMaxK][kMaxN];
-    int nsrc[kMaxK];
-};
-
-__device__ bool resolve_sources(const ExchParams &p, unsigned long long e, SharedTab &st) {
-    const Geometry &g = p.geo;
-    const int k = g.k;
-    const int parity = static_cast<int>(e & 1);
-    bool ok = true;
-    if (p.wmode == kWStatic) {
-        for (int a = threadIdx.x; a < k; a += blockDim.x) {
-            st.self_w[a] = p.tab.self_w[a];
-            st.nsrc[a] = p.tab.nsrc[a];
-            for (int q = 0; q < p.tab.nsrc[a]; ++q) {
-                st.src[a][q] = p.tab.src[a][q];
-                st.coef[a][q] = p.tab.coef[a][q];
-            }
-        }
-    } else if (p.wmode == kWSchedule) {
-        const unsigned long long round = *reinterpret_cast<volatile unsigned long long *>(
-            &pad_of(g, g.me)->round);
-        int tau = 0;
-        while ((1 << tau) < g.n) ++tau;
-        for (int a = threadIdx.x; a < k; a += blockDim.x) {
-            const int gid = g.me * k + a;
-            if (tau == 0) {
-                st.self_w[a] = 1.f;
-                st.nsrc[a] = 0;
-            } else {
-                const int off = 1 << static_cast<int>(round % tau);
-                st.self_w[a] = 0.5f;
-                st.nsrc[a] = 1;
-                st.src[a][0] = static_cast<unsigned char>(((gid - off) % g.n + g.n) % g.n);
-                st.coef[a][0] = 0.5f;
-            }
-        }
-    } else {
-        // one warp per local agent; lanes scan candidate senders j
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        const int nwarps = blockDim.x >> 5;
-        for (int a = warp; a < k; a += nwarps) {
-            const int gid = g.me * k + a;
-            const bool has_src = p.dyn.has_src[a];
-            int total = 0;
-            for (int j0 = 0; j0 < g.n; j0 += 32) {
-                const int j = j0 + lane;
-                bool include = false;
-                float c = 0.f;
-                if (j < g.n && j != gid) {
-                    int qdecl = -1;
-                    if (has_src)
-                        for (int q = 0; q < p.tab.nsrc[a]; ++q)
-                            if (p.tab.src[a][q] == j) qdecl = q;
-                    const bool need = !has_src || qdecl >= 0 || p.check;
-                    if (need) {
-                        const Desc *d = &pad_of(g, j / k)->desc[j % k][parity];
-                        if (!spin_ge(g, &d->epoch, e)) {
-                            ok = false;
-                        } else {
-                            const unsigned long long mask =
-                                *reinterpret_cast<const volatile unsigned long long *>(&d->dstmask);
-                            const unsigned long long hd =
-                                *reinterpret_cast<const volatile unsigned long long *>(&d->has_dst);
-                            const bool to_me = (mask >> gid) & 1ull;
-                            const float s = to_me ? *reinterpret_cast<const volatile float *>(&d->s[gid]) : 1.f;
-                            if (has_src) {
-                                if (qdecl >= 0) {
-                                    include = true;
-                                    c = p.tab.coef[a][qdecl] * s;            // r_ij * s_ij (R1)
-                                    if (p.check && hd && !to_me) ok = false;  // sender never sends to me
-                                } else if (to_me && p.check) {
-                                    ok = false;                               // unlisted pusher
-                                }
-                            } else if (to_me) {
-                                include = true;                               // push-only: r = 1
-                                c = s;
-                            }
-                        }
-                    }
-                }
-                const unsigned int bal = __ballot_sync(0xffffffffu, include);
-                if (include) {
-                    const int pos = total + __popc(bal & ((1u << lane) - 1u));
-                    st.src[a][pos] = static_cast<unsigned char>(j);
-                    st.coef[a][pos] = c;
-                }
-                total += __popc(bal);
-            }
-            if (lane == 0) {
-                st.nsrc[a] = total;
-                st.self_w[a] = p.tab.self_w[a];
-            }
-        }
-        if (!__all_sync(0xffffffffu, ok) && lane == 0) {
-            const unsigned int code =
-                *reinterpret_cast<volatile unsigned int *>(&pad_of(g, g.me)->abort);
-            if (!code) abort_all(g, BF_ERR_TOPOLOGY);
-        }
-    }
-    return __syncthreads_and(ok);
-}
-
-// Block 0 writes the descriptors of the local agents for this epoch.
-__device__ void write_descriptors(const ExchParams &p, unsigned long long e) {
-    const Geometry &g = p.geo;
-    const int parity = static_cast<int>(e & 1);
-    if (blockIdx.x != 0) return;
-    for (int a = threadIdx.x; a < g.k; a += blockDim.x) {
-        Desc *d = &pad_of(g, g.me)->desc[a][parity];
-        unsigned long long mask = 0;
-        for (int q = 0; q < p.dyn.ndst[a]; ++q) {
-            const int j = p.dyn.dst[a][q];
-            mask |= 1ull << j;
-            d->s[j] = p.dyn.s[a][q];
-        }
-        d->dstmask = mask;
-        d->has_dst = p.dyn.has_dst[a];
-        st_release_sys(&d->epoch, e);
-    }
-}
+cudaError_t launch_fused_nar(const ExchParams &p, int x_kind, int grid, cudaStream_t s);
+cudaError_t launch_fused_atc(const ExchParams &p, int g_kind, int wire_kind, int grid, cudaStream_t s);
+cudaError_t launch_fused_awc(const ExchParams &p, int g_kind, int wire_kind, int grid, cudaStream_t s);
 
 // Shared-memory ring of the TMA-prefetched x / g tiles (2 stages).
 template <typename XT, typename GT, bool HAS_G>
@@ -182,546 +36,8 @@ struct Ring {
     static constexpr unsigned kBytes = 2 * (kXBytes + kGBytes);
 };
 
-template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
-__global__ void __launch_bounds__(kThreads, BF_MINB) exchange_kernel(const __grid_constant__ ExchParams p) {
-    using R = Ring<XT, GT, HAS_G>;
-    extern __shared__ __align__(128) unsigned char ring[];
-    __shared__ SharedTab st;
-    __shared__ __align__(8) unsigned long long full[2];
-    __shared__ int s_fail;
-    const Geometry &g = p.geo;
-    Pad *pad = pad_of(g, g.me);
-    if (aborted(g)) return;
-    const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
-    const int parity = static_cast<int>(e & 1);
-    const bool sys = g.nprocs > 1;   // flags of agents on other GPUs need system scope
-
-    if (threadIdx.x == 0) {
-        s_fail = 0;
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        fence_mbar_init();
-    }
-    if (!war_wait(g, e)) return;
-    if (p.wmode == kWDynamic) write_descriptors(p, e);
-    if (!resolve_sources(p, e, st)) return;
-
-    const bool vec = g.vec_ok != 0;
-    const long long count = g.count;
-    const int k = g.k;
-    const long long items = static_cast<long long>(k) * g.T;
-    // an item is staged by TMA when its rows are 16B-aligned and the tile is full
-    auto staged = [&](long long w) {
-        return vec && (count - static_cast<long long>(w / k) * kTile) >= kTile;
-    };
-    auto issue = [&](long long w, int stage) {   // thread 0 only
-        const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
-        const long long off = static_cast<long long>(a) * count + static_cast<long long>(t) * kTile;
-        fence_proxy_async();
-        mbar_expect_tx(&full[stage], R::kXBytes + R::kGBytes);
-        tma_load_1d(ring + stage * R::kXBytes, static_cast<const XT *>(p.x) + off, R::kXBytes, &full[stage]);
-        if constexpr (HAS_G)
-            tma_load_1d(ring + 2 * R::kXBytes + stage * R::kGBytes, static_cast<const GT *>(p.g) + off,
-                        R::kGBytes, &full[stage]);
-    };
-    unsigned phase[2] = {0u, 0u};
-    if (threadIdx.x == 0 && blockIdx.x < items && staged(blockIdx.x)) issue(blockIdx.x, 0);
-
-    int it = 0;
-    for (long long w = blockIdx.x; w < items; w += gridDim.x, ++it) {
-        const int t = static_cast<int>(w / k);
-        const int a = static_cast<int>(w % k);
-        const long long base = static_cast<long long>(t) * kTile;
-        const long long rem = count - base;
-        const int stage = it & 1;
-        // prefetch the next item of this CTA while this one is processed
-        const long long wn = w + gridDim.x;
-        if (threadIdx.x == 0 && wn < items && staged(wn)) issue(wn, stage ^ 1);
-
-        // ---- Eq. 4 local update (ATC) or plain input (neighbor_allreduce) ----
-        float xh[kVecPerThread][4];
-        if (staged(w)) {
-            mbar_wait_b(g, &full[stage], phase[stage], &s_fail);
-            phase[stage] ^= 1u;
-            const XT *xs = reinterpret_cast<const XT *>(ring + stage * R::kXBytes);
-#pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j) Vec4<XT>::load(xs + tile_elem(j), xh[j], 4, true);
-            if constexpr (HAS_G) {
-                const GT *gs = reinterpret_cast<const GT *>(ring + 2 * R::kXBytes + stage * R::kGBytes);
-#pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j) {
-                    float gv[4];
-                    Vec4<GT>::load(gs + tile_elem(j), gv, 4, true);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
-                }
-            }
-        } else {
-            const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(a) * count + base;
-#pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j)
-                Vec4<XT>::load(xr + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
-            if constexpr (HAS_G) {
-                const GT *gr = static_cast<const GT *>(p.g) + static_cast<long long>(a) * count + base;
-#pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j) {
-                    float gv[4];
-                    Vec4<GT>::load(gr + tile_elem(j), gv, clamp_valid(rem, tile_elem(j)), vec);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
-                }
-            }
-        }
-
-        // ---- publish the wire copy into this agent's slot, release flag ----
-        WT *mine = at<WT>(g.peer_base[g.me], p.slot_off + a * p.slot_agent_stride +
-                                                 parity * p.slot_parity_stride) + base;
-#pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j)
-            Vec4<WT>::store(mine + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
-        __syncthreads();
-        if (threadIdx.x == 0)
-            st_release(ready_ptr(g, p.ready_off, p.ready_stride, g.me * k + a, t), e, sys);
-
-        // ---- wait for the in-neighbours' tile t ----
-        const int ns = st.nsrc[a];
-        if (threadIdx.x < ns) {
-            if (!spin_ge(g, ready_ptr(g, p.ready_off, p.ready_stride, st.src[a][threadIdx.x], t), e, sys))
-                s_fail = 1;
-        }
-        __syncthreads();
-        if (s_fail) {
-            // drain the in-flight prefetch before the CTA exits (its smem may be reused)
-            if (threadIdx.x == 0 && wn < items && staged(wn)) {
-                volatile int no_fail = 0;
-                mbar_wait_b(g, &full[stage ^ 1], phase[stage ^ 1], &no_fail);
-            }
-            return;
-        }
-
-        // ---- Eq. 5 / Eq. 9 weighted combine in fp32 ----
-        float acc[kVecPerThread][4];
-        const float cs = st.self_w[a];
-#pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[j][i] = cs * xh[j][i];
-        for (int q = 0; q < ns; ++q) {
-            const int src = st.src[a][q];
-            const float c = st.coef[a][q];
-            const WT *sp = at<const WT>(g.peer_base[src / k],
-                                        p.slot_off + (src % k) * p.slot_agent_stride +
-                                            parity * p.slot_parity_stride) + base;
-            float v[kVecPerThread][4];
-#pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j)
-                Vec4<WT>::load_cg(sp + tile_elem(j), v[j], clamp_valid(rem, tile_elem(j)), vec);
-#pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(c, v[j][i], acc[j][i]);
-        }
-
-        // ---- store (cast) ----
-        YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base;
-#pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j)
-            Vec4<YT>::store(yr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
-        if (p.shadow) {
-            bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base;
-#pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j)
-                Vec4<bf16>::store(sr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
-        }
-    }
-
-    last_cta(pad, [&] {
-        pad->epoch = e;
-        if (p.wmode == kWSchedule) pad->round = pad->round + 1;
-        publish_done(g, e);
-    });
-}
-
-#ifndef BF_LAG
-#define BF_LAG 3
-#endif
-#ifndef BF_PSTAGES
-#define BF_PSTAGES 3
-#endif
-#ifndef BF_CSTAGES
-#define BF_CSTAGES 2
-#endif
-#ifndef BF_NPEER
-#define BF_NPEER 2
-#endif
-constexpr int kConsumerWarps = kThreads / 32;          // 8 consumer warps
-constexpr int kExchThreads = kThreads + 96;            // + 2 producer warps + 1 signal warp
-constexpr int kPub = 16;                               // ring of "published" notifications
-
-// Walks the items w = first, first + stride, ... as (tile t, local agent a)
-// with w = t*k + a, without integer division in the loop.
-struct ItemIt {
-    int t, a, dt, da, k;
-    __device__ ItemIt(int first, int stride, int k_) : t(first / k_), a(first % k_), dt(stride / k_),
-                                                          da(stride % k_), k(k_) {}
-    __device__ __forceinline__ void next() {
-        t += dt;
-        a += da;
-        if (a >= k) {
-            a -= k;
-            ++t;
-        }
-    }
-};
-
-// Per-CTA shared-memory pipelines.
-//   publish ring (PS stages): x / g tile of an item to publish (DRAM reads in flight)
-//   combine ring (CS stages): the tiles combined for an item.  When the wire copy
-//   IS the fp32 x_half (fp32 wire, or neighbor_allreduce) the self term is the
-//   agent's own published tile, staged like a neighbour's (an L2 hit); for ATC
-//   with a bf16 wire the stage re-reads x / g to recompute the fp32 x_half (R18).
-template <typename XT, typename GT, typename WT, bool HAS_G>
-struct Pipe {
-    static constexpr int D = BF_LAG, PS = BF_PSTAGES, CS = BF_CSTAGES, NP = BF_NPEER;
-    static constexpr bool SELF_XG = HAS_G && sizeof(WT) < 4;
-    static constexpr unsigned XB = kTile * sizeof(XT);
-    static constexpr unsigned GB = HAS_G ? kTile * sizeof(GT) : 0;
-    static constexpr unsigned PB = kTile * sizeof(WT);
-    static constexpr unsigned XG = XB + GB;
-    static constexpr int NT = NP + (SELF_XG ? 0 : 1);               // staged tiles per combine stage
-    static constexpr unsigned CST = (SELF_XG ? XG : 0) + NT * PB;
-    static constexpr unsigned BYTES = PS * XG + CS * CST;
-};
-
-// exchange_pipe_kernel: warp-specialised persistent pipeline, one CTA per SM
-// (alternative to exchange_kernel, selected with BF_EXCH=pipe).
-//   producer A : TMA bulk loads of the x / g tiles of items to publish
-//   producer B : TMA bulk loads of the x / g tiles of items to combine (L2 hits,
-//                they were published D items earlier), then acquire the
-//                in-neighbours' ready flags of the tile and LDGSTS (cp.async)
-//                their published tiles -- over NVLink for agents on other GPUs,
-//                from L2 for agents on this GPU
-//   signal     : releases the ready flag of every published tile (the release
-//                fence runs off the consumers' critical path)
-//   consumers  : iteration c publishes item c+D (Eq. 4 adapt, wire copy into
-//                this agent's IPC slot) and combines item c (Eq. 5 / Eq. 9,
-//                fp32) from shared memory.
-// Publishing D items ahead means a neighbour's tile is normally published long
-// before anybody needs it.  Deadlock freedom: items are visited in increasing
-// tile order; publish-side loads never wait on other agents; a tile is
-// published before its owner waits on the tile of any later item; all CTAs are
-// co-resident (cooperative launch) and grid >= local agents.  A fault never
-// exits early: waits fail fast, garbage is computed, the fault is latched, and
-// no TMA or cp.async is left in flight.
-template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
-__global__ void __launch_bounds__(kExchThreads, 1) exchange_pipe_kernel(const __grid_constant__ ExchParams p) {
-    using P = Pipe<XT, GT, WT, HAS_G>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ SharedTab st;
-    __shared__ __align__(8) unsigned long long fullP[P::PS], emptyP[P::PS];
-    __shared__ __align__(8) unsigned long long published[kPub], signaled[kPub];
-    __shared__ __align__(8) unsigned long long fullC[P::CS], emptyC[P::CS];
-    __shared__ int s_fail, drain_fail;
-    volatile int *const fail = &s_fail;
-    const Geometry &g = p.geo;
-    Pad *pad = pad_of(g, g.me);
-    if (aborted(g)) return;
-    const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
-    const int parity = static_cast<int>(e & 1);
-    const bool sys = g.nprocs > 1;   // flags of agents on other GPUs need system scope
-
-    if (threadIdx.x == 0) {
-        s_fail = 0;
-        drain_fail = 0;
-        for (int i = 0; i < P::PS; ++i) {
-            mbar_init(&fullP[i], 1);
-            mbar_init(&emptyP[i], kConsumerWarps);
-        }
-        for (int i = 0; i < kPub; ++i) {
-            mbar_init(&published[i], kConsumerWarps);
-            mbar_init(&signaled[i], 1);
-        }
-        for (int i = 0; i < P::CS; ++i) {
-            mbar_init(&fullC[i], 1 + 32);                 // TMA / plain arrive + 32 cp.async lanes
-            mbar_init(&emptyC[i], kConsumerWarps);
-        }
-        fence_mbar_init();
-    }
-    bool ok = war_wait(g, e);
-    if (p.wmode == kWDynamic) write_descriptors(p, e);
-    ok = resolve_sources(p, e, st) && ok;
-    if (!ok && threadIdx.x == 0) s_fail = 1;
-    __syncthreads();
-
-    const bool vec = g.vec_ok != 0;
-    const long long count = g.count;
-    const int k = g.k;
-    const int items = k * g.T;
-    const int nfull = static_cast<int>(count / kTile);   // tiles that are full
-    const int nmine = static_cast<int>(blockIdx.x) < items
-                          ? (items - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
-                                static_cast<int>(gridDim.x)
-                          : 0;
-    auto staged = [&](int t) { return vec && t < nfull; };   // TMA needs 16B-aligned rows and a full tile
-    unsigned char *const ringP = smem;
-    unsigned char *const ringC = smem + P::PS * P::XG;
-    auto xP = [&](int s) { return ringP + s * P::XG; };
-    auto xC = [&](int s) { return ringC + s * P::CST; };
-    auto tC = [&](int s, int q) { return ringC + s * P::CST + (P::SELF_XG ? P::XG : 0) + q * P::PB; };
-    auto slot_of = [&](int agent) {
-        return at<WT>(g.peer_base[agent / k],
-                      p.slot_off + (agent % k) * p.slot_agent_stride + parity * p.slot_parity_stride);
-    };
-    auto failed = [&]() { return *reinterpret_cast<volatile int *>(&s_fail) != 0; };
-    auto tma_xg = [&](int t, int a, unsigned char *dst, unsigned long long *bar) {   // lane 0 only
-        const long long off = static_cast<long long>(a) * count + static_cast<long long>(t) * kTile;
-        fence_proxy_async();
-        mbar_expect_tx(bar, P::XG);
-        tma_load_1d(dst, static_cast<const XT *>(p.x) + off, P::XB, bar);
-        if constexpr (HAS_G) tma_load_1d(dst + P::XB, static_cast<const GT *>(p.g) + off, P::GB, bar);
-    };
-    // agent whose published tile is staged in tile slot q of a combine stage
-    auto staged_agent = [&](int a, int q) {
-        if constexpr (P::SELF_XG) return static_cast<int>(st.src[a][q]);
-        return q == 0 ? g.me * k + a : static_cast<int>(st.src[a][q - 1]);
-    };
-    auto n_staged = [&](int a) { return min(st.nsrc[a], P::NP) + (P::SELF_XG ? 0 : 1); };
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    if (warp == kConsumerWarps) {
-        // ====================== producer A: publish-side x / g ======================
-        ItemIt it(blockIdx.x, gridDim.x, k);
-        int issued = 0;
-        for (int c = 0; c < nmine; ++c, it.next()) {
-            const int s = c % P::PS;
-            bool okw = true;   // lane 0 waits, the warp follows its verdict (no divergent break)
-            if (c >= P::PS && lane == 0) okw = mbar_wait_b(g, &emptyP[s], static_cast<unsigned>(c / P::PS - 1) & 1u, fail);
-            if (!__shfl_sync(0xffffffffu, okw, 0)) break;
-            issued = c + 1;
-            if (lane == 0) {
-                if (staged(it.t))
-                    tma_xg(it.t, it.a, xP(s), &fullP[s]);
-                else
-                    mbar_arrive(&fullP[s]);
-            }
-            __syncwarp();
-        }
-        // drain: every armed phase completes before the CTA can exit
-        if (lane == 0)
-            for (int c = max(0, issued - P::PS); c < issued; ++c)
-                mbar_wait_b(g, &fullP[c % P::PS], static_cast<unsigned>(c / P::PS) & 1u, &drain_fail);
-    } else if (warp == kConsumerWarps + 1) {
-        // ========== producer B: the published tiles combined for each item ==========
-        ItemIt it(blockIdx.x, gridDim.x, k);
-        int issued = 0;
-        for (int c = 0; c < nmine; ++c, it.next()) {
-            const int s = c % P::CS;
-            bool okw = true;
-            if (c >= P::CS && lane == 0) okw = mbar_wait_b(g, &emptyC[s], static_cast<unsigned>(c / P::CS - 1) & 1u, fail);
-            if (!__shfl_sync(0xffffffffu, okw, 0)) break;
-            issued = c + 1;
-            const int t = it.t, a = it.a;
-            const long long base = static_cast<long long>(t) * kTile;
-            if (lane == 0) {
-                if (P::SELF_XG && staged(t))
-                    tma_xg(t, a, xC(s), &fullC[s]);
-                else
-                    mbar_arrive(&fullC[s]);
-            }
-            const int nt = n_staged(a);
-            bool good = true;
-            if (lane < nt && !failed())
-                good = spin_ge(g, ready_ptr(g, p.ready_off, p.ready_stride, staged_agent(a, lane), t), e, sys);
-            if (!__all_sync(0xffffffffu, good) && lane == 0) s_fail = 1;
-            __syncwarp();
-            if (!failed()) {
-                const long long rem_bytes = (count - base) * static_cast<long long>(sizeof(WT));
-                for (int q = 0; q < nt; ++q) {
-                    const unsigned char *src =
-                        reinterpret_cast<const unsigned char *>(slot_of(staged_agent(a, q)) + base);
-                    unsigned char *dst = tC(s, q);
-#pragma unroll 4
-                    for (int ch = lane; ch < static_cast<int>(P::PB / 16); ch += 32) {
-                        const long long left = rem_bytes - 16ll * ch;
-                        const unsigned nb = left >= 16 ? 16u : (left <= 0 ? 0u : static_cast<unsigned>(left));
-                        cp_async16(dst + 16 * ch, nb ? src + 16 * ch : src, nb);
-                    }
-                }
-            }
-            cp_async_mbar_arrive_noinc(&fullC[s]);
-        }
-        if (lane == 0)
-            for (int c = max(0, issued - P::CS); c < issued; ++c)
-                mbar_wait_b(g, &fullC[c % P::CS], static_cast<unsigned>(c / P::CS) & 1u, &drain_fail);
-    } else if (warp == kConsumerWarps + 2) {
-        // ======== signal warp: release the ready flags of published tiles ========
-        // One release fence covers every tile already published (batch), so the
-        // fence cost is paid per batch, not per tile, and never by the consumers.
-        if (lane == 0) {
-            ItemIt it(blockIdx.x, gridDim.x, k);
-            int c = 0;
-            while (c < nmine) {
-                const bool okp = mbar_wait_b(g, &published[c % kPub], static_cast<unsigned>(c / kPub) & 1u, fail);
-                int c_end = c + 1;
-                while (okp && c_end < nmine && c_end - c < kPub / 2 &&
-                       mbar_test(&published[c_end % kPub], static_cast<unsigned>(c_end / kPub) & 1u))
-                    ++c_end;
-                if (okp) fence_acq_rel(sys);
-                for (int i = c; i < c_end; ++i, it.next()) {
-                    if (okp) st_relaxed(ready_ptr(g, p.ready_off, p.ready_stride, g.me * k + it.a, it.t), e, sys);
-                    mbar_arrive(&signaled[i % kPub]);
-                }
-                c = c_end;
-            }
-        }
-        __syncwarp();
-    } else {
-        // =============================== consumers ===============================
-        // x_half of item (t, a) from a staged x/g tile, or straight from global memory
-        auto adapt = [&](int t, int a, const unsigned char *stage, float (&xh)[kVecPerThread][4]) {
-            const long long base = static_cast<long long>(t) * kTile, rem = count - base;
-            if (staged(t)) {
-                const XT *xsm = reinterpret_cast<const XT *>(stage);
-#pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j) Vec4<XT>::load(xsm + tile_elem(j), xh[j], 4, true);
-                if constexpr (HAS_G) {
-                    const GT *gsm = reinterpret_cast<const GT *>(stage + P::XB);
-#pragma unroll
-                    for (int j = 0; j < kVecPerThread; ++j) {
-                        float gv[4];
-                        Vec4<GT>::load(gsm + tile_elem(j), gv, 4, true);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
-                    }
-                }
-            } else {
-                const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(a) * count + base;
-#pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j)
-                    Vec4<XT>::load(xr + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), vec);
-                if constexpr (HAS_G) {
-                    const GT *gr = static_cast<const GT *>(p.g) + static_cast<long long>(a) * count + base;
-#pragma unroll
-                    for (int j = 0; j < kVecPerThread; ++j) {
-                        float gv[4];
-                        Vec4<GT>::load(gr + tile_elem(j), gv, clamp_valid(rem, tile_elem(j)), vec);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) xh[j][i] = fmaf(-p.lr, gv[i], xh[j][i]);
-                    }
-                }
-            }
-        };
-        ItemIt itP(blockIdx.x, gridDim.x, k);   // next item to publish
-        ItemIt itC(blockIdx.x, gridDim.x, k);   // next item to combine
-        for (int c = -P::D; c < nmine; ++c) {
-            // ---- publish item c + D: Eq. 4 local update, wire copy into the slot ----
-            const int cp = c + P::D;
-            if (cp >= 0 && cp < nmine) {
-                const int s = cp % P::PS;
-                const int t = itP.t, a = itP.a;
-                const long long base = static_cast<long long>(t) * kTile, rem = count - base;
-                mbar_wait_b(g, &fullP[s], static_cast<unsigned>(cp / P::PS) & 1u, fail);
-                float xh[kVecPerThread][4];
-                adapt(t, a, xP(s), xh);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyP[s]);   // x / g consumed: producer A may refill
-                WT *mine = slot_of(g.me * k + a) + base;
-#pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j)
-                    Vec4<WT>::store(mine + tile_elem(j), xh[j], clamp_valid(rem, tile_elem(j)), true);
-                __syncwarp();
-                if (lane == 0) {
-                    if (cp >= kPub)   // the signal warp has consumed the notification kPub items back
-                        mbar_wait_b(g, &signaled[cp % kPub], static_cast<unsigned>(cp / kPub - 1) & 1u, fail);
-                    mbar_arrive(&published[cp % kPub]);   // the signal warp releases the flag
-                }
-                itP.next();
-            }
-            if (c < 0) continue;
-            // ---- combine item c: Eq. 5 / Eq. 9 in fp32 ----
-            const int t = itC.t, a = itC.a;
-            itC.next();
-            const long long base = static_cast<long long>(t) * kTile, rem = count - base;
-            const int s = c % P::CS;
-            mbar_wait_b(g, &fullC[s], static_cast<unsigned>(c / P::CS) & 1u, fail);
-            float acc[kVecPerThread][4];
-            const float cs = st.self_w[a];
-            int q0 = 0;
-            if constexpr (P::SELF_XG) {
-                adapt(t, a, xC(s), acc);   // fp32 x_half for the self term (R18)
-#pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[j][i] *= cs;
-            } else {
-                // own published tile == the fp32 x_half (fp32 wire) or x itself
-                const WT *sm0 = reinterpret_cast<const WT *>(tC(s, 0));
-#pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j) {
-                    Vec4<WT>::load(sm0 + tile_elem(j), acc[j], 4, true);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[j][i] *= cs;
-                }
-                q0 = 1;
-            }
-            const int ns = st.nsrc[a];
-            const int np = min(ns, P::NP);
-            for (int q = 0; q < np; ++q) {
-                const WT *psm = reinterpret_cast<const WT *>(tC(s, q0 + q));
-                const float cq = st.coef[a][q];
-#pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j) {
-                    float v[4];
-                    Vec4<WT>::load(psm + tile_elem(j), v, 4, true);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(cq, v[i], acc[j][i]);
-                }
-            }
-            if (ns > np) {   // more in-neighbours than staged tiles: read the rest directly
-                if (threadIdx.x < ns - np && !failed()) {
-                    if (!spin_ge(g, ready_ptr(g, p.ready_off, p.ready_stride, st.src[a][np + threadIdx.x], t), e,
-                                 sys))
-                        s_fail = 1;
-                }
-                named_bar_sync(1, kThreads);
-                for (int q = np; q < ns; ++q) {
-                    const WT *sp2 = slot_of(st.src[a][q]) + base;
-                    const float cq = st.coef[a][q];
-#pragma unroll
-                    for (int j = 0; j < kVecPerThread; ++j) {
-                        float v[4];
-                        Vec4<WT>::load_cg(sp2 + tile_elem(j), v, clamp_valid(rem, tile_elem(j)), true);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(cq, v[i], acc[j][i]);
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&emptyC[s]);
-            YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base;
-#pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j)
-                Vec4<YT>::store(yr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
-            if (p.shadow) {
-                bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base;
-#pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j)
-                    Vec4<bf16>::store(sr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
-            }
-        }
-    }
-
-    __syncthreads();
-    if (s_fail) return;   // nothing is in flight any more; the fault is latched
-    last_cta(pad, [&] {
-        pad->epoch = e;
-        if (p.wmode == kWSchedule) pad->round = pad->round + 1;
-        publish_done(g, e);
-    });
-}
-
 // --------------------------------------------------------------------------
-// exchange_chunk_kernel (kernel 2, default): chunk-granular synchronisation.
+// exchange_chunk_kernel (kernel 2): chunk-granular synchronisation.
 // The tiles are grouped into chunks of CT tiles (per agent).  Every CTA walks
 // its items (grid-stride, tile-major) twice: it PUBLISHES them (Eq. 4 adapt,
 // wire copy into the IPC slot) and COMBINES them (Eq. 5 / Eq. 9), the combine
@@ -1128,30 +444,42 @@ int max_coresident(const void *func, int threads, size_t smem) {
 
 template <typename XT, typename GT, typename WT, typename YT, bool HAS_G>
 static cudaError_t launch_exch_t(const ExchParams &p, int grid, cudaStream_t s) {
-    const int kind = p.kernel;
-    const bool pipe = kind == 1;
-    const void *fn = pipe ? reinterpret_cast<const void *>(exchange_pipe_kernel<XT, GT, WT, YT, HAS_G>)
-                          : (kind == 2 ? reinterpret_cast<const void *>(exchange_chunk_kernel<XT, GT, WT, YT, HAS_G>)
-                                       : reinterpret_cast<const void *>(exchange_kernel<XT, GT, WT, YT, HAS_G>));
-    const unsigned smem = pipe ? Pipe<XT, GT, WT, HAS_G>::BYTES : Ring<XT, GT, HAS_G>::kBytes;
-    const int threads = pipe ? kExchThreads : kThreads;
-    static bool attr_set[3] = {false, false, false};
-    if (!attr_set[kind]) {
+    const void *fn = reinterpret_cast<const void *>(exchange_chunk_kernel<XT, GT, WT, YT, HAS_G>);
+    const unsigned smem = Ring<XT, GT, HAS_G>::kBytes;
+    static int maxg = 0;   // co-resident CTAs of this instantiation (queried once)
+    if (maxg == 0) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr_set[kind] = true;
+        maxg = max_coresident(fn, kThreads, smem);
     }
-    const int maxg = max_coresident(fn, threads, smem);
     if (grid <= 0 || grid > maxg) grid = maxg;
     const long long items = static_cast<long long>(p.geo.k) * p.geo.T;
     if (grid > items) grid = static_cast<int>(items < p.geo.k ? p.geo.k : items);
     if (grid < 1) grid = 1;
     void *args[] = {const_cast<ExchParams *>(&p)};
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, s);
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);
+}
+
+bool fused_supported(int k, int nprocs) { return k == 1 || k == 2 || k == 4 || (k == 8 && nprocs == 1); }
+
+static cudaError_t launch_fused(const ExchParams &p, int x_kind, int g_kind, int wire_kind, int y_kind, int has_g,
+                                int grid, cudaStream_t s) {
+    if (p.awc) {   // AWC: fp32 master x, wire = the x value in the wire dtype
+        if (x_kind != 0 || y_kind != 0) return cudaErrorInvalidValue;
+        return launch_fused_awc(p, p.g_bf16 ? 1 : 0, wire_kind, grid, s);
+    }
+    if (!has_g) {
+        if (x_kind != wire_kind || x_kind != y_kind) return cudaErrorInvalidValue;
+        return launch_fused_nar(p, x_kind, grid, s);
+    }
+    if (x_kind != 0 || y_kind != 0) return cudaErrorInvalidValue;
+    return launch_fused_atc(p, g_kind, wire_kind, grid, s);
 }
 
 cudaError_t launch_exchange(const ExchParams &p, int x_kind, int g_kind, int wire_kind, int y_kind,
                             int has_g, int grid, cudaStream_t s) {
+    if (p.kernel == 3) return launch_fused(p, x_kind, g_kind, wire_kind, y_kind, has_g, grid, s);
+    // kernel 2 (chunked): any number of local agents
     // neighbor_allreduce: x = wire = y dtype
     if (!has_g) {
         if (x_kind == 0 && wire_kind == 0 && y_kind == 0)

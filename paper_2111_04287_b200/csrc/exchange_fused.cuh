@@ -1,0 +1,409 @@
+// exchange_fused.cuh -- the local-agent fused exchange kernel (kernel 3) and its
+// launch templates; instantiated per operation in fused_nar.cu (MODE 0),
+// fused_atc.cu (MODE 1) and fused_awc.cu (MODE 2) so they compile in parallel.
+#pragma once
+
+#include "exchange_common.cuh"
+
+namespace bf {
+
+// --------------------------------------------------------------------------
+// exchange_fused_kernel (kernel 3, default when the process hosts K = 1, 2, 4
+// or 8 agents).  The K agents of one process share one GPU, so their part of
+// the exchange never has to leave the SM: a consumer thread loads the same
+// 4-element vector of x (and g) of ALL K local agents into registers, forms
+// every x_half there (Eq. 4), and combines each agent's local sources straight
+// from those registers (Eq. 5 / Eq. 9) -- the K x K local block of W is applied
+// in registers.  Only sources on OTHER processes go through the published slots:
+//   * a local agent whose x_half is read by another process (pub mask)
+//     publishes its wire copy kLead sub-items ahead of the combine;
+//   * synchronisation is pairwise between CTAs, not global: sub-item s is
+//     handled by CTA s mod G on every process (same grid everywhere), so CTA b
+//     only ever needs what CTA b of the source process published.  CTA b
+//     releases a progress counter prog[b] = e * 2^24 + (sub-items published)
+//     every kBatch sub-items -- no chunk barrier over all CTAs of both GPUs,
+//     so a slow CTA delays only its peer;
+//   * one communication warp per CTA (lane 0, an event loop that never blocks)
+//     does all cross-GPU work off the consumers' path: it turns the consumers'
+//     "batch published" mbarrier arrivals into system-scope releases of prog[b]
+//     (the fence.acq_rel.sys costs microseconds -- measured: releasing every 2
+//     sub-items from a consumer thread made an HBM-bound round 1.45x slower),
+//     and it pulls the remote sources' tiles over NVLink with TMA bulk copies
+//     (cp.async.bulk, peer addresses of the CUDA-IPC mappings) into a ring of
+//     NSLOT shared-memory slots, up to NSLOT tiles ahead of the consumers, so
+//     the NVLink latency (calibrated 2.7 us one way) never stalls the HBM
+//     stream of the local agents.
+// HBM traffic per agent-element drops from x + g + publish + x (16 B fp32) to
+// x + g + x (12 B) for every agent without remote readers -- at N = 1 that is
+// every agent.
+//   MODE 0: neighbor_allreduce (x is the wire value)
+//   MODE 1: ATC  (Eq. 4-5, Eq. 17):  y_a = sum_b w_ab (x_b - lr g_b)
+//   MODE 2: AWC  (Eq. 16):           y_a = sum_b w_ab x_b - lr g_a
+// Summation order (R18): self, local sources in (a - b) mod K order, then the
+// remote sources in table order; a neighbour's term always uses the value as it
+// travels on the wire (bf16 RNE for a bf16 wire), the self term the fp32 value.
+// Deadlock freedom: consumers publish sub-item m + kLead before they consume
+// sub-item m; the communication warp never blocks (it polls), so releases
+// always follow publication; every wait is bounded by the context timeout.
+constexpr int kSub = kThreads * kVec;      // elements per sub-item: one vector per consumer thread
+constexpr int kNSlot = 16;                 // remote-tile ring slots per CTA
+#ifndef BF_LEAD
+#define BF_LEAD 24
+#endif
+#ifndef BF_BATCH
+#define BF_BATCH 8
+#endif
+constexpr int kLead = BF_LEAD;             // sub-items published ahead of the combine
+constexpr int kBatch = BF_BATCH;           // sub-items per progress release
+constexpr int kProgShift = 24;             // prog = epoch << 24 | sub-items published
+constexpr int kPubRing = 16;               // "batch published" mbarriers (ring)
+// K = 8 local agents (N = 1 of the 8-agent configs) has no remote sources: no
+// producer warp, and the 128-register budget of 2 x 256 threads per SM holds
+// the 16 vectors in flight per thread without spilling.
+// K <= 2 keep too few loads in flight per thread with one sub-item: they
+// combine U = 2 sub-items per iteration (the loads of both issued first).
+template <int K>
+struct FusedCfg {
+    static constexpr bool kRing = K < 8;
+    static constexpr int kThreadsPerCta = kThreads + (kRing ? 32 : 0);   // 8 consumer warps (+ producer)
+    static constexpr int kUnroll = K <= 2 ? 2 : 1;
+};
+
+template <int K>
+struct LocalMix {
+    float c[K][K];                     // c[a][b]: weight of local agent b in agent a's combine
+    float rc[K * kMaxS];               // remote entries, agent-major: weight ...
+    unsigned char rs[K * kMaxS];       // ... and global source agent
+    int rbeg[K + 1];                   // entries of agent a: [rbeg[a], rbeg[a+1])
+    unsigned pub;                      // bit a: agent a's x_half is read by another process
+    unsigned procs;                    // bit q: process q hosts a remote source
+};
+
+template <typename XT, typename GT, typename WT, typename YT, int MODE, int K>
+__global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
+    exchange_fused_kernel(const __grid_constant__ ExchParams p) {
+    constexpr bool HAS_G = MODE != 0;
+    constexpr int U = FusedCfg<K>::kUnroll;
+    constexpr unsigned kSlotBytes = kSub * sizeof(WT);
+    extern __shared__ __align__(128) unsigned char ring[];
+    __shared__ SharedTab st;
+    __shared__ LocalMix<K> lm;
+    __shared__ __align__(8) unsigned long long full[kNSlot], empty[kNSlot], pubbar[kPubRing];
+    __shared__ int s_fail;
+    __shared__ int s_released;   // batches released by the communication warp
+    volatile int *const fail = &s_fail;
+    const Geometry &g = p.geo;
+    Pad *pad = pad_of(g, g.me);
+    if (aborted(g)) return;
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
+    const int parity = static_cast<int>(e & 1);
+    const bool sys = g.nprocs > 1;
+    if (threadIdx.x == 0) {
+        s_fail = 0;
+        s_released = 0;
+        for (int i = 0; i < kNSlot; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kThreads / 32);
+        }
+        for (int i = 0; i < kPubRing; ++i) mbar_init(&pubbar[i], kThreads / 32);
+        fence_mbar_init();
+    }
+    bool ok = war_wait(g, e);
+    if (p.wmode == kWDynamic) write_descriptors(p, e);
+    ok = resolve_sources(p, e, st) && ok;
+    if (!ok) return;   // fault latched; nothing in flight yet
+
+    // ---- split every agent's sources into the local block and the remote list ----
+    if (threadIdx.x == 0) {
+        unsigned procs = 0;
+        int nr = 0;
+        for (int a = 0; a < K; ++a) {
+            for (int b = 0; b < K; ++b) lm.c[a][b] = 0.f;
+            lm.c[a][a] = st.self_w[a];
+            lm.rbeg[a] = nr;
+            for (int q = 0; q < st.nsrc[a]; ++q) {
+                const int src = st.src[a][q];
+                if (src / K == g.me) {
+                    lm.c[a][src % K] += st.coef[a][q];
+                } else {
+                    lm.rs[nr] = static_cast<unsigned char>(src);
+                    lm.rc[nr] = st.coef[a][q];
+                    procs |= 1u << (src / K);
+                    ++nr;
+                }
+            }
+        }
+        lm.rbeg[K] = nr;
+        lm.procs = procs;
+        unsigned pub = 0;
+        if (g.nprocs > 1) {
+            if (p.wmode == kWStatic) {
+                pub = p.pub_mask;
+            } else if (p.wmode == kWSchedule) {   // one-peer exp-2: agent i pushes to i + 2^t (R5)
+                const unsigned long long round = *reinterpret_cast<volatile unsigned long long *>(&pad->round);
+                int tau = 0;
+                while ((1 << tau) < g.n) ++tau;
+                if (tau > 0) {
+                    const int off = 1 << static_cast<int>(round % tau);
+                    for (int a = 0; a < K; ++a)
+                        if (((g.me * K + a + off) % g.n) / K != g.me) pub |= 1u << a;
+                }
+            } else {
+                pub = (1u << K) - 1u;   // pull-only readers are not known to the sender
+            }
+        }
+        lm.pub = pub;
+    }
+    __syncthreads();
+
+    const bool vec = g.vec_ok != 0;
+    const long long count = g.count;
+    const int G = gridDim.x;
+    const int S = static_cast<int>((count + kSub - 1) / kSub);
+    const int nmine = static_cast<int>(blockIdx.x) < S ? (S - static_cast<int>(blockIdx.x) + G - 1) / G : 0;
+    const int nrt = lm.rbeg[K];   // remote tiles per sub-item
+    auto slot_of = [&](int agent) {
+        return at<WT>(g.peer_base[agent / K],
+                      p.slot_off + (agent % K) * p.slot_agent_stride + parity * p.slot_parity_stride);
+    };
+    auto sub = [&](int m) { return static_cast<int>(blockIdx.x) + m * G; };
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == kThreads / 32) {
+        // ============ communication warp (lane 0): releases + TMA pulls ============
+        const int nbatch = lm.pub ? (nmine + kBatch - 1) / kBatch : 0;
+        if (FusedCfg<K>::kRing && lane == 0 && (nrt > 0 || nbatch > 0)) {
+            unsigned long long *prog = at<unsigned long long>(g.peer_base[g.me], p.prog_off) + blockIdx.x;
+            volatile int *released = &s_released;
+            long long issued = 0;              // ring entries issued
+            const long long total = static_cast<long long>(nmine) * nrt;
+            unsigned long long seen[kMaxP];    // last acquired progress of each source process
+            for (int q = 0; q < kMaxP; ++q) seen[q] = 0;
+            int rb = 0;                        // batches released
+            unsigned long long t_idle = globaltimer();
+            unsigned it = 0;
+            while ((rb < nbatch || issued < total) && !*fail) {
+                bool progressed = false;
+                // (1) release every batch the consumers have published
+                while (rb < nbatch && mbar_test(&pubbar[rb % kPubRing], static_cast<unsigned>(rb / kPubRing) & 1u)) {
+                    const int done = min((rb + 1) * kBatch, nmine);
+                    fence_acq_rel(true);   // the consumers' slot stores, visible system-wide ...
+                    st_relaxed(prog, (e << kProgShift) | static_cast<unsigned long long>(done), true);   // ... first
+                    ++rb;
+                    *released = rb;
+                    progressed = true;
+                }
+                // (2) pull the remote tiles of the next sub-items while ring slots are free
+                while (issued < total) {
+                    const int m = static_cast<int>(issued / nrt), i = static_cast<int>(issued % nrt);
+                    const int sl = static_cast<int>(issued % kNSlot);
+                    if (issued >= kNSlot && !mbar_test(&empty[sl], static_cast<unsigned>(issued / kNSlot - 1) & 1u))
+                        break;   // slot still being read
+                    if (i == 0) {   // a new sub-item: every source process must have published it
+                        const unsigned long long need = (e << kProgShift) | static_cast<unsigned long long>(m + 1);
+                        bool ready = true, acquired = false;
+                        for (int q = 0; q < g.nprocs && ready; ++q) {
+                            if (!((lm.procs >> q) & 1u) || seen[q] >= need) continue;
+                            seen[q] = ld_acquire_sys(at<unsigned long long>(g.peer_base[q], p.prog_off) + blockIdx.x);
+                            ready = seen[q] >= need;
+                            acquired = true;
+                        }
+                        if (acquired) fence_proxy_async_global();   // acquire before the async-proxy reads
+                        if (!ready) break;
+                    }
+                    const long long base = static_cast<long long>(sub(m)) * kSub;
+                    const long long left = count - base;
+                    const unsigned bytes =
+                        (static_cast<unsigned>((left < kSub ? left : kSub) * sizeof(WT)) + 15u) & ~15u;
+                    mbar_expect_tx(&full[sl], bytes);
+                    tma_load_1d(ring + sl * kSlotBytes, slot_of(lm.rs[i]) + base, bytes, &full[sl]);
+                    ++issued;
+                    progressed = true;
+                }
+                if (progressed) {
+                    t_idle = globaltimer();
+                } else {   // nothing to do right now: bounded idle
+                    if ((++it & 63u) == 0) {
+                        const unsigned code = ld_relaxed_sys_u32(&pad->abort);
+                        if (code) {
+                            if (g.host_err) *g.host_err = code;
+                            *fail = 1;
+                        } else if (globaltimer() - t_idle > g.timeout_ns) {
+                            abort_all(g, BF_ERR_TIMEOUT);
+                            *fail = 1;
+                        }
+                    }
+                    __nanosleep(32);
+                }
+            }
+            // drain: no bulk copy may be in flight when the CTA exits
+            volatile int no_fail = 0;
+            for (long long i = issued > kNSlot ? issued - kNSlot : 0; i < issued; ++i)
+                mbar_wait_b(g, &full[i % kNSlot], static_cast<unsigned>(i / kNSlot) & 1u, &no_fail);
+        }
+    } else {
+        // ============================ consumer warps ============================
+        const unsigned pub = lm.pub;
+        const unsigned long long pol_stream = policy_evict_first();
+        const unsigned long long pol_keep = policy_evict_normal();
+        auto xrow = [&](int a) { return static_cast<const XT *>(p.x) + static_cast<long long>(a) * count; };
+        auto grow = [&](int a) { return static_cast<const GT *>(p.g) + static_cast<long long>(a) * count; };
+        unsigned long long *prog = at<unsigned long long>(g.peer_base[g.me], p.prog_off) + blockIdx.x;
+        // batch b published: each warp arrives (release.cta) once its slot stores are issued;
+        // the communication warp turns the completed phase into the system-scope release
+        auto batch_done = [&](int b) {
+            if (b >= kPubRing) {   // the ring slot's previous phase must have been released
+                volatile int *released = &s_released;
+                while (*released <= b - kPubRing && !*fail) __nanosleep(64);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pubbar[b % kPubRing]);
+        };
+        if (sys && pub == 0 && threadIdx.x == 0)   // nothing of this process is read remotely
+            st_relaxed(prog, (e << kProgShift) | static_cast<unsigned long long>(nmine), true);
+
+        long long consumed = 0;   // remote ring entries consumed
+        int mp = 0, mc = 0;
+        while (mc < nmine) {
+            if (FusedCfg<K>::kRing && pub && mp < nmine && mp <= mc + kLead) {
+                // ---- publish sub-item mp for the agents with remote readers ----
+                const long long base = static_cast<long long>(sub(mp)) * kSub;
+                const int e0 = threadIdx.x * kVec;
+                const int valid = clamp_valid(count - base, e0);
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    if (!((pub >> a) & 1u)) continue;
+                    float v[4];
+                    Vec4<XT>::load_hint(xrow(a) + base + e0, v, valid, vec, pol_keep);
+                    if constexpr (MODE == 1) {
+                        float gv[4];
+                        Vec4<GT>::load_hint(grow(a) + base + e0, gv, valid, vec, pol_keep);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) v[i] = fmaf(-p.lr, gv[i], v[i]);
+                    }
+                    Vec4<WT>::store_hint(slot_of(g.me * K + a) + base + e0, v, valid, true, pol_keep);
+                }
+                ++mp;
+                if (mp % kBatch == 0 || mp == nmine) batch_done((mp - 1) / kBatch);
+                continue;
+            }
+            // ---- combine sub-items mc .. mc + U - 1 ----
+            const int nu = min(U, nmine - mc);
+            const int e0 = threadIdx.x * kVec;
+            float xv[U][K][4];
+            float gv[U][HAS_G ? K : 1][4];
+            // every local load of the group is issued before the first use
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (u >= nu) break;
+                const long long base = static_cast<long long>(sub(mc + u)) * kSub;
+                const int valid = clamp_valid(count - base, e0);
+#pragma unroll
+                for (int a = 0; a < K; ++a)
+                    Vec4<XT>::load_hint(xrow(a) + base + e0, xv[u][a], valid, vec, pol_stream);
+                if constexpr (HAS_G) {
+#pragma unroll
+                    for (int a = 0; a < K; ++a)
+                        Vec4<GT>::load_hint(grow(a) + base + e0, gv[u][a], valid, vec, pol_stream);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (u >= nu) break;
+                const long long base = static_cast<long long>(sub(mc + u)) * kSub;
+                const int valid = clamp_valid(count - base, e0);
+                if constexpr (MODE == 1) {
+#pragma unroll
+                    for (int a = 0; a < K; ++a)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) xv[u][a][i] = fmaf(-p.lr, gv[u][a][i], xv[u][a][i]);   // Eq. 4
+                }
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    float acc[4];
+                    const float cs = lm.c[a][a];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[i] = cs * xv[u][a][i];
+#pragma unroll
+                    for (int d = 1; d < K; ++d) {
+                        const int b = (a + K - d) % K;
+                        const float c = lm.c[a][b];
+                        if (c != 0.f) {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) acc[i] = fmaf(c, Vec4<WT>::wire(xv[u][b][i]), acc[i]);
+                        }
+                    }
+                    if constexpr (FusedCfg<K>::kRing) {
+                        for (int i = lm.rbeg[a]; i < lm.rbeg[a + 1]; ++i) {   // remote sources from the TMA ring
+                            const long long idx = consumed + i;
+                            const int sl = static_cast<int>(idx % kNSlot);
+                            mbar_wait_b(g, &full[sl], static_cast<unsigned>(idx / kNSlot) & 1u, fail);
+                            float v[4];
+                            Vec4<WT>::load(reinterpret_cast<const WT *>(ring + sl * kSlotBytes) + e0, v, valid, true);
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&empty[sl]);
+                            const float c = lm.rc[i];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) acc[j] = fmaf(c, v[j], acc[j]);
+                        }
+                    }
+                    if constexpr (MODE == 2) {   // AWC (Eq. 16)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) acc[i] = fmaf(-p.lr, gv[u][a][i], acc[i]);
+                    }
+                    YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base + e0;
+                    Vec4<YT>::store_hint(yr, acc, valid, vec, pol_stream);
+                    if (p.shadow) {
+                        bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base + e0;
+                        Vec4<bf16>::store_hint(sr, acc, valid, vec, pol_stream);
+                    }
+                }
+                consumed += nrt;
+            }
+            mc += nu;
+        }
+    }
+    __syncthreads();
+    if (*fail) return;   // nothing is in flight any more; the fault is latched
+    last_cta(pad, [&] {
+        pad->epoch = e;
+        if (p.wmode == kWSchedule) pad->round = pad->round + 1;
+        publish_done(g, e);
+    });
+}
+
+template <typename XT, typename GT, typename WT, typename YT, int MODE, int K>
+static cudaError_t launch_fused_k(const ExchParams &p, int grid, cudaStream_t s) {
+    const void *fn = reinterpret_cast<const void *>(exchange_fused_kernel<XT, GT, WT, YT, MODE, K>);
+    // the remote-tile ring is only needed when other processes exist
+    const bool ringed = FusedCfg<K>::kRing && p.geo.nprocs > 1;
+    if (!FusedCfg<K>::kRing && p.geo.nprocs > 1) return cudaErrorInvalidValue;
+    const unsigned smem = ringed ? kNSlot * kSub * sizeof(WT) : 0;
+    static int maxg[2] = {0, 0};   // co-resident CTAs of this instantiation (queried once per smem size)
+    if (maxg[ringed] == 0) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kNSlot * kSub * sizeof(WT));
+        if (e != cudaSuccess) return e;
+        maxg[ringed] = max_coresident(fn, FusedCfg<K>::kThreadsPerCta, smem);
+    }
+    const long long subs = (p.geo.count + kSub - 1) / kSub;
+    if (grid <= 0 || grid > maxg[ringed]) grid = maxg[ringed];
+    if (grid > subs) grid = static_cast<int>(subs);
+    if (grid > kMaxGrid) grid = kMaxGrid;
+    if (grid < 1) grid = 1;
+    void *args[] = {const_cast<ExchParams *>(&p)};
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FusedCfg<K>::kThreadsPerCta), args, smem, s);
+}
+
+template <typename XT, typename GT, typename WT, typename YT, int MODE>
+static cudaError_t launch_fused_t(const ExchParams &p, int grid, cudaStream_t s) {
+    switch (p.geo.k) {
+        case 1: return launch_fused_k<XT, GT, WT, YT, MODE, 1>(p, grid, s);
+        case 2: return launch_fused_k<XT, GT, WT, YT, MODE, 2>(p, grid, s);
+        case 4: return launch_fused_k<XT, GT, WT, YT, MODE, 4>(p, grid, s);
+        case 8: return launch_fused_k<XT, GT, WT, YT, MODE, 8>(p, grid, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace bf

@@ -1,0 +1,14 @@
+// fused_awc.cu -- instantiations of the local-agent fused exchange kernel for
+// AWC (Eq. 16): every dtype combination x K = 1, 2, 4, 8 local agents.
+#include "exchange_fused.cuh"
+
+namespace bf {
+
+cudaError_t launch_fused_awc(const ExchParams &p, int g_kind, int wire_kind, int grid, cudaStream_t s) {
+    if (g_kind == 0 && wire_kind == 0) return launch_fused_t<float, float, float, float, 2>(p, grid, s);
+    if (g_kind == 0 && wire_kind == 1) return launch_fused_t<float, float, bf16, float, 2>(p, grid, s);
+    if (g_kind == 1 && wire_kind == 0) return launch_fused_t<float, bf16, float, float, 2>(p, grid, s);
+    return launch_fused_t<float, bf16, bf16, float, 2>(p, grid, s);
+}
+
+}  // namespace bf

@@ -84,9 +84,9 @@ struct bf_ctx {
     std::vector<double> WM;
     int sched_kind = 0;
     int topo_check = 1;
-    int exch_kernel = 2;                      // BF_EXCH: tile | pipe | chunk (default)
+    int exch_kernel = 3;                      // BF_EXCH: chunk | fused (default)
     int chunk_tiles = 0;                      // BF_CHUNK_TILES; 0 = 256 on one GPU, 1024 across GPUs
-    unsigned long long ccnt_off = 0, cflag_off = 0;
+    unsigned long long ccnt_off = 0, cflag_off = 0, prog_off = 0;
     // exchange region
     size_t exch_cap = 0;                      // bytes per agent per parity
     size_t exch_begin = 0, exch_top = 0;      // heap range of exchange (+ hierarchical) regions
@@ -183,6 +183,7 @@ bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
     if ((s = heap_alloc(c, static_cast<size_t>(tmax) * 8, &cflag_off))) return s;
     c->ccnt_off = ccnt_off;
     c->cflag_off = cflag_off;
+    if ((s = heap_alloc(c, static_cast<size_t>(kMaxGrid) * 8, &c->prog_off))) return s;
     c->exch_cap = cap;
     c->slot_off = slot_off;
     c->ready_off = ready_off;
@@ -408,7 +409,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     c->heap_bytes = heap_bytes;
     if (const char *t = getenv("BF_TIMEOUT_MS")) c->timeout_ns = strtoull(t, nullptr, 10) * 1000000ull;
     if (const char *x = getenv("BF_EXCH"))
-        c->exch_kernel = strcmp(x, "pipe") == 0 ? 1 : (strcmp(x, "tile") == 0 ? 0 : 2);
+        c->exch_kernel = strcmp(x, "chunk") == 0 ? 2 : 3;
     if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
     cudaError_t e = cudaMalloc(&c->heap, heap_bytes);
     if (e != cudaSuccess) {
@@ -623,9 +624,16 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     p.slot_parity_stride = c->exch_cap;
     p.ready_off = c->ready_off;
     p.ready_stride = c->ready_stride;
-    p.kernel = c->exch_kernel;
+    // kernel 3 (local-agent fused) is instantiated for k = 1, 2, 4, 8; other k use the chunked kernel
+    p.kernel = c->exch_kernel == 3 && !fused_supported(c->k, c->nprocs) ? 2 : c->exch_kernel;
+    if (p.wmode == kWStatic && c->nprocs > 1) {   // local agents whose x_half another process reads
+        for (int a = 0; a < c->k; ++a) {
+            const int gid = c->proc * c->k + a;
+            for (int j = 0; j < c->n; ++j)
+                if (j / c->k != c->proc && c->W[static_cast<size_t>(j) * c->n + gid] != 0.0) p.pub_mask |= 1u << a;
+        }
+    }
     if (awc_g) {
-        if (p.kernel != 2) return fail(BF_ERR_UNSUPPORTED, "AWC is fused in the chunked exchange kernel only");
         p.awc = 1;
         p.g = awc_g;
         p.g_bf16 = g_kind == 1;
@@ -634,6 +642,7 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     }
     p.chunk_tiles = c->chunk_tiles ? c->chunk_tiles : (c->nprocs > 1 ? 1024 : 256);
     p.ccnt_off = c->ccnt_off;
+    p.prog_off = c->prog_off;
     p.cflag_off = c->cflag_off;
     CU(launch_exchange(p, x_kind, awc_g ? x_kind : g_kind, wire_kind, y_kind, g != nullptr, 0, st));
     c->launches++;

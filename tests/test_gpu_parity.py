@@ -536,3 +536,40 @@ def test_hierarchical_machine_size_change():
         torch.cuda.synchronize()
         assert_parity(_np(y), ora.hier(WM, L, X), np.kron(WM, np.full((L, L), 1.0 / L)), X, 1e-6)
     ctx.close()
+
+
+# ------------------------------------------- exchange kernels x local agents ---
+@pytest.mark.parametrize("kernel", ["fused", "chunk"])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_exchange_kernels_all_ops(kernel, n, monkeypatch):
+    """Every exchange kernel (BF_EXCH) against the oracle for the three fused
+    ops -- neighbor_allreduce (Eq. 5), ATC (Eq. 4-5, 17), AWC (Eq. 16) -- with
+    n virtual agents on one GPU (the fused kernel applies W in registers),
+    over sizes with ragged tails and unaligned rows (count % 4 != 0)."""
+    monkeypatch.setenv("BF_EXCH", kernel)
+    lr = 0.1
+    ctx = _ctx(n)
+    rng = np.random.default_rng(n)
+    W = ora.exp2(n) if n > 1 else np.eye(1)
+    if n > 2:   # a directed random graph with negative weights as well
+        W = W + (rng.random((n, n)) < 0.3) * rng.uniform(-0.5, 0.5, (n, n))
+    ctx.set_topology(W)
+    for count in (1, 7, 1023, 1024, 4097, 70001):
+        x, X = _inputs(n, count)
+        y = ctx.neighbor_allreduce(x)
+        torch.cuda.synchronize()
+        assert_parity(_np(y), ora.mix(W, X), W, X, 1e-6)
+        for wire in (torch.float32, torch.bfloat16):
+            g = _gpu(synthetic.agents_grad(n, count, 5))
+            G = _np(g)
+            xa = x.clone()
+            ctx.atc_step(xa, g, lr, wire=wire)
+            torch.cuda.synchronize()
+            extra = np.abs(W) @ (np.float32(lr) * np.abs(G))
+            assert_parity(_np(xa), ora.atc(W, X, G, lr, wire_bf16=(wire == torch.bfloat16)), W, X,
+                          TOL[wire], extra)
+        xw = x.clone()
+        ctx.awc_step(xw, g, lr)
+        torch.cuda.synchronize()
+        assert_parity(_np(xw), ora.awc(W, X, G, lr), W, X, 1e-6, np.float32(lr) * np.abs(G))
+    ctx.close()

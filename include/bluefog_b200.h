@@ -213,6 +213,17 @@ bf_status bf_fill_uniform(void *dst, bf_dtype dtype, size_t count, uint64_t seed
 /* Number of kernels the library launched so far on this context (bench accounting). */
 uint64_t bf_kernel_launches(const bf_ctx *ctx);
 
+/* Diagnostics (not part of the paper's API).  With the environment variable
+ * BF_STATS=1 at bf_init and a library built with -DBF_STATS=1, the fused
+ * exchange kernel accumulates per-CTA timings into a device buffer of
+ * 4096 x 8 u64: [0] kernel ns, [1] consumer ns waiting for remote tiles,
+ * [2] communication-warp ns blocked on peers' progress, [3] ns blocked on ring
+ * slots, [4] release-fence ns, [5] fences, [6] progress polls, [7] prologue ns.
+ * Copies min(cap, 4096 * 8) values to the host buffer `out` (synchronises the
+ * device) and zeroes the buffer if `reset`.  BF_ERR_STATE if BF_STATS was not
+ * set at bf_init; BF_ERR_ARG on null arguments. */
+bf_status bf_exchange_stats(bf_ctx *ctx, uint64_t *out, size_t cap, int reset);
+
 #ifdef __cplusplus
 }
 #endif

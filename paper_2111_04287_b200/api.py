@@ -315,6 +315,13 @@ class Context:
     def poll_error(self):
         check(self.lib.bf_poll_error(self.h))
 
+    def exchange_stats(self, reset: bool = True) -> np.ndarray:
+        """Per-CTA diagnostics of the fused exchange kernel, shape (4096, 8)
+        (BF_STATS=1 and a -DBF_STATS=1 build; see include/bluefog_b200.h)."""
+        buf = (C.c_uint64 * (4096 * 8))()
+        check(self.lib.bf_exchange_stats(self.h, buf, 4096 * 8, int(reset)))
+        return np.frombuffer(buf, dtype=np.uint64).reshape(4096, 8).copy()
+
     def kernel_launches(self) -> int:
         return int(self.lib.bf_kernel_launches(self.h))
 

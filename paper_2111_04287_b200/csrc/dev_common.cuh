@@ -157,6 +157,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive_release(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_acquire(unsigned long long *bar, unsigned phase) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -263,6 +277,22 @@ __device__ __forceinline__ bool mbar_wait_b(const Geometry &g, unsigned long lon
     const unsigned long long t0 = globaltimer();
     while (true) {
         if (mbar_try(bar, phase)) return true;
+        if (*fail) return false;
+        if (globaltimer() - t0 > g.timeout_ns) {
+            *fail = 1;
+            abort_all(g, BF_ERR_TIMEOUT);
+            return false;
+        }
+    }
+}
+
+// bounded wait with explicit acquire semantics (pairs with mbar_arrive_release)
+__device__ __forceinline__ bool mbar_wait_acq_b(const Geometry &g, unsigned long long *bar, unsigned phase,
+                                                volatile int *fail) {
+    if (mbar_try_acquire(bar, phase)) return true;
+    const unsigned long long t0 = globaltimer();
+    while (true) {
+        if (mbar_try_acquire(bar, phase)) return true;
         if (*fail) return false;
         if (globaltimer() - t0 > g.timeout_ns) {
             *fail = 1;

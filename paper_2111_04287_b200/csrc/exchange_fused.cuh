@@ -23,16 +23,17 @@ namespace bf {
 //     releases a progress counter prog[b] = e * 2^24 + (sub-items published)
 //     every kBatch sub-items -- no chunk barrier over all CTAs of both GPUs,
 //     so a slow CTA delays only its peer;
-//   * one communication warp per CTA (lane 0, an event loop that never blocks)
-//     does all cross-GPU work off the consumers' path: it turns the consumers'
-//     "batch published" mbarrier arrivals into system-scope releases of prog[b]
-//     (the fence.acq_rel.sys costs microseconds -- measured: releasing every 2
-//     sub-items from a consumer thread made an HBM-bound round 1.45x slower),
-//     and it pulls the remote sources' tiles over NVLink with TMA bulk copies
-//     (cp.async.bulk, peer addresses of the CUDA-IPC mappings) into a ring of
-//     NSLOT shared-memory slots, up to NSLOT tiles ahead of the consumers, so
-//     the NVLink latency (calibrated 2.7 us one way) never stalls the HBM
-//     stream of the local agents.
+//   * two warps per CTA do all cross-GPU work off the consumers' path:
+//     - a signal warp turns the consumers' "batch published" mbarrier arrivals
+//       into system-scope releases of prog[b].  The fence.acq_rel.sys drains
+//       the SM's outstanding stores: BF_STATS measured 8-36 us per fence under
+//       load, so no warp that moves data may execute it;
+//     - a producer warp (lane 0, a non-blocking poll loop) pulls the remote
+//       sources' tiles over NVLink with TMA bulk copies (cp.async.bulk, peer
+//       addresses of the CUDA-IPC mappings) into a ring of NSLOT shared-memory
+//       slots, up to NSLOT tiles ahead of the consumers, so the NVLink latency
+//       (calibrated 2.7 us one way) never stalls the HBM stream of the local
+//       agents.
 // HBM traffic per agent-element drops from x + g + publish + x (16 B fp32) to
 // x + g + x (12 B) for every agent without remote readers -- at N = 1 that is
 // every agent.
@@ -45,6 +46,18 @@ namespace bf {
 // Deadlock freedom: consumers publish sub-item m + kLead before they consume
 // sub-item m; the communication warp never blocks (it polls), so releases
 // always follow publication; every wait is bounded by the context timeout.
+// BF_STATS=1 (a diagnostic build, never the default library) records per-CTA
+// timings into ExchParams::stats[blockIdx.x * 8 + i]: 0 kernel ns, 1 consumer
+// ns waiting for remote tiles, 2 comm ns blocked on peers' progress, 3 comm ns
+// blocked on ring slots, 4 fence ns, 5 fences, 6 progress polls, 7 prologue ns.
+#ifndef BF_STATS
+#define BF_STATS 0
+#endif
+#if BF_STATS
+#define BF_STAT(expr) expr
+#else
+#define BF_STAT(expr)
+#endif
 constexpr int kSub = kThreads * kVec;      // elements per sub-item: one vector per consumer thread
 constexpr int kNSlot = 16;                 // remote-tile ring slots per CTA
 #ifndef BF_LEAD
@@ -65,7 +78,7 @@ constexpr int kPubRing = 16;               // "batch published" mbarriers (ring)
 template <int K>
 struct FusedCfg {
     static constexpr bool kRing = K < 8;
-    static constexpr int kThreadsPerCta = kThreads + (kRing ? 32 : 0);   // 8 consumer warps (+ producer)
+    static constexpr int kThreadsPerCta = kThreads + (kRing ? 64 : 0);   // 8 consumer warps (+ producer, signal)
     static constexpr int kUnroll = K <= 2 ? 2 : 1;
 };
 
@@ -80,7 +93,7 @@ struct LocalMix {
 };
 
 template <typename XT, typename GT, typename WT, typename YT, int MODE, int K>
-__global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
+__global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     exchange_fused_kernel(const __grid_constant__ ExchParams p) {
     constexpr bool HAS_G = MODE != 0;
     constexpr int U = FusedCfg<K>::kUnroll;
@@ -95,6 +108,8 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
     const Geometry &g = p.geo;
     Pad *pad = pad_of(g, g.me);
     if (aborted(g)) return;
+    BF_STAT(const unsigned long long t_k0 = globaltimer();)
+    BF_STAT(unsigned long long *const stat = p.stats ? p.stats + blockIdx.x * 8 : nullptr;)
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
     const int parity = static_cast<int>(e & 1);
     const bool sys = g.nprocs > 1;
@@ -105,7 +120,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], kThreads / 32);
         }
-        for (int i = 0; i < kPubRing; ++i) mbar_init(&pubbar[i], kThreads / 32);
+        for (int i = 0; i < kPubRing; ++i) mbar_init(&pubbar[i], kThreads);   // every consumer thread arrives
         fence_mbar_init();
     }
     bool ok = war_wait(g, e);
@@ -155,6 +170,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
         lm.pub = pub;
     }
     __syncthreads();
+    BF_STAT(if (stat && threadIdx.x == 0) stat[7] = globaltimer() - t_k0;)
 
     const bool vec = g.vec_ok != 0;
     const long long count = g.count;
@@ -169,36 +185,43 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
     auto sub = [&](int m) { return static_cast<int>(blockIdx.x) + m * G; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    if (warp == kThreads / 32) {
-        // ============ communication warp (lane 0): releases + TMA pulls ============
+    if (warp == kThreads / 32 + 1) {
+        // ================ signal warp (lane 0): system-scope releases ================
         const int nbatch = lm.pub ? (nmine + kBatch - 1) / kBatch : 0;
-        if (FusedCfg<K>::kRing && lane == 0 && (nrt > 0 || nbatch > 0)) {
+        if (FusedCfg<K>::kRing && lane == 0 && nbatch > 0) {
             unsigned long long *prog = at<unsigned long long>(g.peer_base[g.me], p.prog_off) + blockIdx.x;
             volatile int *released = &s_released;
+            for (int rb = 0; rb < nbatch; ++rb) {
+                if (!mbar_wait_acq_b(g, &pubbar[rb % kPubRing], static_cast<unsigned>(rb / kPubRing) & 1u, fail)) break;
+                const int done = min((rb + 1) * kBatch, nmine);
+                BF_STAT(const unsigned long long tf = globaltimer();)
+                fence_acq_rel(true);   // the consumers' slot stores, visible system-wide ...
+                BF_STAT(if (stat) { stat[4] += globaltimer() - tf; stat[5] += 1; })
+                st_relaxed(prog, (e << kProgShift) | static_cast<unsigned long long>(done), true);   // ... first
+                *released = rb + 1;
+            }
+        }
+    } else if (warp == kThreads / 32) {
+        // ============ producer warp (lane 0): TMA pulls of the remote tiles ============
+        if (FusedCfg<K>::kRing && lane == 0 && nrt > 0) {
             long long issued = 0;              // ring entries issued
             const long long total = static_cast<long long>(nmine) * nrt;
             unsigned long long seen[kMaxP];    // last acquired progress of each source process
             for (int q = 0; q < kMaxP; ++q) seen[q] = 0;
-            int rb = 0;                        // batches released
             unsigned long long t_idle = globaltimer();
+            BF_STAT(unsigned long long t_mark = t_idle;)
             unsigned it = 0;
-            while ((rb < nbatch || issued < total) && !*fail) {
+            while (issued < total && !*fail) {
                 bool progressed = false;
-                // (1) release every batch the consumers have published
-                while (rb < nbatch && mbar_test(&pubbar[rb % kPubRing], static_cast<unsigned>(rb / kPubRing) & 1u)) {
-                    const int done = min((rb + 1) * kBatch, nmine);
-                    fence_acq_rel(true);   // the consumers' slot stores, visible system-wide ...
-                    st_relaxed(prog, (e << kProgShift) | static_cast<unsigned long long>(done), true);   // ... first
-                    ++rb;
-                    *released = rb;
-                    progressed = true;
-                }
-                // (2) pull the remote tiles of the next sub-items while ring slots are free
+                // pull the remote tiles of the next sub-items while ring slots are free
+                BF_STAT(int why = 0;)   // 1: blocked on a ring slot, 2: blocked on a peer's progress
                 while (issued < total) {
                     const int m = static_cast<int>(issued / nrt), i = static_cast<int>(issued % nrt);
                     const int sl = static_cast<int>(issued % kNSlot);
-                    if (issued >= kNSlot && !mbar_test(&empty[sl], static_cast<unsigned>(issued / kNSlot - 1) & 1u))
+                    if (issued >= kNSlot && !mbar_test(&empty[sl], static_cast<unsigned>(issued / kNSlot - 1) & 1u)) {
+                        BF_STAT(why = 1;)
                         break;   // slot still being read
+                    }
                     if (i == 0) {   // a new sub-item: every source process must have published it
                         const unsigned long long need = (e << kProgShift) | static_cast<unsigned long long>(m + 1);
                         bool ready = true, acquired = false;
@@ -207,9 +230,13 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
                             seen[q] = ld_acquire_sys(at<unsigned long long>(g.peer_base[q], p.prog_off) + blockIdx.x);
                             ready = seen[q] >= need;
                             acquired = true;
+                            BF_STAT(if (stat) stat[6] += 1;)
                         }
                         if (acquired) fence_proxy_async_global();   // acquire before the async-proxy reads
-                        if (!ready) break;
+                        if (!ready) {
+                            BF_STAT(why = 2;)
+                            break;
+                        }
                     }
                     const long long base = static_cast<long long>(sub(m)) * kSub;
                     const long long left = count - base;
@@ -220,6 +247,9 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
                     ++issued;
                     progressed = true;
                 }
+                BF_STAT(const unsigned long long now = globaltimer();
+                        if (stat && !progressed && why) stat[why == 1 ? 3 : 2] += now - t_mark;
+                        t_mark = now;)
                 if (progressed) {
                     t_idle = globaltimer();
                 } else {   // nothing to do right now: bounded idle
@@ -249,15 +279,15 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
         auto xrow = [&](int a) { return static_cast<const XT *>(p.x) + static_cast<long long>(a) * count; };
         auto grow = [&](int a) { return static_cast<const GT *>(p.g) + static_cast<long long>(a) * count; };
         unsigned long long *prog = at<unsigned long long>(g.peer_base[g.me], p.prog_off) + blockIdx.x;
-        // batch b published: each warp arrives (release.cta) once its slot stores are issued;
-        // the communication warp turns the completed phase into the system-scope release
+        // batch b published: every consumer thread arrives with release semantics after its
+        // own slot stores; the signal warp acquires the completed phase and turns it into the
+        // system-scope release (fence.acq_rel.sys is cumulative over what it acquired)
         auto batch_done = [&](int b) {
             if (b >= kPubRing) {   // the ring slot's previous phase must have been released
                 volatile int *released = &s_released;
                 while (*released <= b - kPubRing && !*fail) __nanosleep(64);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pubbar[b % kPubRing]);
+            mbar_arrive_release(&pubbar[b % kPubRing]);
         };
         if (sys && pub == 0 && threadIdx.x == 0)   // nothing of this process is read remotely
             st_relaxed(prog, (e << kProgShift) | static_cast<unsigned long long>(nmine), true);
@@ -295,9 +325,9 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
             // every local load of the group is issued before the first use
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                if (u >= nu) break;
+                // a slot of the group past the end (u >= nu) runs with valid = 0: no memory access
                 const long long base = static_cast<long long>(sub(mc + u)) * kSub;
-                const int valid = clamp_valid(count - base, e0);
+                const int valid = u < nu ? clamp_valid(count - base, e0) : 0;
 #pragma unroll
                 for (int a = 0; a < K; ++a)
                     Vec4<XT>::load_hint(xrow(a) + base + e0, xv[u][a], valid, vec, pol_stream);
@@ -307,9 +337,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
                         Vec4<GT>::load_hint(grow(a) + base + e0, gv[u][a], valid, vec, pol_stream);
                 }
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (u >= nu) break;
+            for (int u = 0; u < nu; ++u) {
                 const long long base = static_cast<long long>(sub(mc + u)) * kSub;
                 const int valid = clamp_valid(count - base, e0);
                 if constexpr (MODE == 1) {
@@ -337,7 +365,9 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
                         for (int i = lm.rbeg[a]; i < lm.rbeg[a + 1]; ++i) {   // remote sources from the TMA ring
                             const long long idx = consumed + i;
                             const int sl = static_cast<int>(idx % kNSlot);
+                            BF_STAT(const unsigned long long tw = globaltimer();)
                             mbar_wait_b(g, &full[sl], static_cast<unsigned>(idx / kNSlot) & 1u, fail);
+                            BF_STAT(if (stat && threadIdx.x == 0) stat[1] += globaltimer() - tw;)
                             float v[4];
                             Vec4<WT>::load(reinterpret_cast<const WT *>(ring + sl * kSlotBytes) + e0, v, valid, true);
                             __syncwarp();
@@ -364,6 +394,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 4 ? 2 : 3))
         }
     }
     __syncthreads();
+    BF_STAT(if (stat && threadIdx.x == 0) stat[0] = globaltimer() - t_k0;)
     if (*fail) return;   // nothing is in flight any more; the fault is latched
     last_cta(pad, [&] {
         pad->epoch = e;

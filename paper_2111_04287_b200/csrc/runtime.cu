@@ -103,6 +103,10 @@ struct bf_ctx {
     std::map<std::string, Window> windows;
     unsigned long long bar_epoch = 0;
     unsigned long long launches = 0;
+    unsigned long long *stats = nullptr;      // BF_STATS=1: per-CTA diagnostics of the fused kernel
+    void *scratch = nullptr;                  // fused kernel, bf16 outputs across GPUs: fp32 partial sums
+    size_t scratch_bytes = 0;
+    int lag = 0;                              // BF_FUSED_LAG (0 = automatic)
 };
 
 bf_status bf_barrier_internal(bf_ctx *c);
@@ -411,6 +415,10 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     if (const char *x = getenv("BF_EXCH"))
         c->exch_kernel = strcmp(x, "chunk") == 0 ? 2 : 3;
     if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
+    if (const char *x = getenv("BF_FUSED_LAG")) c->lag = std::max(0, atoi(x));
+    if (const char *x = getenv("BF_STATS"))
+        if (atoi(x) && cudaMalloc(&c->stats, static_cast<size_t>(kMaxGrid) * 8 * 8) == cudaSuccess)
+            cudaMemset(c->stats, 0, static_cast<size_t>(kMaxGrid) * 8 * 8);
     cudaError_t e = cudaMalloc(&c->heap, heap_bytes);
     if (e != cudaSuccess) {
         delete c;
@@ -485,6 +493,8 @@ bf_status bf_finalize(bf_ctx *c) {
     if (c->heap) cudaFree(c->heap);
     if (c->stage_x) cudaFree(c->stage_x);
     if (c->stage_g) cudaFree(c->stage_g);
+    if (c->stats) cudaFree(c->stats);
+    if (c->scratch) cudaFree(c->scratch);
     if (c->h_err) cudaFreeHost(const_cast<unsigned int *>(c->h_err));
     delete c;
     return BF_OK;
@@ -494,6 +504,16 @@ int bf_size(const bf_ctx *c) { return c ? c->n : 0; }
 int bf_rank(const bf_ctx *c) { return c ? c->proc * c->k : -1; }
 int bf_local_agents(const bf_ctx *c) { return c ? c->k : 0; }
 uint64_t bf_kernel_launches(const bf_ctx *c) { return c ? c->launches : 0; }
+
+bf_status bf_exchange_stats(bf_ctx *c, uint64_t *out, size_t cap, int reset) {
+    if (!c || !out) return fail(BF_ERR_ARG, "null argument");
+    if (!c->stats) return fail(BF_ERR_STATE, "context was not created with BF_STATS=1");
+    const size_t n = std::min(cap, static_cast<size_t>(kMaxGrid) * 8);
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(out, c->stats, n * 8, cudaMemcpyDeviceToHost));
+    if (reset) CU(cudaMemset(c->stats, 0, static_cast<size_t>(kMaxGrid) * 8 * 8));
+    return BF_OK;
+}
 
 // ---- topology ------------------------------------------------------------------
 bf_status bf_topology_matrix(int kind, int n, uint64_t k, double *W) {
@@ -643,6 +663,13 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     p.chunk_tiles = c->chunk_tiles ? c->chunk_tiles : (c->nprocs > 1 ? 1024 : 256);
     p.ccnt_off = c->ccnt_off;
     p.prog_off = c->prog_off;
+    p.stats = c->stats;
+    p.lag = c->lag;
+    if (p.kernel == 3 && c->nprocs > 1 && y_kind != 0) {   // fp32 partial sums of a bf16 output
+        s = ensure_stage(&c->scratch, &c->scratch_bytes, static_cast<size_t>(c->k) * count * 4);
+        if (s) return s;
+        p.scratch = static_cast<float *>(c->scratch);
+    }
     p.cflag_off = c->cflag_off;
     CU(launch_exchange(p, x_kind, awc_g ? x_kind : g_kind, wire_kind, y_kind, g != nullptr, 0, st));
     c->launches++;

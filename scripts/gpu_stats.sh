@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+export BF_TIMEOUT_MS=5000
+N=$(nvidia-smi -L | wc -l)
+for topo in one_peer exp2; do
+BF_STATS=1 BF_LIB_PATH=variants/lib_stats.so timeout 120 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr 127.0.0.1 --master-port 29519 scripts/stats_probe.py $topo 2>&1 | grep -E "^rank|Error|error" | sort | head -30
+done

@@ -132,6 +132,61 @@ __global__ void pingpong(volatile unsigned long long *my_flag, unsigned long lon
     }
 }
 
+// Fence cost under load: warps 0..7 stream (local HBM copy, or pull from a peer
+// when `peer` != nullptr); warp 8 lane 0 times `iters` fences of kind `kind`
+// (0 fence.acq_rel.sys, 1 fence.acq_rel.gpu, 2 st.release.sys of a flag, 3 none).
+// Streaming warps with self_fence != 0 fence (same kind) after every 16 vectors
+// and record their own fence time in out[2].
+__global__ void __launch_bounds__(288) fence_cost(const float4 *src, float4 *dst, size_t n, int kind, int iters,
+                                                  unsigned long long *out, unsigned long long *flag, int self_fence) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ volatile int stop;
+    if (threadIdx.x == 0) stop = 0;
+    __syncthreads();
+    auto fence = [&](int k) {
+        if (k == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else if (k == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        else if (k == 2) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag + blockIdx.x), "l"(1ull) : "memory");
+    };
+    if (warp == 8) {
+        if (lane == 0) {
+            unsigned long long tot = 0;
+            for (int i = 0; i < iters; ++i) {
+                unsigned long long t0, t1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                fence(kind);
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                tot += t1 - t0;
+                __nanosleep(2000);
+            }
+            atomicAdd(&out[0], tot);
+            atomicAdd(&out[1], (unsigned long long)iters);
+            stop = 1;
+        }
+        return;
+    }
+    const size_t stride = static_cast<size_t>(gridDim.x) * 256;
+    size_t i = static_cast<size_t>(blockIdx.x) * 256 + threadIdx.x;
+    unsigned long long ft = 0, fc = 0;
+    int cnt = 0;
+    while (!stop) {
+        for (int r = 0; r < 16 && i < n; ++r, i += stride) dst[i] = __ldcg(src + i);
+        if (i >= n) i = static_cast<size_t>(blockIdx.x) * 256 + threadIdx.x;
+        if (self_fence && ++cnt % 1 == 0) {
+            unsigned long long t0, t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            fence(kind);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            ft += t1 - t0;
+            ++fc;
+        }
+    }
+    if (self_fence && lane == 0) {
+        atomicAdd(&out[2], ft);
+        atomicAdd(&out[3], fc);
+    }
+}
+
 static int g_sms = 148;
 
 struct Timer {
@@ -278,6 +333,28 @@ int main(int argc, char **argv) {
         ms = time_on(1, d0, [&](int) { tma_copy<4, 32768><<<grid, 32, 4 * 32768>>>(A[0], B[1], bytes); });
         emit("tma_push_1to1_4x32K", 1, grid, 4, ms, gb);
     }
+    // ---- TMA chunk size sweep, both directions busy (the exchange case) ----
+    CK(cudaSetDevice(1));
+    CK(cudaFuncSetAttribute(tma_copy<16, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096));
+    CK(cudaFuncSetAttribute(tma_copy<8, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 8192));
+    CK(cudaFuncSetAttribute(tma_copy<4, 16384>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 16384));
+    CK(cudaSetDevice(0));
+    CK(cudaFuncSetAttribute(tma_copy<16, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096));
+    CK(cudaFuncSetAttribute(tma_copy<8, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 8192));
+    CK(cudaFuncSetAttribute(tma_copy<4, 16384>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 16384));
+    for (int gm : {1, 2}) {
+        const int grid = g_sms * gm;
+        double ms = time_on(2, d01, [&](int d) { tma_copy<16, 4096><<<grid, 32, 16 * 4096>>>(A[1 - d], B[d], bytes); });
+        emit("tma_pull_bidir_16x4K", 2, grid, 16, ms, gb);
+        ms = time_on(2, d01, [&](int d) { tma_copy<8, 8192><<<grid, 32, 8 * 8192>>>(A[1 - d], B[d], bytes); });
+        emit("tma_pull_bidir_8x8K", 2, grid, 8, ms, gb);
+        ms = time_on(2, d01, [&](int d) { tma_copy<4, 16384><<<grid, 32, 4 * 16384>>>(A[1 - d], B[d], bytes); });
+        emit("tma_pull_bidir_4x16K", 2, grid, 4, ms, gb);
+        ms = time_on(2, d01, [&](int d) { tma_copy<4, 32768><<<grid, 32, 4 * 32768>>>(A[1 - d], B[d], bytes); });
+        emit("tma_pull_bidir_4x32K", 2, grid, 4, ms, gb);
+        ms = time_on(1, d0, [&](int) { tma_copy<16, 4096><<<grid, 32, 16 * 4096>>>(A[1], B[0], bytes); });
+        emit("tma_pull_1to1_16x4K", 1, grid, 16, ms, gb);
+    }
     // ---- copy engine ----
     {
         double ms = time_on(1, d0, [&](int) { CK(cudaMemcpyPeerAsync(B[0], 0, A[1], 1, bytes, 0)); });
@@ -314,6 +391,32 @@ int main(int argc, char **argv) {
             double ms = time_on(n, all.data(), [&](int d) { launch_copy_u(4, A[(d + n - 1) % n], B[d], bytes, grid); });
             emit("pull_shift1_per_gpu", n, grid, 4, ms, gb);
         }
+    }
+    // ---- fence cost under load ----
+    {
+        unsigned long long *out;
+        CK(cudaSetDevice(0));
+        CK(cudaMalloc(&out, 64));
+        const char *kn[] = {"fence.acq_rel.sys", "fence.acq_rel.gpu", "st.release.sys", "none"};
+        const char *ld[] = {"idle", "hbm_copy", "nvlink_pull"};
+        for (int load = 0; load < 3; ++load)
+            for (int kind = 0; kind < 3; ++kind)
+                for (int self = 0; self < 2; ++self) {
+                    if (load == 0 && self) continue;
+                    CK(cudaMemset(out, 0, 64));
+                    const float4 *src = reinterpret_cast<const float4 *>(load == 2 ? A[1] : A[0]);
+                    size_t nvec = load == 0 ? 0 : bytes / 16;
+                    fence_cost<<<g_sms * 2, 288>>>(src, reinterpret_cast<float4 *>(B[0]), nvec, kind, 50, out,
+                                                   reinterpret_cast<unsigned long long *>(C[0]), self);
+                    CK(cudaDeviceSynchronize());
+                    unsigned long long h[4];
+                    CK(cudaMemcpy(h, out, 32, cudaMemcpyDeviceToHost));
+                    printf("{\"test\": \"fence_cost\", \"fence\": \"%s\", \"load\": \"%s\", \"streamers_fence\": %d, "
+                           "\"signal_warp_us\": %.3f, \"streamer_us\": %.3f}\n",
+                           kn[kind], ld[load], self, h[1] ? h[0] / 1e3 / h[1] : 0.0, h[3] ? h[2] / 1e3 / h[3] : 0.0);
+                    fflush(stdout);
+                }
+        CK(cudaFree(out));
     }
     // ---- flag round trip (GPU0 <-> GPU1) ----
     {

@@ -351,6 +351,26 @@ struct Vec4<float> {
     }
     // value as it travels on a wire of this dtype
     static __device__ __forceinline__ float wire(float f) { return f; }
+    // two-stage load: the raw 16 bytes first (so a thread can issue all of its
+    // loads before the first use), converted to fp32 afterwards
+    using Raw = float4;
+    static __device__ __forceinline__ void load_raw_fast(const float *p, Raw &r, unsigned long long pol) {
+        r = ld_hint_v4f(p, pol);
+    }
+    static __device__ __forceinline__ void load_raw(const float *p, Raw &r, int valid, bool vec,
+                                                    unsigned long long pol) {
+        if (vec && valid == 4) {
+            r = ld_hint_v4f(p, pol);
+        } else {
+            r.x = valid > 0 ? p[0] : 0.f;
+            r.y = valid > 1 ? p[1] : 0.f;
+            r.z = valid > 2 ? p[2] : 0.f;
+            r.w = valid > 3 ? p[3] : 0.f;
+        }
+    }
+    static __device__ __forceinline__ void unpack(const Raw &r, float v[4]) {
+        v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w;
+    }
 };
 
 __device__ __forceinline__ unsigned short f2bf(float f) {
@@ -412,6 +432,26 @@ struct Vec4<__nv_bfloat16> {
     }
     // value as it travels on a bf16 wire: round to nearest even (R17)
     static __device__ __forceinline__ float wire(float f) { return bf2f(f2bf(f)); }
+    using Raw = uint2;
+    static __device__ __forceinline__ void load_raw_fast(const __nv_bfloat16 *p, Raw &r, unsigned long long pol) {
+        r = ld_hint_v2u(p, pol);
+    }
+    static __device__ __forceinline__ void load_raw(const __nv_bfloat16 *p, Raw &r, int valid, bool vec,
+                                                    unsigned long long pol) {
+        if (vec && valid == 4) {
+            r = ld_hint_v2u(p, pol);
+        } else {
+            const unsigned short *q = reinterpret_cast<const unsigned short *>(p);
+            const unsigned e0 = valid > 0 ? q[0] : 0u, e1 = valid > 1 ? q[1] : 0u;
+            const unsigned e2 = valid > 2 ? q[2] : 0u, e3 = valid > 3 ? q[3] : 0u;
+            r.x = e0 | (e1 << 16);
+            r.y = e2 | (e3 << 16);
+        }
+    }
+    static __device__ __forceinline__ void unpack(const Raw &r, float v[4]) {
+        v[0] = __uint_as_float(r.x << 16); v[1] = __uint_as_float(r.x & 0xFFFF0000u);
+        v[2] = __uint_as_float(r.y << 16); v[3] = __uint_as_float(r.y & 0xFFFF0000u);
+    }
 };
 
 __device__ __forceinline__ void Vec4<float>::store_hint(float *p, const float v[4], int valid, bool vec,

@@ -73,9 +73,9 @@ constexpr int kPubRing = 16;               // "batch published" mbarriers (ring)
 // K = 8 local agents (N = 1 of the 8-agent configs) has no remote sources: no
 // producer warp, and the 128-register budget of 2 x 256 threads per SM holds
 // the 16 vectors in flight per thread without spilling.
-// K <= 2 keep too few loads in flight per thread with one sub-item: they
-// combine U = 2 sub-items per iteration (the loads of both issued first).
-template <int K>
+// K <= 2 keep too few bytes in flight per thread with one sub-item: they
+// combine U = 2 sub-items per iteration (all loads issued first).
+template <int K, int XBYTES = 4>
 struct FusedCfg {
     static constexpr bool kRing = K < 8;
     static constexpr int kThreadsPerCta = kThreads + (kRing ? 64 : 0);   // 8 consumer warps (+ producer, signal)
@@ -96,7 +96,7 @@ template <typename XT, typename GT, typename WT, typename YT, int MODE, int K>
 __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     exchange_fused_kernel(const __grid_constant__ ExchParams p) {
     constexpr bool HAS_G = MODE != 0;
-    constexpr int U = FusedCfg<K>::kUnroll;
+    constexpr int U = FusedCfg<K, sizeof(XT)>::kUnroll;
     constexpr unsigned kSlotBytes = kSub * sizeof(WT);
     extern __shared__ __align__(128) unsigned char ring[];
     __shared__ SharedTab st;
@@ -322,20 +322,49 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
             const int e0 = threadIdx.x * kVec;
             float xv[U][K][4];
             float gv[U][HAS_G ? K : 1][4];
-            // every local load of the group is issued before the first use
+            {
+                // every local load of the group is issued (raw) before the first use
+                typename Vec4<XT>::Raw xr[U][K];
+                typename Vec4<GT>::Raw gr[U][HAS_G ? K : 1];
+                // one branch per group: the common case is a straight line of vector loads
+                bool fast = vec;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                // a slot of the group past the end (u >= nu) runs with valid = 0: no memory access
-                const long long base = static_cast<long long>(sub(mc + u)) * kSub;
-                const int valid = u < nu ? clamp_valid(count - base, e0) : 0;
+                for (int u = 0; u < U; ++u)
+                    fast = fast && u < nu && clamp_valid(count - static_cast<long long>(sub(mc + u)) * kSub, e0) == 4;
+                if (fast) {
 #pragma unroll
-                for (int a = 0; a < K; ++a)
-                    Vec4<XT>::load_hint(xrow(a) + base + e0, xv[u][a], valid, vec, pol_stream);
-                if constexpr (HAS_G) {
+                    for (int u = 0; u < U; ++u) {
+                        const long long base = static_cast<long long>(sub(mc + u)) * kSub + e0;
 #pragma unroll
-                    for (int a = 0; a < K; ++a)
-                        Vec4<GT>::load_hint(grow(a) + base + e0, gv[u][a], valid, vec, pol_stream);
+                        for (int a = 0; a < K; ++a) Vec4<XT>::load_raw_fast(xrow(a) + base, xr[u][a], pol_stream);
+                        if constexpr (HAS_G) {
+#pragma unroll
+                            for (int a = 0; a < K; ++a) Vec4<GT>::load_raw_fast(grow(a) + base, gr[u][a], pol_stream);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        // a slot of the group past the end (u >= nu) runs with valid = 0: no memory access
+                        const long long base = static_cast<long long>(sub(mc + u)) * kSub;
+                        const int valid = u < nu ? clamp_valid(count - base, e0) : 0;
+#pragma unroll
+                        for (int a = 0; a < K; ++a)
+                            Vec4<XT>::load_raw(xrow(a) + base + e0, xr[u][a], valid, false, pol_stream);
+                        if constexpr (HAS_G) {
+#pragma unroll
+                            for (int a = 0; a < K; ++a)
+                                Vec4<GT>::load_raw(grow(a) + base + e0, gr[u][a], valid, false, pol_stream);
+                        }
+                    }
                 }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int a = 0; a < K; ++a) {
+                        Vec4<XT>::unpack(xr[u][a], xv[u][a]);
+                        if constexpr (HAS_G) Vec4<GT>::unpack(gr[u][a], gv[u][a]);
+                    }
             }
             for (int u = 0; u < nu; ++u) {
                 const long long base = static_cast<long long>(sub(mc + u)) * kSub;
@@ -358,7 +387,8 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                         const float c = lm.c[a][b];
                         if (c != 0.f) {
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) acc[i] = fmaf(c, Vec4<WT>::wire(xv[u][b][i]), acc[i]);
+                            for (int i = 0; i < 4; ++i)   // MODE 0: x is already a wire value
+                                acc[i] = fmaf(c, MODE == 0 ? xv[u][b][i] : Vec4<WT>::wire(xv[u][b][i]), acc[i]);
                         }
                     }
                     if constexpr (FusedCfg<K>::kRing) {
@@ -423,6 +453,11 @@ static cudaError_t launch_fused_k(const ExchParams &p, int grid, cudaStream_t s)
     if (grid > kMaxGrid) grid = kMaxGrid;
     if (grid < 1) grid = 1;
     void *args[] = {const_cast<ExchParams *>(&p)};
+    // one process: no CTA of the launch ever waits for another, so a plain launch
+    // (lower launch latency) is enough; across processes CTA b waits for CTA b of
+    // the peers, so every CTA must be resident: cooperative launch
+    if (p.geo.nprocs == 1)
+        return cudaLaunchKernel(fn, dim3(grid), dim3(FusedCfg<K>::kThreadsPerCta), args, smem, s);
     return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FusedCfg<K>::kThreadsPerCta), args, smem, s);
 }
 

@@ -10,6 +10,8 @@
   C5  push-sum through win_accumulate / win_update_then_collect, 340M bf16 per
       agent, one-peer destinations inside the static exp-2 window topology
   H   hierarchical_neighbor_allreduce, 25.6M fp32, L = 2, 4
+  O   ATC optimizer wrapper over ResNet-50's 161 parameter tensors (tensor
+      fusion into buckets, one fused kernel per bucket)
 
 One JSON object per line.  N = 1: the 8 agents are virtual agents of one GPU;
 under torchrun, 8/N agents per GPU.  Every number is CUDA-event time on the
@@ -29,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c3,c5,h,c2")
+    ap.add_argument("--only", default="c1,c3,c5,h,o,c2")
     ap.add_argument("--agents", type=int, default=8)
     ap.add_argument("--max-bytes", type=int, default=1 << 30)
     ap.add_argument("--out", default=None)
@@ -171,9 +173,15 @@ def main():
             ctx.set_machine_topology(bfp.topology_matrix("exp2", nm), L)
             ms = timed(lambda: ctx.hierarchical_neighbor_allreduce(x, out=y), 20)
             dm = 1 if nm == 2 else (2 if nm in (3, 4) else 3)
-            per_agent = (2 * (L - 1) + dm) * count * 4 / L + 3 * count * 4
+            if world == 1:
+                # one GPU: the Kronecker mix W_M (x) J/L in the fused kernel -- read x, write y
+                per_agent, path = 2 * count * 4, "fused kernel, W = W_M (x) J_L/L (read x + write y)"
+            else:
+                per_agent = (2 * (L - 1) + dm) * count * 4 / L + 3 * count * 4
+                path = "staged kernel (sliced reduce-scatter, machine combine, gather)"
             emit({"config": f"H hierarchical_neighbor_allreduce 25.6M fp32, {nm} machines x {L}", "ms": ms,
-                  "gbs_per_gpu": k * per_agent / (ms * 1e-3) / 1e9})
+                  "path": path, "gbs_per_gpu": k * per_agent / (ms * 1e-3) / 1e9,
+                  "hbm_frac": k * per_agent / (ms * 1e-3) / 1e9 / peak if world == 1 else None})
         ctx.close()
 
     # ---------------------------------------------------------------- C5 ----
@@ -212,6 +220,34 @@ def main():
             ctx.close()
         except Exception as ex:  # noqa: BLE001
             emit({"config": "C5", "error": repr(ex)[:300]})
+
+    # ----------------------------------------------------------------- O ----
+    # ATC optimizer over ResNet-50's 161 parameter tensors (tensor fusion into
+    # buckets, one fused kernel per bucket), synthetic gradients (§8(f) rank 3)
+    if "o" in only:
+        import math
+        from paper_2111_04287_b200.optim import DistributedAdaptThenCombineOptimizer, resnet50_param_shapes
+        n = a.agents
+        k = n // world
+        shapes = resnet50_param_shapes()
+        total = sum(math.prod(sh) for sh in shapes)
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=k * 2 * total * 4 + (256 << 20), device=local)
+        ctx.set_dynamic_schedule("one_peer_exp2", 0)
+        for bucket_mb in (4, 25, 128):
+            params = [torch.nn.Parameter(torch.zeros(k, *sh, device="cuda")) for sh in shapes]
+            opt = DistributedAdaptThenCombineOptimizer(ctx, params, 0.1, bucket_bytes=bucket_mb << 20)
+            for bi, bkt in enumerate(opt.buckets):
+                for la in range(k):
+                    bfp.Context.fill_uniform(bkt.x[la], synthetic.SEED_X0 + ctx.rank + la, offset=bi << 28)
+                    bfp.Context.fill_uniform(bkt.g[la], synthetic.grad_seed(0, ctx.rank + la), offset=bi << 28,
+                                             scale=2.0 ** -7)
+            ms = timed(opt.step, 20)
+            emit({"config": f"O ATC optimizer, ResNet-50 parameter list (161 tensors, {total} elements) x "
+                            f"{n} agents, one-peer, {bucket_mb} MB buckets", "buckets": len(opt.buckets),
+                  "ms_per_step": ms, "iters_per_s": 1e3 / ms,
+                  "hbm_gbs": k * 12 * total / (ms * 1e-3) / 1e9 if world == 1 else None})
+            del opt, params
+        ctx.close()
 
     # ---------------------------------------------------------------- C2 ----
     if "c2" in only and world == 1:

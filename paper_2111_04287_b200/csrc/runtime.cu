@@ -107,6 +107,7 @@ struct bf_ctx {
     void *scratch = nullptr;                  // fused kernel, bf16 outputs across GPUs: fp32 partial sums
     size_t scratch_bytes = 0;
     int lag = 0;                              // BF_FUSED_LAG (0 = automatic)
+    bool hier_staged = false;                 // BF_HIER=staged: always the staged hierarchical kernel
 };
 
 bf_status bf_barrier_internal(bf_ctx *c);
@@ -416,6 +417,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
         c->exch_kernel = strcmp(x, "chunk") == 0 ? 2 : 3;
     if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
     if (const char *x = getenv("BF_FUSED_LAG")) c->lag = std::max(0, atoi(x));
+    if (const char *x = getenv("BF_HIER")) c->hier_staged = strcmp(x, "staged") == 0;
     if (const char *x = getenv("BF_STATS"))
         if (atoi(x) && cudaMalloc(&c->stats, static_cast<size_t>(kMaxGrid) * 8 * 8) == cudaSuccess)
             cudaMemset(c->stats, 0, static_cast<size_t>(kMaxGrid) * 8 * 8);
@@ -616,13 +618,20 @@ bf_status bf_reserve(bf_ctx *c, size_t bytes_per_agent) {
 // ---- hot path ---------------------------------------------------------------
 static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *y, void *shadow, size_t count,
                                  int x_kind, int g_kind, int wire_kind, int y_kind, float lr,
-                                 const bf_weights *weights, cudaStream_t st, const void *awc_g = nullptr) {
+                                 const bf_weights *weights, cudaStream_t st, const void *awc_g = nullptr,
+                                 const SrcTab *static_tab = nullptr) {
     if (count == 0) return BF_OK;
     if (count > (1ull << 40)) return fail(BF_ERR_ARG, "count too large");
     ExchParams p;
     memset(&p, 0, sizeof(p));
-    bf_status s = fill_weights(c, weights, p);
-    if (s) return s;
+    bf_status s = BF_OK;
+    if (static_tab) {   // a W assembled by the caller (hierarchical on one GPU)
+        p.wmode = kWStatic;
+        p.tab = *static_tab;
+    } else {
+        s = fill_weights(c, weights, p);
+        if (s) return s;
+    }
     const size_t wire_es = wire_kind == 0 ? 4 : 2;
     s = ensure_exchange(c, count * wire_es);
     if (s) return s;
@@ -741,6 +750,11 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
     const int L = c->machine_L, NM = c->n_machines;
     HierParams p;
     memset(&p, 0, sizeof(p));
+    // One process hosting every agent (N = 1): the hierarchical average is the
+    // plain mix with W = W_M (x) J_L / L (R12), applied in registers by
+    // the fused exchange kernel (read x, write y) instead of the staged kernel.
+    const bool as_mix = c->nprocs == 1 && !c->hier_staged && c->exch_kernel == 3 && fused_supported(c->k, 1) &&
+                        L * NM - 1 <= kMaxS;
     for (int a = 0; a < c->k; ++a) {
         const int gid = c->proc * c->k + a, m = gid / L;
         if (!machine_weights) {
@@ -766,6 +780,29 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
             }
             p.mtab.nsrc[a] = static_cast<unsigned char>(w.n_src > 0 ? w.n_src : 0);
         }
+    }
+    if (as_mix) {
+        SrcTab tab;
+        memset(&tab, 0, sizeof(tab));
+        for (int a = 0; a < c->k; ++a) {
+            const int m = a / L;   // gid == a on one process
+            tab.self_w[a] = p.mtab.self_w[a] / static_cast<float>(L);
+            int cnt = 0;
+            auto add = [&](int mm, float w) {
+                for (int l = 0; l < L; ++l) {
+                    const int j = mm * L + l;
+                    if (j == a) continue;
+                    tab.src[a][cnt] = static_cast<unsigned char>(j);
+                    tab.coef[a][cnt] = w / static_cast<float>(L);
+                    ++cnt;
+                }
+            };
+            add(m, p.mtab.self_w[a]);   // the rest of the own machine
+            for (int q = 0; q < p.mtab.nsrc[a]; ++q) add(p.mtab.src[a][q], p.mtab.coef[a][q]);
+            tab.nsrc[a] = static_cast<unsigned char>(cnt);
+        }
+        return exchange_common(c, x, nullptr, y, nullptr, count, dtype, dtype, dtype, dtype, 0.f, nullptr,
+                               static_cast<cudaStream_t>(stream), nullptr, &tab);
     }
     const size_t es = dtype == BF_FLOAT32 ? 4 : 2;
     s = ensure_exchange(c, count * es);

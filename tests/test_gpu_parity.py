@@ -294,9 +294,13 @@ def test_invalid_configurations_rejected_on_host():
 
 
 # ------------------------------------------------------------- hierarchical ---
+@pytest.mark.parametrize("impl", ["fused", "staged"])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("nm,L", [(4, 2), (2, 4), (1, 8), (8, 1), (2, 2)])
-def test_hierarchical(nm, L, dtype):
+def test_hierarchical(nm, L, dtype, impl, monkeypatch):
+    # one GPU: "fused" = the Kronecker mix W_M (x) J/L in the fused exchange kernel,
+    # "staged" = the leader-free sliced kernel used across GPUs (BF_HIER=staged)
+    monkeypatch.setenv("BF_HIER", impl)
     n = nm * L
     WM = ora.exp2(nm)
     ctx = _ctx(n)
@@ -572,4 +576,44 @@ def test_exchange_kernels_all_ops(kernel, n, monkeypatch):
         ctx.awc_step(xw, g, lr)
         torch.cuda.synchronize()
         assert_parity(_np(xw), ora.awc(W, X, G, lr), W, X, 1e-6, np.float32(lr) * np.abs(G))
+    ctx.close()
+
+
+# ----------------------------------------- optimizer wrapper: tensor fusion + ATC ---
+@pytest.mark.parametrize("overlap", [False, True])
+@pytest.mark.parametrize("awc", [False, True])
+def test_optimizer_bucketed_matches_oracle(overlap, awc):
+    """DistributedAdaptThenCombineOptimizer: parameters re-homed into
+    bucket buffers, one fused call per bucket (from backward hooks when
+    overlap) == the oracle's ATC / AWC (Eq. 17 / Eq. 16) of the concatenated
+    per-agent vectors: bucketing is invisible to the result."""
+    from paper_2111_04287_b200.optim import DistributedAdaptThenCombineOptimizer
+    n, lr = 4, 0.05
+    ctx = _ctx(n)
+    W = ora.exp2(n)
+    ctx.set_topology(W)
+    shapes = [(7, 3), (129,), (64, 65), (5,), (1000,), (33, 17)]
+    torch.manual_seed(0)
+    params = [torch.nn.Parameter(torch.randn(n, *s, device="cuda")) for s in shapes]
+    X = np.concatenate([_np(p.detach().reshape(n, -1)) for p in params], axis=1)
+    opt = DistributedAdaptThenCombineOptimizer(ctx, params, lr, bucket_bytes=4 * 2000, overlap=overlap, awc=awc)
+    assert len(opt.buckets) >= 3
+    # gradients from a real backward: loss = sum_i c_i * sum(p_i^2) / 2  ->  g_i = c_i * p_i
+    coef = [0.1 * (i + 1) for i in range(len(params))]
+    loss = sum(c * (p * p).sum() / 2 for c, p in zip(coef, params))
+    opt.zero_grad()
+    loss.backward()
+    widths = [int(np.prod(sh)) for sh in shapes]
+    G = X * np.concatenate([np.full(w_, np.float32(c)) for c, w_ in zip(coef, widths)])[None, :]
+    # the gradient buffers hold exactly what backward produced
+    Gb = np.concatenate([_np(p.grad.reshape(n, -1)) for p in params], axis=1)
+    assert np.allclose(Gb, G, rtol=1e-6, atol=1e-7)
+    opt.step()
+    torch.cuda.synchronize()
+    Y = np.concatenate([_np(p.detach().reshape(n, -1)) for p in params], axis=1)
+    ref = ora.awc(W, X, Gb, lr) if awc else ora.atc(W, X, Gb, lr)
+    extra = np.float32(lr) * np.abs(Gb) if awc else np.abs(W) @ (np.float32(lr) * np.abs(Gb))
+    assert_parity(Y, ref, W, X, 1e-6, extra)
+    assert opt.steps_launched == len(opt.buckets)
+    opt.remove_hooks()
     ctx.close()

@@ -114,3 +114,23 @@ def test_bootstrap_allgather_gloo_world2():
     for rank, firsts, lens, tmax in res:
         assert firsts == [0, 1] and lens == [size, size]
         assert tmax == 2.5
+
+
+# ------------------------------------------------ optimizer wrapper (host logic) ---
+def test_plan_buckets_reverse_order_no_split():
+    from paper_2111_04287_b200.optim import plan_buckets
+    numels = [5, 3, 8, 2, 20, 1]
+    b = plan_buckets(numels, 10)
+    # reverse registration order (backward produces the last layer first)
+    assert [i for bb in b for i in bb] == list(reversed(range(len(numels))))
+    for bb in b:   # a bucket only exceeds the target when one tensor alone does
+        assert sum(numels[i] for i in bb) <= 10 or len(bb) == 1
+    assert b == [[5], [4], [3, 2], [1, 0]]
+
+
+def test_resnet50_shapes():
+    import math
+    from paper_2111_04287_b200.optim import resnet50_param_shapes
+    s = resnet50_param_shapes()
+    # torchvision ResNet-50: 161 parameter tensors, 25 557 032 parameters (the model of P:892)
+    assert len(s) == 161 and sum(math.prod(x) for x in s) == 25_557_032

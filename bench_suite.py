@@ -208,6 +208,22 @@ def main():
                 ctx.win_update_then_collect("ext")
                 r[0] += 1
             ms = timed(c5, 10)
+            # drain (untimed): every process collects what it was sent, then pushes what its
+            # outboxes still owe and collects again -- only then is sum_i p_i = n exact
+            def sync():
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+            sync()
+            ctx.win_update_then_collect("ext")       # everything already delivered
+            sync()
+            flush = [{j: 0.0 for j in ctx.out_neighbor_ranks(ctx.rank + la)} for la in range(k)]
+            ctx.win_accumulate("ext", self_weight=[1.0] * k, dst_weights=flush)   # owed outboxes only
+            sync()
+            if world > 1:
+                dist.barrier()
+            ctx.win_update_then_collect("ext")
+            torch.cuda.synchronize()
             p = ctx.win_p("ext")
             tot = torch.tensor([float(p.sum())], device="cuda", dtype=torch.float64)
             if world > 1:

@@ -169,6 +169,15 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *ctx, const void *x, void *y
 bf_status bf_win_create(bf_ctx *ctx, const char *name, void *x, size_t count, bf_dtype dtype,
                         int zero_init, int with_p);
 bf_status bf_win_free(bf_ctx *ctx, const char *name);
+/* Error feedback for a bf16 window (reading R24 in DESIGN.md; not in the
+ * paper).  Payloads travel in the window dtype, so a bf16 payload is rounded
+ * (RNE) like BlueFog's MPI window in the tensor dtype; with enable != 0 the
+ * sender keeps the rounding residual in its fp32 outbox and adds it to the next
+ * payload to that destination, so the total mass sum_i x_i + in-flight is
+ * conserved exactly at the cost of 8 B of outbox traffic per element
+ * and round.  Off by default (BF_WIN_EF=1 at bf_init turns it on for new
+ * windows).  Local, not collective; BF_ERR_WINDOW for an unknown name. */
+bf_status bf_win_set_error_feedback(bf_ctx *ctx, const char *name, int enable);
 /* put / accumulate by the local agents selected in agent_mask (bit a = local
  * agent a; 0 = all): for each dst j in weights[a] (self + dst only; dst must
  * be out-neighbours at creation) deliver s_ja * x_a into j's slot for a

@@ -79,6 +79,7 @@ _SIGS = {
     "bf_fill_uniform": (_i, [_vp, _i, _sz, _u64, _u64, C.c_float, _vp]),
     "bf_kernel_launches": (_u64, [_vp]),
     "bf_exchange_stats": (_i, [_vp, C.POINTER(_u64), _sz, _i]),
+    "bf_win_set_error_feedback": (_i, [_vp, C.c_char_p, _i]),
 }
 
 _lib = None

@@ -265,6 +265,11 @@ class Context:
                                      _DT[tensor.dtype], 1 if zero_init else 0, 1 if with_p else 0))
         return True
 
+    def win_set_error_feedback(self, name: str, enable: bool = True) -> bool:
+        """bf16 windows: keep the wire rounding residual in the sender's outbox (R24)."""
+        check(self.lib.bf_win_set_error_feedback(self.h, name.encode(), 1 if enable else 0))
+        return True
+
     def win_free(self, name: str) -> bool:
         torch.cuda.synchronize(self.device)
         check(self.lib.bf_win_free(self.h, name.encode()))

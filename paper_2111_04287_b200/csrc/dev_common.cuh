@@ -472,6 +472,107 @@ __device__ __forceinline__ void Vec4<__nv_bfloat16>::store_hint(__nv_bfloat16 *p
     }
 }
 
+// ---- V-element vectors (16-byte accesses for bf16: V = 8) -------------------
+// VecN<T, 4> is Vec4<T>; VecN<bf16, 8> moves 8 bf16 values with one 16-byte
+// access (the fused kernel uses V = 16 / sizeof(x dtype) elements per thread).
+template <typename T, int V>
+struct VecN;
+
+template <typename T>
+struct VecN<T, 4> {
+    using Raw = typename Vec4<T>::Raw;
+    static __device__ __forceinline__ void load_raw_fast(const T *p, Raw &r, unsigned long long pol) {
+        Vec4<T>::load_raw_fast(p, r, pol);
+    }
+    static __device__ __forceinline__ void load_raw(const T *p, Raw &r, int valid, unsigned long long pol) {
+        Vec4<T>::load_raw(p, r, valid, false, pol);
+    }
+    static __device__ __forceinline__ void unpack(const Raw &r, float v[4]) { Vec4<T>::unpack(r, v); }
+    static __device__ __forceinline__ void load(const T *p, float v[4], int valid, bool vec) {
+        Vec4<T>::load(p, v, valid, vec);
+    }
+    static __device__ __forceinline__ void load_hint(const T *p, float v[4], int valid, bool vec,
+                                                     unsigned long long pol) {
+        Vec4<T>::load_hint(p, v, valid, vec, pol);
+    }
+    static __device__ __forceinline__ void store_hint(T *p, const float v[4], int valid, bool vec,
+                                                      unsigned long long pol) {
+        Vec4<T>::store_hint(p, v, valid, vec, pol);
+    }
+    static __device__ __forceinline__ float wire(float f) { return Vec4<T>::wire(f); }
+};
+
+template <>
+struct VecN<__nv_bfloat16, 8> {
+    using Raw = uint4;
+    static __device__ __forceinline__ void load_raw_fast(const __nv_bfloat16 *p, Raw &r, unsigned long long pol) {
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(p), "l"(pol));
+    }
+    static __device__ __forceinline__ void load_raw(const __nv_bfloat16 *p, Raw &r, int valid,
+                                                    unsigned long long) {
+        const unsigned short *q = reinterpret_cast<const unsigned short *>(p);
+        unsigned e[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) e[i] = i < valid ? q[i] : 0u;
+        r.x = e[0] | (e[1] << 16); r.y = e[2] | (e[3] << 16);
+        r.z = e[4] | (e[5] << 16); r.w = e[6] | (e[7] << 16);
+    }
+    static __device__ __forceinline__ void unpack(const Raw &r, float v[8]) {
+        const unsigned w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            v[2 * i] = __uint_as_float(w[i] << 16);
+            v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+    }
+    static __device__ __forceinline__ void load(const __nv_bfloat16 *p, float v[8], int valid, bool vec) {
+        Raw r;
+        if (vec && valid == 8) {
+            r = *reinterpret_cast<const uint4 *>(p);
+        } else {
+            load_raw(p, r, valid, 0ull);
+        }
+        unpack(r, v);
+    }
+    static __device__ __forceinline__ void load_hint(const __nv_bfloat16 *p, float v[8], int valid, bool vec,
+                                                     unsigned long long pol) {
+        Raw r;
+        if (vec && valid == 8)
+            load_raw_fast(p, r, pol);
+        else
+            load_raw(p, r, valid, pol);
+        unpack(r, v);
+    }
+    static __device__ __forceinline__ void store_hint(__nv_bfloat16 *p, const float v[8], int valid, bool vec,
+                                                      unsigned long long pol) {
+        unsigned short h[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) h[i] = f2bf(v[i]);
+        if (vec && valid == 8) {
+            const unsigned a = h[0] | (static_cast<unsigned>(h[1]) << 16), b = h[2] | (static_cast<unsigned>(h[3]) << 16);
+            const unsigned c = h[4] | (static_cast<unsigned>(h[5]) << 16), d = h[6] | (static_cast<unsigned>(h[7]) << 16);
+            asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b),
+                         "r"(c), "r"(d), "l"(pol)
+                         : "memory");
+        } else {
+            unsigned short *q = reinterpret_cast<unsigned short *>(p);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (i < valid) q[i] = h[i];
+        }
+    }
+    static __device__ __forceinline__ float wire(float f) { return bf2f(f2bf(f)); }
+};
+
+// valid elements of the V-vector at offset e of a row with `rem` elements left
+template <int V>
+__device__ __forceinline__ int clamp_valid_v(long long rem, int e) {
+    long long v = rem - e;
+    return v >= V ? V : (v <= 0 ? 0 : static_cast<int>(v));
+}
+
 // Element index of vector j (0..kVecPerThread-1) of this thread inside a tile:
 // consecutive threads touch consecutive 4-element vectors (coalesced).
 __device__ __forceinline__ int tile_elem(int j) { return (j * kThreads + threadIdx.x) * kVec; }

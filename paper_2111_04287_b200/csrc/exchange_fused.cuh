@@ -58,7 +58,12 @@ namespace bf {
 #else
 #define BF_STAT(expr)
 #endif
-constexpr int kSub = kThreads * kVec;      // elements per sub-item: one vector per consumer thread
+// elements per thread-vector: 16-byte accesses of the x dtype (4 fp32, 8 bf16);
+// a sub-item is one vector per consumer thread (1024 fp32 / 2048 bf16 elements)
+template <typename XT>
+struct FusedVec {
+    static constexpr int V = sizeof(XT) >= 4 ? 4 : 8;
+};
 constexpr int kNSlot = 16;                 // remote-tile ring slots per CTA
 #ifndef BF_LEAD
 #define BF_LEAD 24
@@ -97,7 +102,9 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     exchange_fused_kernel(const __grid_constant__ ExchParams p) {
     constexpr bool HAS_G = MODE != 0;
     constexpr int U = FusedCfg<K, sizeof(XT)>::kUnroll;
-    constexpr unsigned kSlotBytes = kSub * sizeof(WT);
+    constexpr int V = FusedVec<XT>::V;         // elements per thread-vector (16-byte x accesses)
+    constexpr int kSubT = kThreads * V;        // elements per sub-item
+    constexpr unsigned kSlotBytes = kSubT * sizeof(WT);
     extern __shared__ __align__(128) unsigned char ring[];
     __shared__ SharedTab st;
     __shared__ LocalMix<K> lm;
@@ -175,7 +182,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     const bool vec = g.vec_ok != 0;
     const long long count = g.count;
     const int G = gridDim.x;
-    const int S = static_cast<int>((count + kSub - 1) / kSub);
+    const int S = static_cast<int>((count + kSubT - 1) / kSubT);
     const int nmine = static_cast<int>(blockIdx.x) < S ? (S - static_cast<int>(blockIdx.x) + G - 1) / G : 0;
     const int nrt = lm.rbeg[K];   // remote tiles per sub-item
     auto slot_of = [&](int agent) {
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                 const int done = min((rb + 1) * kBatch, nmine);
                 BF_STAT(const unsigned long long tf = globaltimer();)
                 fence_acq_rel(true);   // the consumers' slot stores, visible system-wide ...
-                BF_STAT(if (stat) { stat[4] += globaltimer() - tf; stat[5] += 1; })
+                BF_STAT(if (stat) { stat[V] += globaltimer() - tf; stat[5] += 1; })
                 st_relaxed(prog, (e << kProgShift) | static_cast<unsigned long long>(done), true);   // ... first
                 *released = rb + 1;
             }
@@ -238,10 +245,10 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                             break;
                         }
                     }
-                    const long long base = static_cast<long long>(sub(m)) * kSub;
+                    const long long base = static_cast<long long>(sub(m)) * kSubT;
                     const long long left = count - base;
                     const unsigned bytes =
-                        (static_cast<unsigned>((left < kSub ? left : kSub) * sizeof(WT)) + 15u) & ~15u;
+                        (static_cast<unsigned>((left < kSubT ? left : kSubT) * sizeof(WT)) + 15u) & ~15u;
                     mbar_expect_tx(&full[sl], bytes);
                     tma_load_1d(ring + sl * kSlotBytes, slot_of(lm.rs[i]) + base, bytes, &full[sl]);
                     ++issued;
@@ -297,21 +304,21 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
         while (mc < nmine) {
             if (FusedCfg<K>::kRing && pub && mp < nmine && mp <= mc + kLead) {
                 // ---- publish sub-item mp for the agents with remote readers ----
-                const long long base = static_cast<long long>(sub(mp)) * kSub;
-                const int e0 = threadIdx.x * kVec;
-                const int valid = clamp_valid(count - base, e0);
+                const long long base = static_cast<long long>(sub(mp)) * kSubT;
+                const int e0 = threadIdx.x * V;
+                const int valid = clamp_valid_v<V>(count - base, e0);
 #pragma unroll
                 for (int a = 0; a < K; ++a) {
                     if (!((pub >> a) & 1u)) continue;
-                    float v[4];
-                    Vec4<XT>::load_hint(xrow(a) + base + e0, v, valid, vec, pol_keep);
+                    float v[V];
+                    VecN<XT, V>::load_hint(xrow(a) + base + e0, v, valid, vec, pol_keep);
                     if constexpr (MODE == 1) {
-                        float gv[4];
-                        Vec4<GT>::load_hint(grow(a) + base + e0, gv, valid, vec, pol_keep);
+                        float gv[V];
+                        VecN<GT, V>::load_hint(grow(a) + base + e0, gv, valid, vec, pol_keep);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) v[i] = fmaf(-p.lr, gv[i], v[i]);
+                        for (int i = 0; i < V; ++i) v[i] = fmaf(-p.lr, gv[i], v[i]);
                     }
-                    Vec4<WT>::store_hint(slot_of(g.me * K + a) + base + e0, v, valid, true, pol_keep);
+                    VecN<WT, V>::store_hint(slot_of(g.me * K + a) + base + e0, v, valid, true, pol_keep);
                 }
                 ++mp;
                 if (mp % kBatch == 0 || mp == nmine) batch_done((mp - 1) / kBatch);
@@ -319,42 +326,42 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
             }
             // ---- combine sub-items mc .. mc + U - 1 ----
             const int nu = min(U, nmine - mc);
-            const int e0 = threadIdx.x * kVec;
-            float xv[U][K][4];
-            float gv[U][HAS_G ? K : 1][4];
+            const int e0 = threadIdx.x * V;
+            float xv[U][K][V];
+            float gv[U][HAS_G ? K : 1][V];
             {
                 // every local load of the group is issued (raw) before the first use
-                typename Vec4<XT>::Raw xr[U][K];
-                typename Vec4<GT>::Raw gr[U][HAS_G ? K : 1];
+                typename VecN<XT, V>::Raw xr[U][K];
+                typename VecN<GT, V>::Raw gr[U][HAS_G ? K : 1];
                 // one branch per group: the common case is a straight line of vector loads
                 bool fast = vec;
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    fast = fast && u < nu && clamp_valid(count - static_cast<long long>(sub(mc + u)) * kSub, e0) == 4;
+                    fast = fast && u < nu && clamp_valid_v<V>(count - static_cast<long long>(sub(mc + u)) * kSubT, e0) == V;
                 if (fast) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        const long long base = static_cast<long long>(sub(mc + u)) * kSub + e0;
+                        const long long base = static_cast<long long>(sub(mc + u)) * kSubT + e0;
 #pragma unroll
-                        for (int a = 0; a < K; ++a) Vec4<XT>::load_raw_fast(xrow(a) + base, xr[u][a], pol_stream);
+                        for (int a = 0; a < K; ++a) VecN<XT, V>::load_raw_fast(xrow(a) + base, xr[u][a], pol_stream);
                         if constexpr (HAS_G) {
 #pragma unroll
-                            for (int a = 0; a < K; ++a) Vec4<GT>::load_raw_fast(grow(a) + base, gr[u][a], pol_stream);
+                            for (int a = 0; a < K; ++a) VecN<GT, V>::load_raw_fast(grow(a) + base, gr[u][a], pol_stream);
                         }
                     }
                 } else {
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         // a slot of the group past the end (u >= nu) runs with valid = 0: no memory access
-                        const long long base = static_cast<long long>(sub(mc + u)) * kSub;
-                        const int valid = u < nu ? clamp_valid(count - base, e0) : 0;
+                        const long long base = static_cast<long long>(sub(mc + u)) * kSubT;
+                        const int valid = u < nu ? clamp_valid_v<V>(count - base, e0) : 0;
 #pragma unroll
                         for (int a = 0; a < K; ++a)
-                            Vec4<XT>::load_raw(xrow(a) + base + e0, xr[u][a], valid, false, pol_stream);
+                            VecN<XT, V>::load_raw(xrow(a) + base + e0, xr[u][a], valid, pol_stream);
                         if constexpr (HAS_G) {
 #pragma unroll
                             for (int a = 0; a < K; ++a)
-                                Vec4<GT>::load_raw(grow(a) + base + e0, gr[u][a], valid, false, pol_stream);
+                                VecN<GT, V>::load_raw(grow(a) + base + e0, gr[u][a], valid, pol_stream);
                         }
                     }
                 }
@@ -362,33 +369,33 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                 for (int u = 0; u < U; ++u)
 #pragma unroll
                     for (int a = 0; a < K; ++a) {
-                        Vec4<XT>::unpack(xr[u][a], xv[u][a]);
-                        if constexpr (HAS_G) Vec4<GT>::unpack(gr[u][a], gv[u][a]);
+                        VecN<XT, V>::unpack(xr[u][a], xv[u][a]);
+                        if constexpr (HAS_G) VecN<GT, V>::unpack(gr[u][a], gv[u][a]);
                     }
             }
             for (int u = 0; u < nu; ++u) {
-                const long long base = static_cast<long long>(sub(mc + u)) * kSub;
-                const int valid = clamp_valid(count - base, e0);
+                const long long base = static_cast<long long>(sub(mc + u)) * kSubT;
+                const int valid = clamp_valid_v<V>(count - base, e0);
                 if constexpr (MODE == 1) {
 #pragma unroll
                     for (int a = 0; a < K; ++a)
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) xv[u][a][i] = fmaf(-p.lr, gv[u][a][i], xv[u][a][i]);   // Eq. 4
+                        for (int i = 0; i < V; ++i) xv[u][a][i] = fmaf(-p.lr, gv[u][a][i], xv[u][a][i]);   // Eq. 4
                 }
 #pragma unroll
                 for (int a = 0; a < K; ++a) {
-                    float acc[4];
+                    float acc[V];
                     const float cs = lm.c[a][a];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[i] = cs * xv[u][a][i];
+                    for (int i = 0; i < V; ++i) acc[i] = cs * xv[u][a][i];
 #pragma unroll
                     for (int d = 1; d < K; ++d) {
                         const int b = (a + K - d) % K;
                         const float c = lm.c[a][b];
                         if (c != 0.f) {
 #pragma unroll
-                            for (int i = 0; i < 4; ++i)   // MODE 0: x is already a wire value
-                                acc[i] = fmaf(c, MODE == 0 ? xv[u][b][i] : Vec4<WT>::wire(xv[u][b][i]), acc[i]);
+                            for (int i = 0; i < V; ++i)   // MODE 0: x is already a wire value
+                                acc[i] = fmaf(c, MODE == 0 ? xv[u][b][i] : VecN<WT, V>::wire(xv[u][b][i]), acc[i]);
                         }
                     }
                     if constexpr (FusedCfg<K>::kRing) {
@@ -398,24 +405,24 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                             BF_STAT(const unsigned long long tw = globaltimer();)
                             mbar_wait_b(g, &full[sl], static_cast<unsigned>(idx / kNSlot) & 1u, fail);
                             BF_STAT(if (stat && threadIdx.x == 0) stat[1] += globaltimer() - tw;)
-                            float v[4];
-                            Vec4<WT>::load(reinterpret_cast<const WT *>(ring + sl * kSlotBytes) + e0, v, valid, true);
+                            float v[V];
+                            VecN<WT, V>::load(reinterpret_cast<const WT *>(ring + sl * kSlotBytes) + e0, v, valid, true);
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&empty[sl]);
                             const float c = lm.rc[i];
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) acc[j] = fmaf(c, v[j], acc[j]);
+                            for (int j = 0; j < V; ++j) acc[j] = fmaf(c, v[j], acc[j]);
                         }
                     }
                     if constexpr (MODE == 2) {   // AWC (Eq. 16)
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) acc[i] = fmaf(-p.lr, gv[u][a][i], acc[i]);
+                        for (int i = 0; i < V; ++i) acc[i] = fmaf(-p.lr, gv[u][a][i], acc[i]);
                     }
                     YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base + e0;
-                    Vec4<YT>::store_hint(yr, acc, valid, vec, pol_stream);
+                    VecN<YT, V>::store_hint(yr, acc, valid, vec, pol_stream);
                     if (p.shadow) {
                         bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base + e0;
-                        Vec4<bf16>::store_hint(sr, acc, valid, vec, pol_stream);
+                        VecN<bf16, V>::store_hint(sr, acc, valid, vec, pol_stream);
                     }
                 }
                 consumed += nrt;
@@ -439,15 +446,16 @@ static cudaError_t launch_fused_k(const ExchParams &p, int grid, cudaStream_t s)
     // the remote-tile ring is only needed when other processes exist
     const bool ringed = FusedCfg<K>::kRing && p.geo.nprocs > 1;
     if (!FusedCfg<K>::kRing && p.geo.nprocs > 1) return cudaErrorInvalidValue;
-    const unsigned smem = ringed ? kNSlot * kSub * sizeof(WT) : 0;
+    constexpr int kSubT = kThreads * FusedVec<XT>::V;
+    const unsigned smem = ringed ? kNSlot * kSubT * sizeof(WT) : 0;
     static int maxg[2] = {0, 0};   // co-resident CTAs of this instantiation (queried once per smem size)
     if (maxg[ringed] == 0) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kNSlot * kSub * sizeof(WT));
+                                             kNSlot * kSubT * sizeof(WT));
         if (e != cudaSuccess) return e;
         maxg[ringed] = max_coresident(fn, FusedCfg<K>::kThreadsPerCta, smem);
     }
-    const long long subs = (p.geo.count + kSub - 1) / kSub;
+    const long long subs = (p.geo.count + kSubT - 1) / kSubT;
     if (grid <= 0 || grid > maxg[ringed]) grid = maxg[ringed];
     if (grid > subs) grid = static_cast<int>(subs);
     if (grid > kMaxGrid) grid = kMaxGrid;

@@ -59,6 +59,7 @@ struct Window {
     void *x = nullptr;
     size_t count = 0;
     int dtype = 0, with_p = 0, zero_init = 0;
+    int ef = 0;                 // error feedback of the bf16 wire rounding (R24)
     int maxdin = 1, maxdout = 1;
     std::vector<WinSide> side;  // per global agent
     WinParams base{};           // offsets filled at creation
@@ -108,6 +109,7 @@ struct bf_ctx {
     size_t scratch_bytes = 0;
     int lag = 0;                              // BF_FUSED_LAG (0 = automatic)
     bool hier_staged = false;                 // BF_HIER=staged: always the staged hierarchical kernel
+    bool win_ef = false;                      // BF_WIN_EF=1: new windows start with error feedback on
 };
 
 bf_status bf_barrier_internal(bf_ctx *c);
@@ -418,6 +420,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
     if (const char *x = getenv("BF_FUSED_LAG")) c->lag = std::max(0, atoi(x));
     if (const char *x = getenv("BF_HIER")) c->hier_staged = strcmp(x, "staged") == 0;
+    if (const char *x = getenv("BF_WIN_EF")) c->win_ef = atoi(x) != 0;
     if (const char *x = getenv("BF_STATS"))
         if (atoi(x) && cudaMalloc(&c->stats, static_cast<size_t>(kMaxGrid) * 8 * 8) == cudaSuccess)
             cudaMemset(c->stats, 0, static_cast<size_t>(kMaxGrid) * 8 * 8);
@@ -879,6 +882,7 @@ bf_status bf_win_create(bf_ctx *c, const char *name, void *x, size_t count, bf_d
     w.count = count;
     w.dtype = dtype;
     w.with_p = with_p ? 1 : 0;
+    w.ef = c->win_ef ? 1 : 0;
     w.zero_init = zero_init ? 1 : 0;
     w.side.resize(c->n);
     for (int i = 0; i < c->n; ++i) {
@@ -943,6 +947,15 @@ bf_status bf_win_create(bf_ctx *c, const char *name, void *x, size_t count, bf_d
     return BF_OK;
 }
 
+bf_status bf_win_set_error_feedback(bf_ctx *c, const char *name, int enable) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    Window *w = find_win(c, name);
+    if (!w) return fail(BF_ERR_WINDOW, "unknown window '%s'", name ? name : "(null)");
+    w->ef = enable ? 1 : 0;
+    return BF_OK;
+}
+
 bf_status bf_win_free(bf_ctx *c, const char *name) {
     bf_status s = check_ctx(c);
     if (s) return s;
@@ -975,7 +988,7 @@ static bf_status win_push(bf_ctx *c, const char *name, const bf_weights *weights
     WinParams p;
     win_setup(c, w, agent_mask, p);
     p.overwrite = overwrite;
-    p.ef = (w->dtype == BF_BFLOAT16 && !overwrite) ? 1 : 0;
+    p.ef = (w->dtype == BF_BFLOAT16 && !overwrite && w->ef) ? 1 : 0;
     for (int a = 0; a < c->k; ++a) {
         const int gid = c->proc * c->k + a;
         const auto &outs = w->side[gid].out;

@@ -380,10 +380,11 @@ def test_window_sync_pushsum_matches_oracle():
     ctx.close()
 
 
-@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_window_async_event_model(dtype):
+@pytest.mark.parametrize("dtype,ef", [(torch.float32, False), (torch.bfloat16, False), (torch.bfloat16, True)])
+def test_window_async_event_model(dtype, ef):
     # random per-agent interleaving of accumulate / collect (agent_mask selects
     # the acting agent); the GPU follows the oracle's state machine event by event
+    # (bf16: with and without error feedback of the wire rounding, R24)
     Wst = _fig2_static()
     n = Wst.shape[0]
     count = 4099
@@ -392,6 +393,8 @@ def test_window_async_event_model(dtype):
     x = _gpu(synthetic.agents_x0(n, count), dtype)
     X0 = _np(x)
     ctx.win_create(x, "a", zero_init=True, with_p=True)
+    if ef:
+        ctx.win_set_error_feedback("a", True)
     win = ora.Window(Wst, np.concatenate([X0, np.ones((n, 1))], axis=1), zero_init=True)
     rng = np.random.default_rng(7)
     mass0 = X0.sum(axis=0)

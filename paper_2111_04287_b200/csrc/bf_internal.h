@@ -147,7 +147,7 @@ struct WinParams {
     int with_p;
     unsigned long long agent_mask;
     int maxdin, maxdout;
-    long long cpad;                         // row stride of slots / outboxes: count rounded up to 4
+    long long cpad;                         // row stride of slots / outboxes: count rounded up to 8
     // heap offsets (symmetric)
     unsigned long long slot_off;            // [k][maxdin][2][count]
     unsigned long long pslot_off;           // double [k][maxdin][2]

@@ -500,6 +500,12 @@ struct VecN<T, 4> {
         Vec4<T>::store_hint(p, v, valid, vec, pol);
     }
     static __device__ __forceinline__ float wire(float f) { return Vec4<T>::wire(f); }
+    static __device__ __forceinline__ void store(T *p, const float v[4], int valid, bool vec) {
+        Vec4<T>::store(p, v, valid, vec);
+    }
+    static __device__ __forceinline__ void load_cg(const T *p, float v[4], int valid, bool vec) {
+        Vec4<T>::load_cg(p, v, valid, vec);
+    }
 };
 
 template <>
@@ -564,6 +570,49 @@ struct VecN<__nv_bfloat16, 8> {
         }
     }
     static __device__ __forceinline__ float wire(float f) { return bf2f(f2bf(f)); }
+    static __device__ __forceinline__ void store(__nv_bfloat16 *p, const float v[8], int valid, bool vec) {
+        unsigned short h[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) h[i] = f2bf(v[i]);
+        if (vec && valid == 8) {
+            uint4 w;
+            w.x = h[0] | (static_cast<unsigned>(h[1]) << 16); w.y = h[2] | (static_cast<unsigned>(h[3]) << 16);
+            w.z = h[4] | (static_cast<unsigned>(h[5]) << 16); w.w = h[6] | (static_cast<unsigned>(h[7]) << 16);
+            *reinterpret_cast<uint4 *>(p) = w;
+        } else {
+            unsigned short *q = reinterpret_cast<unsigned short *>(p);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (i < valid) q[i] = h[i];
+        }
+    }
+    static __device__ __forceinline__ void load_cg(const __nv_bfloat16 *p, float v[8], int valid, bool vec) {
+        Raw r;
+        if (vec && valid == 8) {
+            r = __ldcg(reinterpret_cast<const uint4 *>(p));
+        } else {
+            const unsigned short *q = reinterpret_cast<const unsigned short *>(p);
+            unsigned e[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) e[i] = i < valid ? __ldcg(q + i) : 0u;
+            r.x = e[0] | (e[1] << 16); r.y = e[2] | (e[3] << 16);
+            r.z = e[4] | (e[5] << 16); r.w = e[6] | (e[7] << 16);
+        }
+        unpack(r, v);
+    }
+};
+
+// fp32 side buffers (window outboxes) next to 8-wide bf16 vectors: two float4
+template <>
+struct VecN<float, 8> {
+    static __device__ __forceinline__ void load(const float *p, float v[8], int valid, bool vec) {
+        Vec4<float>::load(p, v, valid < 4 ? valid : 4, vec);
+        Vec4<float>::load(p + 4, v + 4, valid > 4 ? valid - 4 : 0, vec);
+    }
+    static __device__ __forceinline__ void store(float *p, const float v[8], int valid, bool vec) {
+        Vec4<float>::store(p, v, valid < 4 ? valid : 4, vec);
+        Vec4<float>::store(p + 4, v + 4, valid > 4 ? valid - 4 : 0, vec);
+    }
 };
 
 // valid elements of the V-vector at offset e of a row with `rem` elements left

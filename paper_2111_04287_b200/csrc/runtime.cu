@@ -906,7 +906,7 @@ bf_status bf_win_create(bf_ctx *c, const char *name, void *x, size_t count, bf_d
         }                                              \
         b.field = off;                                 \
     } while (0)
-    const size_t cpad = (count + 3) / 4 * 4;
+    const size_t cpad = (count + 7) / 8 * 8;   // 16-byte rows for 8-wide bf16 / 4-wide fp32 vectors
     WALLOC(slot_off, K * DI * 2 * cpad * es);
     WALLOC(pslot_off, K * DI * 2 * 8);
     WALLOC(version_off, K * DI * 8);
@@ -973,7 +973,8 @@ bf_status bf_win_free(bf_ctx *c, const char *name) {
 static bf_status win_setup(bf_ctx *c, Window *w, uint64_t agent_mask, WinParams &p) {
     p = w->base;
     p.geo = make_geo(c, w->count);
-    p.geo.vec_ok = (w->count % 4 == 0) && aligned16(w->x);
+    // 16-byte vectors: 4 fp32 or 8 bf16 elements per access (WinVec)
+    p.geo.vec_ok = (w->count % (w->dtype == BF_BFLOAT16 ? 8 : 4) == 0) && aligned16(w->x);
     const uint64_t all = c->k >= 64 ? ~0ull : ((1ull << c->k) - 1);
     p.agent_mask = agent_mask ? (agent_mask & all) : all;
     return BF_OK;

@@ -43,8 +43,19 @@ __global__ void win_push_decide(const __grid_constant__ WinParams p) {
     }
 }
 
+// Elements per thread-vector (16-byte accesses of the window dtype) and vectors
+// per thread per tile; element of vector j of this thread: (j*kThreads + tid)*V.
+template <typename T>
+struct WinVec {
+    static constexpr int V = sizeof(T) >= 4 ? 4 : 8;
+    static constexpr int NV = kTile / (kThreads * V);
+};
+template <int V>
+__device__ __forceinline__ int win_elem(int j) { return (j * kThreads + threadIdx.x) * V; }
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) win_push_kernel(const __grid_constant__ WinParams p) {
+    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV;
     const Geometry &g = p.geo;
     const unsigned long long me = g.peer_base[g.me];
     Pad *pad = pad_of(g, g.me);
@@ -60,10 +71,19 @@ __global__ void __launch_bounds__(kThreads) win_push_kernel(const __grid_constan
         if (!active(p, a)) continue;
         const long long base = static_cast<long long>(t) * kTile, rem = count - base;
         T *xr = static_cast<T *>(p.x) + static_cast<long long>(a) * count + base;
-        float xv[kVecPerThread][4];
+        // x and the first destination's outbox are loaded before the first use
+        float xv[NV][V], ob0[NV][V];
+        const bool ob0_used = p.nout[a] > 0 && obv[a * p.maxdout + p.out_q[a][0]] != 0 && !p.overwrite;
+        const float *ob0p = at<float>(me, p.outbox_off) +
+                            static_cast<long long>(a * p.maxdout + (p.nout[a] > 0 ? p.out_q[a][0] : 0)) * p.cpad + base;
 #pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j)
-            Vec4<T>::load(xr + tile_elem(j), xv[j], clamp_valid(rem, tile_elem(j)), vec);
+        for (int j = 0; j < NV; ++j)
+            VecN<T, V>::load(xr + win_elem<V>(j), xv[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+        if (ob0_used) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+                VecN<float, V>::load(ob0p + win_elem<V>(j), ob0[j], clamp_valid_v<V>(rem, win_elem<V>(j)), true);
+        }
         for (int q = 0; q < p.nout[a]; ++q) {
             const int qo = p.out_q[a][q], dst = p.out_dst[a][q], qin = p.out_qin[a][q];
             const float s = p.out_s[a][q];
@@ -71,13 +91,20 @@ __global__ void __launch_bounds__(kThreads) win_push_kernel(const __grid_constan
             const bool deliver = dec[ci] != 0;
             const bool use_ob = obv[ci] != 0 && !p.overwrite;
             float *ob = at<float>(me, p.outbox_off) + static_cast<long long>(ci) * p.cpad + base;
-            float pay[kVecPerThread][4];
+            float pay[NV][V];
 #pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j) {
-                const int vl = clamp_valid(rem, tile_elem(j));
-                if (use_ob) Vec4<float>::load(ob + tile_elem(j), pay[j], vl, true);
+            for (int j = 0; j < NV; ++j) {
+                const int vl = clamp_valid_v<V>(rem, win_elem<V>(j));
+                if (use_ob) {
+                    if (q == 0) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) pay[j][i] = use_ob ? fmaf(s, xv[j][i], pay[j][i]) : s * xv[j][i];
+                        for (int i = 0; i < V; ++i) pay[j][i] = ob0[j][i];
+                    } else {
+                        VecN<float, V>::load(ob + win_elem<V>(j), pay[j], vl, true);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < V; ++i) pay[j][i] = use_ob ? fmaf(s, xv[j][i], pay[j][i]) : s * xv[j][i];
             }
             if (deliver) {
                 const int half = static_cast<int>(dlv[ci] & 1ull);
@@ -85,32 +112,32 @@ __global__ void __launch_bounds__(kThreads) win_push_kernel(const __grid_constan
                                 p.slot_off + ((static_cast<unsigned long long>(dst % k) * p.maxdin + qin) * 2 + half) *
                                                  p.cpad * esize(p)) + base;
 #pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j) {
-                    const int vl = clamp_valid(rem, tile_elem(j));
-                    Vec4<T>::store(slot + tile_elem(j), pay[j], vl, vec);
-                    if (p.ef) {   // keep the wire rounding residual (bf16) in the outbox
-                        float r[4];
+                for (int j = 0; j < NV; ++j) {
+                    const int vl = clamp_valid_v<V>(rem, win_elem<V>(j));
+                    VecN<T, V>::store(slot + win_elem<V>(j), pay[j], vl, vec);
+                    if (p.ef) {   // keep the wire rounding residual (bf16) in the outbox (R24)
+                        float r[V];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
+                        for (int i = 0; i < V; ++i) {
                             const float wire = sizeof(T) == 2 ? bf2f(f2bf(pay[j][i])) : pay[j][i];
                             r[i] = pay[j][i] - wire;
                         }
-                        Vec4<float>::store(ob + tile_elem(j), r, vl, true);
+                        VecN<float, V>::store(ob + win_elem<V>(j), r, vl, true);
                     }
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j)
-                    Vec4<float>::store(ob + tile_elem(j), pay[j], clamp_valid(rem, tile_elem(j)), true);
+                for (int j = 0; j < NV; ++j)
+                    VecN<float, V>::store(ob + win_elem<V>(j), pay[j], clamp_valid_v<V>(rem, win_elem<V>(j)), true);
             }
         }
         const float sw = p.self_w[a];
         if (sw != 1.0f) {
 #pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j) {
+            for (int j = 0; j < NV; ++j) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) xv[j][i] *= sw;
-                Vec4<T>::store(xr + tile_elem(j), xv[j], clamp_valid(rem, tile_elem(j)), vec);
+                for (int i = 0; i < V; ++i) xv[j][i] *= sw;
+                VecN<T, V>::store(xr + win_elem<V>(j), xv[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
             }
         }
     }
@@ -189,6 +216,7 @@ __global__ void __launch_bounds__(kThreads) win_collect_kernel(const __grid_cons
     for (int idx = threadIdx.x; idx < k * p.maxdin; idx += blockDim.x)
         (void)ld_acquire_sys(at<unsigned long long>(me, p.version_off) + idx);
     __syncthreads();
+    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV;
     const long long items = static_cast<long long>(k) * g.T;
     for (long long w = blockIdx.x; w < items; w += gridDim.x) {
         const int t = static_cast<int>(w / k), b = static_cast<int>(w % k);
@@ -196,14 +224,31 @@ __global__ void __launch_bounds__(kThreads) win_collect_kernel(const __grid_cons
         const long long base = static_cast<long long>(t) * kTile, rem = count - base;
         const T *xr = static_cast<const T *>(p.x) + static_cast<long long>(b) * count + base;
         T *outr = static_cast<T *>(p.out) + static_cast<long long>(b) * count + base;
-        float acc[kVecPerThread][4];
         const float sw = update ? p.self_w[b] : 1.0f;
-#pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j) {
-            Vec4<T>::load(xr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[j][i] *= sw;
+        // the first payload of the first in-neighbour is loaded together with x
+        // (the common one-payload case has every load in flight before the first use)
+        const T *pre_h = nullptr;
+        if (p.nin[b] > 0) {
+            const int ci = b * p.maxdin;
+            const unsigned long long c0 = snap[ci * 2], v0 = snap[ci * 2 + 1];
+            const unsigned long long m0 = update ? v0 - 1 : c0;
+            if (update || c0 < v0)
+                pre_h = at<const T>(me, p.slot_off + (static_cast<unsigned long long>(ci) * 2 + (m0 & 1)) * p.cpad *
+                                                         esize(p)) + base;
         }
+        float acc[NV][V], pre[NV][V];
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            VecN<T, V>::load(xr + win_elem<V>(j), acc[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+        if (pre_h) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+                VecN<T, V>::load_cg(pre_h + win_elem<V>(j), pre[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+        }
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[j][i] *= sw;
         for (int q = 0; q < p.nin[b]; ++q) {
             const int ci = b * p.maxdin + q;
             const unsigned long long c = snap[ci * 2], v = snap[ci * 2 + 1];
@@ -217,18 +262,23 @@ __global__ void __launch_bounds__(kThreads) win_collect_kernel(const __grid_cons
                 const T *h = at<const T>(me, p.slot_off + (static_cast<unsigned long long>(ci) * 2 + (m & 1)) *
                                                               p.cpad * esize(p)) + base;
 #pragma unroll
-                for (int j = 0; j < kVecPerThread; ++j) {
-                    float v4[4];
-                    Vec4<T>::load_cg(h + tile_elem(j), v4, clamp_valid(rem, tile_elem(j)), vec);
+                for (int j = 0; j < NV; ++j) {
+                    float v4[V];
+                    if (h == pre_h) {   // already loaded with x
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(r, v4[i], acc[j][i]);
+                        for (int i = 0; i < V; ++i) v4[i] = pre[j][i];
+                    } else {
+                        VecN<T, V>::load_cg(h + win_elem<V>(j), v4, clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+                    }
+#pragma unroll
+                    for (int i = 0; i < V; ++i) acc[j][i] = fmaf(r, v4[i], acc[j][i]);
                 }
                 if (update) break;
             }
         }
 #pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j)
-            Vec4<T>::store(outr + tile_elem(j), acc[j], clamp_valid(rem, tile_elem(j)), vec);
+        for (int j = 0; j < NV; ++j)
+            VecN<T, V>::store(outr + win_elem<V>(j), acc[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
     }
 
     __syncthreads();

@@ -12,6 +12,8 @@
   H   hierarchical_neighbor_allreduce, 25.6M fp32, L = 2, 4
   O   ATC optimizer wrapper over ResNet-50's 161 parameter tensors (tensor
       fusion into buckets, one fused kernel per bucket)
+  E   Exact-Diffusion step (appendix ed-1..ed-3), 8 agents x 25.6M fp32; and
+      in C2, Exact-Diffusion vs ATC distance to the exact minimiser x*
 
 One JSON object per line.  N = 1: the 8 agents are virtual agents of one GPU;
 under torchrun, 8/N agents per GPU.  Every number is CUDA-event time on the
@@ -31,7 +33,7 @@ sys.path.insert(0, ROOT)
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c3,c5,h,o,c2")
+    ap.add_argument("--only", default="c1,c3,c5,h,o,e,c2")
     ap.add_argument("--agents", type=int, default=8)
     ap.add_argument("--max-bytes", type=int, default=1 << 30)
     ap.add_argument("--out", default=None)
@@ -237,6 +239,28 @@ def main():
         except Exception as ex:  # noqa: BLE001
             emit({"config": "C5", "error": repr(ex)[:300]})
 
+    # ----------------------------------------------------------------- E ----
+    # Exact-Diffusion step (appendix ed-1..ed-3) fused like ATC, C4-sized vectors
+    if "e" in only:
+        n = a.agents
+        k = n // world
+        count = 25_600_000
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=k * 2 * count * 4 + (256 << 20), device=local)
+        ctx.set_topology(bfp.topology_matrix("exp2", n))
+        x = torch.empty(k, count, device="cuda")
+        g = torch.empty(k, count, device="cuda")
+        psi = torch.empty(k, count, device="cuda")
+        for la in range(k):
+            bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + ctx.rank + la)
+            bfp.Context.fill_uniform(g[la], synthetic.grad_seed(0, ctx.rank + la), scale=2.0 ** -7)
+        psi.copy_(x)
+        ms = timed(lambda: ctx.exact_diffusion_step(x, g, psi, 0.1), 20)
+        hbm = k * 20 * count / (ms * 1e-3) / 1e9     # x, g, psi read + psi, x write
+        emit({"config": f"E Exact-Diffusion step, {n} agents x {count} fp32, static exp-2", "ms_per_step": ms,
+              "iters_per_s": 1e3 / ms, "hbm_gbs": hbm if world == 1 else None,
+              "hbm_frac": hbm / peak if world == 1 else None})
+        ctx.close()
+
     # ----------------------------------------------------------------- O ----
     # ATC optimizer over ResNet-50's 161 parameter tensors (tensor fusion into
     # buckets, one fused kernel per bucket), synthetic gradients (§8(f) rank 3)
@@ -281,9 +305,11 @@ def main():
         ctx = bfp.Context(agents_per_proc=n, heap_bytes=64 << 20, device=local)
         x = torch.zeros(n, d, device="cuda")
         g = torch.empty_like(x)
-        for topo in ("exp2", "one_peer"):
+        for topo in ("exp2", "one_peer", "exp2_exact_diffusion"):
             x.zero_()
-            if topo == "exp2":
+            ed = topo == "exp2_exact_diffusion"
+            psi = torch.zeros_like(x) if ed else None
+            if topo.startswith("exp2"):
                 ctx.set_topology(bfp.topology_matrix("exp2", n))
             else:
                 ctx.set_dynamic_schedule("one_peer_exp2", 0)
@@ -291,7 +317,10 @@ def main():
             def step():
                 r_ = torch.bmm(As, x.unsqueeze(2)).squeeze(2) - bs
                 torch.bmm(As.transpose(1, 2), r_.unsqueeze(2), out=g.unsqueeze(2))
-                ctx.atc_step(x, g, lr)
+                if ed:
+                    ctx.exact_diffusion_step(x, g, psi, lr)
+                else:
+                    ctx.atc_step(x, g, lr)
             ms = timed(step, 200, warm=0)
             ctx.set_dynamic_schedule("none")
             xs, _ = ora.lsq_solve(As.double().cpu().numpy(), bs.double().cpu().numpy(), tol=1e-10, max_iter=500)

@@ -150,6 +150,21 @@ bf_status bf_atc_step(bf_ctx *ctx, float *x, const void *g, bf_dtype g_dtype, si
  * exchange does not depend on this step's gradient. */
 bf_status bf_awc_step(bf_ctx *ctx, float *x, const void *g, bf_dtype g_dtype, size_t count, float lr,
                       const bf_weights *weights, void *stream);
+/* Exact-Diffusion step (appendix of the paper, Eqs. ed-1..ed-3, Listing ED-static;
+ * SURVEY 8(f) rank 4), fused like bf_atc_step:
+ *   psi_i = x_i - lr * g_i            (local update; written over psi, the state)
+ *   phi_i = psi_i + x_i - psi_prev_i  (bias correction; psi_prev = psi on entry)
+ *   x_i  <- sum_j w_ij phi_j          (partial averaging: static topology, schedule
+ *                                      or per-call views as in bf_neighbor_allreduce)
+ * x and psi: fp32 device tensors [agents_per_proc][count], updated in place; g:
+ * fp32 or bf16.  Initialise psi = x^(0) so the first step is an ATC step.  The
+ * neighbours' phi travel in `wire` (bf16: RNE, R18/R25).  Needs the fused
+ * exchange kernel (agents_per_proc 1, 2, 4, or 8 on one GPU): else
+ * BF_ERR_UNSUPPORTED.  Errors as bf_atc_step; host pointers are rejected. */
+bf_status bf_exact_diffusion_step(bf_ctx *ctx, float *x, const void *g, bf_dtype g_dtype, float *psi,
+                                  size_t count, float lr, bf_dtype wire, const bf_weights *weights,
+                                  void *stream);
+
 /* bf_hierarchical_neighbor_allreduce (R12): y = (W_M kron J_L/L) x:
  * intra-machine average, machine-level neighbour averaging, broadcast.
  * machine_weights: NULL (static machine topology) or an array of

@@ -53,6 +53,7 @@ def lib():
         L.ora_mix.argtypes = [C.c_int, C.c_longlong, _dp, _dp, _dp]
         L.ora_atc.argtypes = [C.c_int, C.c_longlong, _dp, _dp, _dp, C.c_double, C.c_int, _dp]
         L.ora_awc.argtypes = [C.c_int, C.c_longlong, _dp, _dp, _dp, C.c_double, _dp]
+        L.ora_exact_diffusion.argtypes = [C.c_int, C.c_longlong, _dp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp]
         L.ora_hier.argtypes = [C.c_int, C.c_int, C.c_longlong, _dp, _dp, _dp]
         L.ora_bf16_rne.argtypes = [C.c_float]
         L.ora_bf16_rne.restype = C.c_uint16
@@ -185,6 +186,16 @@ def atc(W, X, G, lr, wire_bf16=False):
     lib().ora_atc(W.shape[0], X.shape[1], _d(W), _d(X), _d(G), float(np.float32(lr)),
                   1 if wire_bf16 else 0, _d(Y))
     return Y
+
+
+def exact_diffusion(W, X, G, Psi_prev, lr, wire_bf16=False):
+    """One Exact-Diffusion step (appendix Eqs. ed-1..ed-3): returns (x^(k+1), psi^(k))."""
+    W, X, G, P = _f64(W), _f64(X), _f64(G), _f64(Psi_prev)
+    Y = np.zeros_like(X)
+    Pout = np.zeros_like(X)
+    lib().ora_exact_diffusion(W.shape[0], X.shape[1], _d(W), _d(X), _d(G), _d(P), float(np.float32(lr)),
+                              1 if wire_bf16 else 0, _d(Y), _d(Pout))
+    return Y, Pout
 
 
 def awc(W, X, G, lr):

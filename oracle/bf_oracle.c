@@ -224,6 +224,32 @@ void ora_atc(int n, long long count, const double *W, const double *X,
     free(wire);
 }
 
+/* Exact-Diffusion, appendix Eqs. ed-1..ed-3 (Listing ED-static):
+ *   psi_i^(k) = x_i^(k) - gamma * g_i                 (local update; stored as fp32 state, R25)
+ *   phi_i^(k) = psi_i^(k) + x_i^(k) - psi_i^(k-1)     (bias correction; defined value fp32, R25)
+ *   x_i^(k+1) = w_ii phi_i^(k) + sum_j w_ij phi_j^(k) (partial averaging; neighbours' phi as on the wire)
+ * Psi_prev holds psi^(k-1); Psi_out receives psi^(k). */
+void ora_exact_diffusion(int n, long long count, const double *W, const double *X, const double *G,
+                         const double *Psi_prev, double lr, int wire_bf16, double *Y, double *Psi_out) {
+    double *phi = (double *)malloc(sizeof(double) * (size_t)n * count);
+    double *wire = (double *)malloc(sizeof(double) * (size_t)n * count);
+    for (long long q = 0; q < (long long)n * count; ++q) {
+        const double psi = (double)ora_f32(X[q] - lr * G[q]);
+        Psi_out[q] = psi;
+        phi[q] = (double)ora_f32(psi + X[q] - Psi_prev[q]);
+        wire[q] = wire_bf16 ? bf16_value(ora_bf16_rne((float)phi[q])) : phi[q];
+    }
+    for (int i = 0; i < n; ++i)
+        for (long long e = 0; e < count; ++e) {
+            double acc = W[i * n + i] * phi[(long long)i * count + e];
+            for (int j = 0; j < n; ++j)
+                if (j != i) acc += W[i * n + j] * wire[(long long)j * count + e];
+            Y[(long long)i * count + e] = acc;
+        }
+    free(phi);
+    free(wire);
+}
+
 /* AWC, Eq. 16: x_i^k = sum_{j in N+(i)} w_ij x_j^{k-1} - gamma g_i. */
 void ora_awc(int n, long long count, const double *W, const double *X,
              const double *G, double lr, double *Y) {

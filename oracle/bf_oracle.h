@@ -55,6 +55,8 @@ void ora_mix(int n, long long count, const double *W, const double *X, double *Y
 void ora_atc(int n, long long count, const double *W, const double *X,
              const double *G, double lr, int wire_bf16, double *Y);
 /* AWC (Eq. 16): y_i = sum_j w_ij x_j - lr*g_i  */
+void ora_exact_diffusion(int n, long long count, const double *W, const double *X, const double *G,
+                         const double *Psi_prev, double lr, int wire_bf16, double *Y, double *Psi_out);
 void ora_awc(int n, long long count, const double *W, const double *X,
              const double *G, double lr, double *Y);
 

@@ -80,6 +80,7 @@ _SIGS = {
     "bf_kernel_launches": (_u64, [_vp]),
     "bf_exchange_stats": (_i, [_vp, C.POINTER(_u64), _sz, _i]),
     "bf_win_set_error_feedback": (_i, [_vp, C.c_char_p, _i]),
+    "bf_exact_diffusion_step": (_i, [_vp, _vp, _vp, _i, _vp, _sz, C.c_float, _i, _wp, _vp]),
 }
 
 _lib = None

@@ -211,6 +211,20 @@ class Context:
                                    v.ptr() if v else None, _stream_ptr(stream)))
         return x
 
+    def exact_diffusion_step(self, x: torch.Tensor, g: torch.Tensor, psi: torch.Tensor, lr: float,
+                             wire: torch.dtype = torch.float32, self_weight=None, src_weights=None,
+                             dst_weights=None, stream=None) -> torch.Tensor:
+        """Exact-Diffusion (appendix ed-1..ed-3): psi <- x - lr g, x <- W (psi + x - psi_prev),
+        fused in one kernel; x and psi (fp32) are updated in place (psi = x^(0) initially)."""
+        if x.dtype != torch.float32 or psi.dtype != torch.float32 or psi.shape != x.shape:
+            raise ValueError("x and psi must be fp32 tensors of the same shape")
+        count = self._rows(x)
+        v = self._views(self_weight, src_weights, dst_weights)
+        check(self.lib.bf_exact_diffusion_step(self.h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()),
+                                               _DT[g.dtype], C.c_void_p(psi.data_ptr()), count, float(lr),
+                                               _DT[wire], v.ptr() if v else None, _stream_ptr(stream)))
+        return x
+
     def awc_step(self, x: torch.Tensor, g: torch.Tensor, lr: float, self_weight=None, src_weights=None,
                  dst_weights=None, stream=None) -> torch.Tensor:
         """Fused AWC-DSGD step (Eq. 16): x <- W x - lr*g, in place on the fp32 master x."""

@@ -27,6 +27,7 @@ namespace bf {
 cudaError_t launch_fused_nar(const ExchParams &p, int x_kind, int grid, cudaStream_t s);
 cudaError_t launch_fused_atc(const ExchParams &p, int g_kind, int wire_kind, int grid, cudaStream_t s);
 cudaError_t launch_fused_awc(const ExchParams &p, int g_kind, int wire_kind, int grid, cudaStream_t s);
+cudaError_t launch_fused_ed(const ExchParams &p, int g_kind, int wire_kind, int grid, cudaStream_t s);
 
 // Shared-memory ring of the TMA-prefetched x / g tiles (2 stages).
 template <typename XT, typename GT, bool HAS_G>
@@ -471,6 +472,10 @@ static cudaError_t launch_fused(const ExchParams &p, int x_kind, int g_kind, int
     if (!has_g) {
         if (x_kind != wire_kind || x_kind != y_kind) return cudaErrorInvalidValue;
         return launch_fused_nar(p, x_kind, grid, s);
+    }
+    if (p.psi) {   // Exact-Diffusion
+        if (x_kind != 0 || y_kind != 0) return cudaErrorInvalidValue;
+        return launch_fused_ed(p, g_kind, wire_kind, grid, s);
     }
     if (x_kind != 0 || y_kind != 0) return cudaErrorInvalidValue;
     return launch_fused_atc(p, g_kind, wire_kind, grid, s);

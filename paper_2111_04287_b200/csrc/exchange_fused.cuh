@@ -40,6 +40,8 @@ namespace bf {
 //   MODE 0: neighbor_allreduce (x is the wire value)
 //   MODE 1: ATC  (Eq. 4-5, Eq. 17):  y_a = sum_b w_ab (x_b - lr g_b)
 //   MODE 2: AWC  (Eq. 16):           y_a = sum_b w_ab x_b - lr g_a
+//   MODE 3: Exact-Diffusion (appendix ed-1..ed-3): psi = x - lr g (stored over
+//           psi_prev), phi = psi + x - psi_prev, y_a = sum_b w_ab phi_b
 // Summation order (R18): self, local sources in (a - b) mod K order, then the
 // remote sources in table order; a neighbour's term always uses the value as it
 // travels on the wire (bf16 RNE for a bf16 wire), the self term the fp32 value.
@@ -318,6 +320,14 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
 #pragma unroll
                         for (int i = 0; i < V; ++i) v[i] = fmaf(-p.lr, gv[i], v[i]);
                     }
+                    if constexpr (MODE == 3) {   // Exact-Diffusion: phi = (x - lr g) + x - psi_prev
+                        float gv[V], pv[V];
+                        VecN<GT, V>::load_hint(grow(a) + base + e0, gv, valid, vec, pol_keep);
+                        VecN<float, V>::load_hint(p.psi + static_cast<long long>(a) * count + base + e0, pv, valid,
+                                                  vec, pol_keep);
+#pragma unroll
+                        for (int i = 0; i < V; ++i) v[i] = (fmaf(-p.lr, gv[i], v[i]) + v[i]) - pv[i];
+                    }
                     VecN<WT, V>::store_hint(slot_of(g.me * K + a) + base + e0, v, valid, true, pol_keep);
                 }
                 ++mp;
@@ -333,6 +343,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                 // every local load of the group is issued (raw) before the first use
                 typename VecN<XT, V>::Raw xr[U][K];
                 typename VecN<GT, V>::Raw gr[U][HAS_G ? K : 1];
+                typename VecN<float, MODE == 3 ? V : 4>::Raw pr[U][MODE == 3 ? K : 1];   // Exact-Diffusion psi^(k-1)
                 // one branch per group: the common case is a straight line of vector loads
                 bool fast = vec;
 #pragma unroll
@@ -347,6 +358,12 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                         if constexpr (HAS_G) {
 #pragma unroll
                             for (int a = 0; a < K; ++a) VecN<GT, V>::load_raw_fast(grow(a) + base, gr[u][a], pol_stream);
+                        }
+                        if constexpr (MODE == 3) {
+#pragma unroll
+                            for (int a = 0; a < K; ++a)
+                                VecN<float, V>::load_raw_fast(p.psi + static_cast<long long>(a) * count + base, pr[u][a],
+                                                              pol_stream);
                         }
                     }
                 } else {
@@ -363,6 +380,12 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                             for (int a = 0; a < K; ++a)
                                 VecN<GT, V>::load_raw(grow(a) + base + e0, gr[u][a], valid, pol_stream);
                         }
+                        if constexpr (MODE == 3) {
+#pragma unroll
+                            for (int a = 0; a < K; ++a)
+                                VecN<float, V>::load_raw(p.psi + static_cast<long long>(a) * count + base + e0, pr[u][a],
+                                                         valid, pol_stream);
+                        }
                     }
                 }
 #pragma unroll
@@ -371,6 +394,17 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                     for (int a = 0; a < K; ++a) {
                         VecN<XT, V>::unpack(xr[u][a], xv[u][a]);
                         if constexpr (HAS_G) VecN<GT, V>::unpack(gr[u][a], gv[u][a]);
+                        if constexpr (MODE == 3) {   // psi_prev kept in gv's place after use below
+                            float pv[V];
+                            VecN<float, V>::unpack(pr[u][a], pv);
+                            // psi = x - lr g (ed-1, the new state); phi = psi + x - psi_prev (ed-2)
+#pragma unroll
+                            for (int i = 0; i < V; ++i) {
+                                const float psi = fmaf(-p.lr, gv[u][a][i], xv[u][a][i]);
+                                gv[u][a][i] = psi;
+                                xv[u][a][i] = (psi + xv[u][a][i]) - pv[i];
+                            }
+                        }
                     }
             }
             for (int u = 0; u < nu; ++u) {
@@ -381,6 +415,12 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                     for (int a = 0; a < K; ++a)
 #pragma unroll
                         for (int i = 0; i < V; ++i) xv[u][a][i] = fmaf(-p.lr, gv[u][a][i], xv[u][a][i]);   // Eq. 4
+                }
+                if constexpr (MODE == 3) {   // store psi^(k) over psi^(k-1) (same elements, same thread)
+#pragma unroll
+                    for (int a = 0; a < K; ++a)
+                        VecN<float, V>::store_hint(p.psi + static_cast<long long>(a) * count + base + e0, gv[u][a], valid,
+                                                   vec, pol_stream);
                 }
 #pragma unroll
                 for (int a = 0; a < K; ++a) {

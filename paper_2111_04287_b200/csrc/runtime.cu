@@ -622,7 +622,7 @@ bf_status bf_reserve(bf_ctx *c, size_t bytes_per_agent) {
 static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *y, void *shadow, size_t count,
                                  int x_kind, int g_kind, int wire_kind, int y_kind, float lr,
                                  const bf_weights *weights, cudaStream_t st, const void *awc_g = nullptr,
-                                 const SrcTab *static_tab = nullptr) {
+                                 const SrcTab *static_tab = nullptr, float *psi = nullptr) {
     if (count == 0) return BF_OK;
     if (count > (1ull << 40)) return fail(BF_ERR_ARG, "count too large");
     ExchParams p;
@@ -677,6 +677,13 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     p.prog_off = c->prog_off;
     p.stats = c->stats;
     p.lag = c->lag;
+    if (psi) {   // Exact-Diffusion: only the fused kernel implements MODE 3
+        if (p.kernel != 3)
+            return fail(BF_ERR_UNSUPPORTED, "Exact-Diffusion needs the fused exchange kernel (agents_per_proc 1, 2, 4 "
+                                            "or 8 on one GPU)");
+        if (!aligned16(psi)) p.geo.vec_ok = 0;
+        p.psi = psi;
+    }
     if (p.kernel == 3 && c->nprocs > 1 && y_kind != 0) {   // fp32 partial sums of a bf16 output
         s = ensure_stage(&c->scratch, &c->scratch_bytes, static_cast<size_t>(c->k) * count * 4);
         if (s) return s;
@@ -740,6 +747,20 @@ bf_status bf_awc_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, size
     if (is_host_ptr(x) || is_host_ptr(g)) return fail(BF_ERR_ARG, "bf_awc_step takes device tensors");
     return exchange_common(c, x, nullptr, x, nullptr, count, 0, g_dtype, 0, 0, lr, weights,
                            static_cast<cudaStream_t>(stream), g);
+}
+
+bf_status bf_exact_diffusion_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, float *psi, size_t count,
+                                  float lr, bf_dtype wire, const bf_weights *weights, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!x || !g || !psi) return fail(BF_ERR_ARG, "null tensor");
+    if ((g_dtype != BF_FLOAT32 && g_dtype != BF_BFLOAT16) || (wire != BF_FLOAT32 && wire != BF_BFLOAT16))
+        return fail(BF_ERR_UNSUPPORTED, "dtype");
+    if (!std::isfinite(lr)) return fail(BF_ERR_ARG, "non-finite lr");
+    if (is_host_ptr(x) || is_host_ptr(g) || is_host_ptr(psi))
+        return fail(BF_ERR_ARG, "bf_exact_diffusion_step takes device tensors");
+    return exchange_common(c, x, g, x, nullptr, count, 0, g_dtype, wire, 0, lr, weights,
+                           static_cast<cudaStream_t>(stream), nullptr, nullptr, psi);
 }
 
 bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, size_t count, bf_dtype dtype,

@@ -102,6 +102,20 @@ def main():
               Wk, X, tol, np.abs(Wk) @ (0.1 * np.abs(G.astype(np.float64))))
     ctx.set_dynamic_schedule("none")
 
+    # ---- Exact-Diffusion (appendix ed-1..ed-3), static exp-2 ------------------------
+    We = ora.exp2(n)
+    ctx.set_topology(We)
+    x, X = inputs(50003)
+    Ge = np.stack([synthetic.uniform(synthetic.grad_seed(3, r), 50003, scale=2.0 ** -7) for r in range(n)])
+    Pe = np.stack([synthetic.uniform(synthetic.grad_seed(4, r), 50003) for r in range(n)])
+    g = torch.from_numpy(Ge[rows].copy()).cuda()
+    psi = torch.from_numpy(Pe[rows].copy()).cuda()
+    ctx.exact_diffusion_step(x, g, psi, 0.1)
+    torch.cuda.synchronize()
+    ref, _ = ora.exact_diffusion(We, X, Ge.astype(np.float64), Pe.astype(np.float64), 0.1)
+    check("exact diffusion", np_(x), ref, We, X, 1e-6,
+          np.abs(We) @ (np.abs(X) + 0.1 * np.abs(Ge.astype(np.float64)) + np.abs(Pe.astype(np.float64))))
+
     # ---- hierarchical -------------------------------------------------------------
     for L in (2, n):
         if n % L or n // L < 1:

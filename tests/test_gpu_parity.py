@@ -620,3 +620,55 @@ def test_optimizer_bucketed_matches_oracle(overlap, awc):
     assert opt.steps_launched == len(opt.buckets)
     opt.remove_hooks()
     ctx.close()
+
+
+# ------------------------------------ Exact-Diffusion (appendix ed-1..ed-3, §8(f) 4) ---
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("wire,gdt", [(torch.float32, torch.float32), (torch.bfloat16, torch.float32),
+                                      (torch.float32, torch.bfloat16)])
+def test_exact_diffusion_step(n, wire, gdt):
+    lr = 0.1
+    ctx = _ctx(n)
+    W = ora.exp2(n) if n > 1 else np.eye(1)
+    ctx.set_topology(W)
+    for count in (1, 7, 1023, 4097, 70001):
+        x, X = _inputs(n, count)
+        g = _gpu(synthetic.agents_grad(n, count, 2), gdt)
+        G = _np(g)
+        psi = _gpu(synthetic.agents_grad(n, count, 9) * 64.0)
+        P = _np(psi)
+        ctx.exact_diffusion_step(x, g, psi, lr, wire=wire)
+        torch.cuda.synchronize()
+        ref, pref = ora.exact_diffusion(W, X, G, P, lr, wire_bf16=(wire == torch.bfloat16))
+        scale = np.abs(W) @ (2 * np.abs(X) + np.float32(lr) * np.abs(G) + np.abs(P))
+        assert_parity(_np(x), ref, W, X, TOL[wire], scale - np.abs(W) @ np.abs(X))
+        assert np.abs(_np(psi) - pref).max() <= 1e-6 * (np.abs(X) + lr * np.abs(G)).max()
+    ctx.close()
+
+
+def test_exact_diffusion_reaches_exact_minimiser_on_gpu():
+    # least squares (Eq. 12-13 shape, small): ED with a constant step converges to x*
+    # (the appendix's bias correction), gradients by torch bmm (workload plumbing)
+    # exp-2 on 8 agents: weights 1/4, exactly doubly stochastic in fp32.  (With 1/3
+    # weights the fp32 rows sum to 1 + 3e-8; ED integrates that into a ~1e-4 offset
+    # of its fixed point -- reading R25 in DESIGN.md.)
+    n, m, d, lr = 8, 64, 32, 0.5
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((n, m, d)) / np.sqrt(m)
+    b = rng.standard_normal((n, m))
+    xs = np.linalg.lstsq(A.reshape(n * m, d), b.reshape(n * m), rcond=None)[0]
+    ctx = _ctx(n)
+    ctx.set_topology(ora.exp2(n))
+    # the gradient in fp64 (plumbing; a TF32 GEMM would move the fixed point by ~1e-4)
+    At = torch.from_numpy(A).cuda()
+    bt = torch.from_numpy(b).cuda()
+    x = torch.zeros(n, d, device="cuda")
+    psi = x.clone()
+    for _ in range(4000):
+        x64 = x.double()
+        g = torch.bmm(At.transpose(1, 2), (torch.bmm(At, x64.unsqueeze(2)).squeeze(2) - bt).unsqueeze(2)).squeeze(2)
+        ctx.exact_diffusion_step(x, g.float().contiguous(), psi, lr)
+    torch.cuda.synchronize()
+    err = np.abs(_np(x) - xs[None, :]).max()
+    assert err < 1e-5 * np.abs(xs).max(), err   # the fp32 oracle reaches 3e-7 on this problem
+    ctx.close()

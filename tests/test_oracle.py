@@ -431,3 +431,55 @@ def test_window_async_pushsum_invariants():
     y = Xf[:, :-1] / Xf[:, -1:]
     assert np.abs(y - target).max() < 1e-9
     assert abs(win.mass(cnt - 1) - n) < 1e-12
+
+
+# ------------------------------------------- Exact-Diffusion (appendix ed-1..ed-3) ---
+def _lsq_problem(n=4, m=12, d=5, seed=11):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((n, m, d)) / np.sqrt(m)
+    b = rng.standard_normal((n, m))
+    # global minimiser of sum_i ||A_i x - b_i||^2 / 2 by a library solver (independent of the oracle)
+    xs = np.linalg.lstsq(A.reshape(n * m, d), b.reshape(n * m), rcond=None)[0]
+    return A, b, xs
+
+
+def test_exact_diffusion_converges_to_exact_minimiser():
+    # The appendix's claim: ED "can correct the bias suffered by
+    # decentralized gradient descent" -- with a constant step it reaches the exact
+    # minimiser x*, while ATC-DGD stops at an O(gamma) distance.  Ring topology (Listing ED).
+    n = 4
+    A, b, xs = _lsq_problem(n)
+    W = ora.ring(n)
+    lr = 0.3
+    grad = lambda X: np.einsum("imd,im->id", A, np.einsum("imd,id->im", A, X) - b)
+    X = np.zeros((n, A.shape[2]))
+    psi = X.copy()                 # psi^(-1) = x^(0): the first ED step is an ATC step
+    Xa = X.copy()
+    for _ in range(3000):
+        X, psi = ora.exact_diffusion(W, X, grad(X), psi, lr)
+        Xa = ora.atc(W, Xa, grad(Xa), lr)
+    err_ed = np.abs(X - xs[None, :]).max()
+    err_atc = np.abs(Xa - xs[None, :]).max()
+    assert err_ed < 2e-6, err_ed          # fp32 state: exact up to single precision
+    assert err_atc > 1e3 * err_ed, (err_atc, err_ed)
+
+
+def test_exact_diffusion_special_cases():
+    rng = np.random.default_rng(3)
+    n, c, lr = 3, 64, 0.25
+    X = rng.uniform(-1, 1, (n, c)).astype(np.float32).astype(np.float64)
+    G = rng.uniform(-1, 1, (n, c)).astype(np.float32).astype(np.float64)
+    P = rng.uniform(-1, 1, (n, c)).astype(np.float32).astype(np.float64)
+    # W = I: x+ = phi = (x - lr g) + x - psi_prev, psi = x - lr g  (ed-1, ed-2 written out)
+    Y, Pout = ora.exact_diffusion(np.eye(n), X, G, P, lr)
+    psi = X - np.float32(lr) * G
+    assert np.allclose(Pout, psi, rtol=0, atol=1e-7)
+    assert np.allclose(Y, psi + X - P, rtol=0, atol=2e-7)
+    # psi_prev = x: phi = psi, i.e. the step is exactly the ATC step (Eq. 17)
+    W = ora.exp2(n)
+    Y1, _ = ora.exact_diffusion(W, X, G, X, lr)
+    assert np.allclose(Y1, ora.atc(W, X, G, lr), rtol=0, atol=1e-12)
+    # doubly stochastic W preserves the sum over agents of phi (ed-3 + P:231-234)
+    Y2, _ = ora.exact_diffusion(W, X, G, P, lr)
+    phi = psi + X - P
+    assert np.allclose(Y2.sum(axis=0), phi.sum(axis=0), rtol=0, atol=1e-6)

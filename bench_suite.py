@@ -305,11 +305,15 @@ def main():
         ctx = bfp.Context(agents_per_proc=n, heap_bytes=64 << 20, device=local)
         x = torch.zeros(n, d, device="cuda")
         g = torch.empty_like(x)
-        for topo in ("exp2", "one_peer", "exp2_exact_diffusion"):
+        # Exact-Diffusion on the ring (the paper's Listing ED-static; ED assumes a symmetric W --
+        # on the directed exp-2 graph it diverges)
+        for topo in ("exp2", "one_peer", "ring_exact_diffusion"):
             x.zero_()
             ed = topo == "exp2_exact_diffusion"
             psi = torch.zeros_like(x) if ed else None
-            if topo.startswith("exp2"):
+            if topo == "ring_exact_diffusion":
+                ctx.set_topology(bfp.topology_matrix("ring", n))
+            elif topo == "exp2":
                 ctx.set_topology(bfp.topology_matrix("exp2", n))
             else:
                 ctx.set_dynamic_schedule("one_peer_exp2", 0)

@@ -24,7 +24,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    agents, count = 8, 25_600_000
+    agents = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    count = 25_600_000
     k = agents // world
     ctx = bfp.Context(agents_per_proc=k, heap_bytes=k * 2 * count * 4 + (64 << 20), device=local)
     n = ctx.n

@@ -318,9 +318,22 @@ static int stream_grid(long long items) {
     return g < 1 ? 1 : static_cast<int>(g);
 }
 
+// grid of a window streaming kernel: every CTA the SMs can hold (occupancy), at
+// most one per item
+template <typename F>
+static int occ_grid(F fn, long long items) {
+    static int maxg = 0;
+    if (maxg == 0) maxg = max_coresident(reinterpret_cast<const void *>(fn), kThreads, 0);
+    long long g = maxg > 0 ? maxg : stream_grid(items);
+    if (items < g) g = items;
+    return g < 1 ? 1 : static_cast<int>(g);
+}
+
 cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s) {
     win_push_decide<<<1, 256, 0, s>>>(p);
-    if (grid <= 0) grid = stream_grid(static_cast<long long>(p.geo.k) * p.geo.T);
+    if (grid <= 0)
+        grid = p.dtype == 0 ? occ_grid(win_push_kernel<float>, static_cast<long long>(p.geo.k) * p.geo.T)
+                            : occ_grid(win_push_kernel<bf16>, static_cast<long long>(p.geo.k) * p.geo.T);
     if (p.dtype == 0)
         win_push_kernel<float><<<grid, kThreads, 0, s>>>(p);
     else
@@ -330,7 +343,9 @@ cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s) {
 
 cudaError_t launch_win_collect(const WinParams &p, int update, int grid, cudaStream_t s) {
     win_collect_decide<<<1, 256, 0, s>>>(p);
-    if (grid <= 0) grid = stream_grid(static_cast<long long>(p.geo.k) * p.geo.T);
+    if (grid <= 0)
+        grid = p.dtype == 0 ? occ_grid(win_collect_kernel<float>, static_cast<long long>(p.geo.k) * p.geo.T)
+                            : occ_grid(win_collect_kernel<bf16>, static_cast<long long>(p.geo.k) * p.geo.T);
     if (p.dtype == 0)
         win_collect_kernel<float><<<grid, kThreads, 0, s>>>(p, update);
     else

@@ -198,6 +198,19 @@ def exact_diffusion(W, X, G, Psi_prev, lr, wire_bf16=False):
     return Y, Pout
 
 
+def gradient_tracking_step(W, U, V, Y, Gprev, grad, lr):
+    """One round of push-sum gradient tracking (appendix),
+    written out with the oracle's W-mix (ora_mix) for every partial averaging:
+        u+ = W (u - lr y);  v+ = W v;  x+ = u+ / v+;  g+ = grad(x+);  y+ = W (y + g+ - g).
+    U, Y, Gprev: (n, d); V: (n, 1).  Returns (x+, u+, v+, y+, g+)."""
+    Un = mix(W, _f64(U) - lr * _f64(Y))
+    Vn = mix(W, _f64(V))
+    Xn = Un / Vn
+    Gn = _f64(grad(Xn))
+    Yn = mix(W, _f64(Y) + Gn - _f64(Gprev))
+    return Xn, Un, Vn, Yn, Gn
+
+
 def awc(W, X, G, lr):
     W, X, G = _f64(W), _f64(X), _f64(G)
     Y = np.zeros_like(X)

@@ -672,3 +672,50 @@ def test_exact_diffusion_reaches_exact_minimiser_on_gpu():
     err = np.abs(_np(x) - xs[None, :]).max()
     assert err < 1e-5 * np.abs(xs).max(), err   # the fp32 oracle reaches 3e-7 on this problem
     ctx.close()
+
+
+# ------------------------- push-sum gradient tracking from the fused primitives ---
+def test_gradient_tracking_matches_oracle_and_converges():
+    # appendix "Push-sum gradient tracking": 3 partial averagings per round, each a
+    # fused library call (algorithms.gradient_tracking_step), directed column-stochastic W
+    from paper_2111_04287_b200.algorithms import gradient_tracking_step
+    n, m, d, lr = 5, 10, 4, 0.05
+    rng = np.random.default_rng(8)
+    A = rng.standard_normal((n, m, d)) / np.sqrt(m)
+    b = rng.standard_normal((n, m))
+    xs = np.linalg.lstsq(A.reshape(n * m, d), b.reshape(n * m), rcond=None)[0]
+    Adj = np.eye(n, dtype=bool)
+    r2 = np.random.default_rng(2)
+    for i in range(n):
+        Adj[(i + 1) % n, i] = True
+        for j in r2.choice(n, 2, replace=False):
+            Adj[j, i] = True
+    W = Adj / Adj.sum(axis=0, keepdims=True)
+    ctx = _ctx(n)
+    ctx.set_topology(W)
+    At = torch.from_numpy(A).cuda()
+    bt = torch.from_numpy(b).cuda()
+
+    def grad_gpu(X):   # fp64 GEMV plumbing, fp32 result
+        X64 = X.double()
+        return torch.bmm(At.transpose(1, 2), (torch.bmm(At, X64.unsqueeze(2)).squeeze(2) - bt).unsqueeze(2)) \
+            .squeeze(2).float().contiguous()
+    grad_np = lambda X: np.einsum("imd,im->id", A, np.einsum("imd,id->im", A, X) - b)
+    u = torch.zeros(n, d, device="cuda")
+    v = torch.ones(n, 1, device="cuda")
+    g = grad_gpu(u / v)
+    y = g.clone()
+    # step-by-step parity: the GPU state is fed to the oracle every round
+    for _ in range(5):
+        U, V, Y, Gp = _np(u), _np(v), _np(y), _np(g)
+        x, u, v, y, g = gradient_tracking_step(ctx, u, v, y, g, grad_gpu, lr)
+        torch.cuda.synchronize()
+        Xr, Ur, Vr, Yr, Gr = ora.gradient_tracking_step(W, U, V, Y, Gp, grad_np, lr)
+        assert np.allclose(_np(v), Vr, rtol=1e-6, atol=0)
+        assert np.allclose(_np(u), Ur, rtol=1e-5, atol=1e-6)
+        assert np.allclose(_np(y), Yr, rtol=1e-4, atol=1e-6)
+    for _ in range(3000):
+        x, u, v, y, g = gradient_tracking_step(ctx, u, v, y, g, grad_gpu, lr)
+    torch.cuda.synchronize()
+    assert np.abs(_np(x) - xs[None, :]).max() < 1e-4 * np.abs(xs).max()
+    ctx.close()

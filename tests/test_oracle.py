@@ -483,3 +483,35 @@ def test_exact_diffusion_special_cases():
     Y2, _ = ora.exact_diffusion(W, X, G, P, lr)
     phi = psi + X - P
     assert np.allclose(Y2.sum(axis=0), phi.sum(axis=0), rtol=0, atol=1e-6)
+
+
+# ------------------------------- push-sum gradient tracking (appendix listing) ---
+def _column_stochastic_directed(n, seed=2):
+    # directed, strongly connected (ring i -> i+1 plus random extra edges), push weights
+    # 1 / (out-degree + 1) on every out-edge and on the self loop: column-stochastic only
+    rng = np.random.default_rng(seed)
+    A = np.eye(n, dtype=bool)
+    for i in range(n):
+        A[(i + 1) % n, i] = True
+        for j in rng.choice(n, 2, replace=False):
+            A[j, i] = True
+    W = A / A.sum(axis=0, keepdims=True)
+    return W
+
+
+def test_gradient_tracking_invariants_and_convergence():
+    n, m, d = 5, 10, 4
+    A, b, xs = _lsq_problem(n, m, d, seed=8)
+    W = _column_stochastic_directed(n)
+    assert np.allclose(W.sum(axis=0), 1.0) and not np.allclose(W.sum(axis=1), 1.0)
+    grad = lambda X: np.einsum("imd,im->id", A, np.einsum("imd,id->im", A, X) - b)
+    U = np.zeros((n, d)); V = np.ones((n, 1))
+    G = grad(U / V); Y = G.copy()          # y^(0) = g^(0)
+    lr = 0.05
+    for _ in range(3000):
+        X, U, V, Y, G = ora.gradient_tracking_step(W, U, V, Y, G, grad, lr)
+        # column-stochastic W: sum_i v_i = n, and y tracks the sum of the gradients
+        assert abs(V.sum() - n) < 1e-9
+        assert np.allclose(Y.sum(axis=0), G.sum(axis=0), rtol=0, atol=1e-9)
+    assert np.abs(X - xs[None, :]).max() < 1e-8      # exact convergence on a directed graph
+    assert np.abs(V - 1).max() > 1e-2                 # and the push-sum weights really matter

@@ -68,7 +68,14 @@ template <typename XT>
 struct FusedVec {
     static constexpr int V = sizeof(XT) >= 4 ? 4 : 8;
 };
-constexpr int kNSlot = 16;                 // remote-tile ring slots per CTA
+#ifndef BF_RING_KB
+#define BF_RING_KB 64
+#endif
+// remote-tile ring: BF_RING_KB of shared memory per CTA (2 CTAs per SM fit), as
+// many slots as tiles fit -- 16 fp32, 32 bf16 tiles of 1024 elements (measured: a
+// 96 KB ring changed nothing for exp-2 and slowed one-peer at N = 2 by 4%)
+constexpr int kRingBytes = BF_RING_KB * 1024;
+constexpr int kMaxSlot = 64;
 #ifndef BF_LEAD
 #define BF_LEAD 24
 #endif
@@ -109,6 +116,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     constexpr int V = FusedVec<XT>::V;         // elements per thread-vector (16-byte x accesses)
     constexpr int kSubT = kThreads * V;        // elements per sub-item
     constexpr unsigned kSlotBytes = kSubT * sizeof(WT);
+    constexpr int kNSlot = kRingBytes / kSlotBytes < kMaxSlot ? kRingBytes / kSlotBytes : kMaxSlot;
     extern __shared__ __align__(128) unsigned char ring[];
     __shared__ SharedTab st;
     __shared__ LocalMix<K> lm;
@@ -489,11 +497,11 @@ static cudaError_t launch_fused_k(const ExchParams &p, int grid, cudaStream_t s)
     const bool ringed = FusedCfg<K>::kRing && p.geo.nprocs > 1;
     if (!FusedCfg<K>::kRing && p.geo.nprocs > 1) return cudaErrorInvalidValue;
     constexpr int kSubT = kThreads * FusedVec<XT>::V;
-    const unsigned smem = ringed ? kNSlot * kSubT * sizeof(WT) : 0;
+    const unsigned smem = ringed ? kRingBytes : 0;
     static int maxg[2] = {0, 0};   // co-resident CTAs of this instantiation (queried once per smem size)
     if (maxg[ringed] == 0) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kNSlot * kSubT * sizeof(WT));
+                                             kRingBytes);
         if (e != cudaSuccess) return e;
         maxg[ringed] = max_coresident(fn, FusedCfg<K>::kThreadsPerCta, smem);
     }

@@ -184,6 +184,23 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *ctx, const void *x, void *y
 bf_status bf_win_create(bf_ctx *ctx, const char *name, void *x, size_t count, bf_dtype dtype,
                         int zero_init, int with_p);
 bf_status bf_win_free(bf_ctx *ctx, const char *name);
+/* Symmetric-heap allocation (collective: same sizes in the same order on every
+ * process, so the block has the same offset in every heap).  *ptr receives a
+ * device pointer that stays valid until bf_finalize; never freed separately.
+ * BF_ERR_NOMEM when the heap is exhausted. */
+bf_status bf_alloc(bf_ctx *ctx, size_t bytes, void **ptr);
+/* neighbor_win_get (reading R26): for every local agent in agent_mask
+ * (0 = all) and every in-neighbour j at window creation selected by weights[a]
+ * (src ranks + weights; self_weight required by the view rules but ignored;
+ * NULL = every in-neighbour with weight 1), copy weight * x_j -- j's window
+ * tensor as it is in memory now -- into this agent's slot for j and release a
+ * new version, so bf_win_update sees it as the latest payload.  The window
+ * tensor must live in the symmetric heap (bf_alloc), because other processes
+ * read it; else BF_ERR_UNSUPPORTED.  Stream-ordered, one-sided (no call on the
+ * owners).  Mixing get with put / accumulate on the same window is a race (as
+ * with MPI windows without a mutex). */
+bf_status bf_win_get(bf_ctx *ctx, const char *name, const bf_weights *weights, uint64_t agent_mask,
+                     void *stream);
 /* Error feedback for a bf16 window (reading R24 in DESIGN.md; not in the
  * paper).  Payloads travel in the window dtype, so a bf16 payload is rounded
  * (RNE) like BlueFog's MPI window in the tensor dtype; with enable != 0 the

@@ -80,6 +80,8 @@ _SIGS = {
     "bf_kernel_launches": (_u64, [_vp]),
     "bf_exchange_stats": (_i, [_vp, C.POINTER(_u64), _sz, _i]),
     "bf_win_set_error_feedback": (_i, [_vp, C.c_char_p, _i]),
+    "bf_alloc": (_i, [_vp, _sz, C.POINTER(_vp)]),
+    "bf_win_get": (_i, [_vp, C.c_char_p, _wp, _u64, _vp]),
     "bf_exact_diffusion_step": (_i, [_vp, _vp, _vp, _i, _vp, _sz, C.c_float, _i, _wp, _vp]),
 }
 

@@ -279,6 +279,37 @@ class Context:
                                      _DT[tensor.dtype], 1 if zero_init else 0, 1 if with_p else 0))
         return True
 
+    def alloc(self, shape, dtype: torch.dtype = torch.float32) -> torch.Tensor:
+        """A tensor in the symmetric heap (collective, bf_alloc): windows created on
+        it can be read by the neighbours (win_get)."""
+        shape = tuple(int(d) for d in shape)
+        nbytes = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+        ptr = C.c_void_p()
+        check(self.lib.bf_alloc(self.h, nbytes, C.byref(ptr)))
+
+        class _HeapBlock:   # __cuda_array_interface__ view; the heap owns the memory
+            pass
+        blk = _HeapBlock()
+        typestr = {torch.float32: "<f4", torch.bfloat16: "<V2"}[dtype]
+        blk.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr.value, False),
+                                        "version": 2, "strides": None}
+        if dtype == torch.bfloat16:   # no bf16 typestr: wrap as int16 and reinterpret
+            blk.__cuda_array_interface__["typestr"] = "<i2"
+            t = torch.as_tensor(blk, device=f"cuda:{self.device}").view(torch.bfloat16)
+        else:
+            t = torch.as_tensor(blk, device=f"cuda:{self.device}")
+        return t
+
+    def win_get(self, name: str, src_weights=None, agent_mask: int = 0, stream=None) -> bool:
+        """neighbor_win_get: fetch weight * x_j of the selected in-neighbours into
+        this agent's slots (the window tensor must come from alloc())."""
+        v = None
+        if src_weights is not None:
+            v = _Views(self.k, [1.0] * self.k, src_weights, None)
+        check(self.lib.bf_win_get(self.h, name.encode(), v.ptr() if v else None, int(agent_mask),
+                                  _stream_ptr(stream)))
+        return True
+
     def win_set_error_feedback(self, name: str, enable: bool = True) -> bool:
         """bf16 windows: keep the wire rounding residual in the sender's outbox (R24)."""
         check(self.lib.bf_win_set_error_feedback(self.h, name.encode(), 1 if enable else 0))

@@ -184,6 +184,7 @@ cudaError_t launch_hier(const HierParams &p, int x_kind, int grid, cudaStream_t 
 cudaError_t launch_barrier(const Geometry &geo, unsigned long long epoch, cudaStream_t s);
 cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s);
 cudaError_t launch_win_collect(const WinParams &p, int update, int grid, cudaStream_t s);
+cudaError_t launch_win_get(const WinParams &p, unsigned long long x_off, cudaStream_t s);
 cudaError_t launch_fill_uniform(void *dst, int kind, size_t count, unsigned long long seed,
                                 unsigned long long offset, float scale, cudaStream_t s);
 cudaError_t launch_set_u64(unsigned long long *dst, unsigned long long v, cudaStream_t s);

@@ -1109,6 +1109,53 @@ static bf_status win_pull(bf_ctx *c, const char *name, const bf_weights *weights
     return BF_OK;
 }
 
+bf_status bf_alloc(bf_ctx *c, size_t bytes, void **ptr) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!ptr || bytes == 0) return fail(BF_ERR_ARG, "bad allocation request");
+    unsigned long long off;
+    if ((s = heap_alloc(c, bytes, &off))) return s;
+    *ptr = c->heap + off;
+    return BF_OK;
+}
+
+bf_status bf_win_get(bf_ctx *c, const char *name, const bf_weights *weights, uint64_t agent_mask, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    Window *w = find_win(c, name);
+    if (!w) return fail(BF_ERR_WINDOW, "unknown window '%s'", name ? name : "(null)");
+    const char *xp = static_cast<const char *>(w->x);
+    if (xp < c->heap || xp + w->count * c->k * (w->dtype == BF_BFLOAT16 ? 2 : 4) > c->heap + c->heap_bytes)
+        return fail(BF_ERR_UNSUPPORTED, "win_get reads the neighbours' window tensors: create the window on a "
+                                        "tensor allocated with bf_alloc (symmetric heap)");
+    WinParams p;
+    win_setup(c, w, agent_mask, p);
+    for (int b = 0; b < c->k; ++b) {
+        const int gid = c->proc * c->k + b;
+        const auto &ins = w->side[gid].in;
+        p.nin[b] = static_cast<unsigned char>(ins.size());
+        for (size_t q = 0; q < ins.size(); ++q) {
+            p.in_src[b][q] = static_cast<unsigned char>(ins[q]);
+            p.in_r[b][q] = weights ? 0.f : 1.f;   // default: every in-neighbour, weight 1
+        }
+        if (weights) {
+            const bf_weights &v = weights[b];
+            s = validate_view(c, gid, v, true, false, c->n);
+            if (s) return s;
+            for (int q = 0; q < v.n_src; ++q) {
+                auto it = std::find(ins.begin(), ins.end(), v.src_ranks[q]);
+                if (it == ins.end())
+                    return fail(BF_ERR_WINDOW, "agent %d: src %d is not an in-neighbour at window creation", gid,
+                                v.src_ranks[q]);
+                p.in_r[b][it - ins.begin()] = static_cast<float>(v.src_weights[q]);
+            }
+        }
+    }
+    CU(launch_win_get(p, static_cast<unsigned long long>(xp - c->heap), static_cast<cudaStream_t>(stream)));
+    c->launches += 2;
+    return BF_OK;
+}
+
 bf_status bf_win_update(bf_ctx *c, const char *name, const bf_weights *weights, void *out, uint64_t agent_mask,
                         void *stream) {
     return win_pull(c, name, weights, out, agent_mask, 1, stream);

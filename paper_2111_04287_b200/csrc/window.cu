@@ -309,6 +309,62 @@ __global__ void __launch_bounds__(kThreads) win_collect_kernel(const __grid_cons
     }
 }
 
+// ---- neighbor_win_get: pull the in-neighbours' window tensors ---------
+// Needs the window tensor in the symmetric heap (bf_alloc): agent j's tensor is
+// then at peer_base[j / k] + x_off + (j % k) * count * es in every process.
+// For each selected in-neighbour (in_r[a][q] != 0): my slot (a, q), half
+// version & 1, <- in_r * x_j; win_get_finish then releases version + 1, so
+// win_update sees the fetched value as the latest complete payload (R26).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) win_get_kernel(const __grid_constant__ WinParams p,
+                                                           unsigned long long x_off) {
+    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV;
+    const Geometry &g = p.geo;
+    const unsigned long long me = g.peer_base[g.me];
+    const long long count = g.count;
+    const bool vec = g.vec_ok != 0;
+    const int k = g.k;
+    const unsigned long long *ver = at<unsigned long long>(me, p.version_off);
+    const long long items = static_cast<long long>(k) * g.T;
+    for (long long w = blockIdx.x; w < items; w += gridDim.x) {
+        const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        if (!active(p, a)) continue;
+        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        for (int q = 0; q < p.nin[a]; ++q) {
+            const float r = p.in_r[a][q];
+            if (r == 0.f) continue;
+            const int j = p.in_src[a][q];
+            const int ci = a * p.maxdin + q;
+            const T *xj = at<const T>(g.peer_base[j / k], x_off + static_cast<unsigned long long>(j % k) * count *
+                                                                 esize(p)) + base;
+            T *slot = at<T>(me, p.slot_off + (static_cast<unsigned long long>(ci) * 2 + (ver[ci] & 1ull)) * p.cpad *
+                                                 esize(p)) + base;
+            float v[NV][V];
+#pragma unroll
+            for (int jv = 0; jv < NV; ++jv)
+                VecN<T, V>::load_cg(xj + win_elem<V>(jv), v[jv], clamp_valid_v<V>(rem, win_elem<V>(jv)), vec);
+#pragma unroll
+            for (int jv = 0; jv < NV; ++jv) {
+#pragma unroll
+                for (int i = 0; i < V; ++i) v[jv][i] *= r;
+                VecN<T, V>::store(slot + win_elem<V>(jv), v[jv], clamp_valid_v<V>(rem, win_elem<V>(jv)), vec);
+            }
+        }
+    }
+}
+
+__global__ void win_get_finish(const __grid_constant__ WinParams p) {
+    const Geometry &g = p.geo;
+    const unsigned long long me = g.peer_base[g.me];
+    __threadfence();   // every slot store of the copy kernel (stream-ordered before) is visible
+    for (int idx = threadIdx.x; idx < g.k * kMaxS; idx += blockDim.x) {
+        const int a = idx / kMaxS, q = idx % kMaxS;
+        if (!active(p, a) || q >= p.nin[a] || p.in_r[a][q] == 0.f) continue;
+        unsigned long long *v = at<unsigned long long>(me, p.version_off) + a * p.maxdin + q;
+        st_release_gpu(v, *v + 1);
+    }
+}
+
 static int stream_grid(long long items) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -338,6 +394,16 @@ cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s) {
         win_push_kernel<float><<<grid, kThreads, 0, s>>>(p);
     else
         win_push_kernel<bf16><<<grid, kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_win_get(const WinParams &p, unsigned long long x_off, cudaStream_t s) {
+    const long long items = static_cast<long long>(p.geo.k) * p.geo.T;
+    if (p.dtype == 0)
+        win_get_kernel<float><<<occ_grid(win_get_kernel<float>, items), kThreads, 0, s>>>(p, x_off);
+    else
+        win_get_kernel<bf16><<<occ_grid(win_get_kernel<bf16>, items), kThreads, 0, s>>>(p, x_off);
+    win_get_finish<<<1, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 

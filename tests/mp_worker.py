@@ -128,6 +128,27 @@ def main():
         torch.cuda.synchronize()
         check(f"hier L={L}", np_(y), ora.hier(WM, L, X), np.kron(WM, np.full((L, L), 1.0 / L)), X, 1e-6)
 
+    # ---- neighbor_win_get on a symmetric-heap tensor (reads over NVLink) ------------
+    Wst = ora.exp2(n)
+    ctx.set_topology(Wst)
+    Xg = np.stack([synthetic.uniform(synthetic.SEED_X0 + 50 + r, 7001) for r in range(n)]).astype(np.float32)
+    xg = ctx.alloc((k, 7001))
+    xg.copy_(torch.from_numpy(Xg[rows]))
+    ctx.win_create(xg, "get", zero_init=True)
+    torch.cuda.synchronize()
+    dist.barrier()   # every owner's tensor is in place before anybody reads it
+    ins = [[j for j in range(n) if j != i and Wst[i, j] != 0] for i in range(n)]
+    ctx.win_get("get", src_weights=[{j: 0.5 for j in ins[r0 + a]} for a in range(k)])
+    outg = torch.empty_like(xg)
+    ctx.win_update("get", self_weight=[0.0] * k, src_weights=[{j: 1.0 for j in ins[r0 + a]} for a in range(k)],
+                   out=outg)
+    torch.cuda.synchronize()
+    Wg = 0.5 * (Wst != 0)
+    np.fill_diagonal(Wg, 0.0)
+    check("win_get", np_(outg), ora.mix(Wg, Xg.astype(np.float64)), Wg, Xg.astype(np.float64), 1e-6)
+    dist.barrier()
+    ctx.win_free("get")
+
     # ---- windows: synchronous push-sum ------------------------------------------
     Wst = ora.exp2(n)
     ctx.set_topology(Wst)

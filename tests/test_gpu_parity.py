@@ -719,3 +719,50 @@ def test_gradient_tracking_matches_oracle_and_converges():
     torch.cuda.synchronize()
     assert np.abs(_np(x) - xs[None, :]).max() < 1e-4 * np.abs(xs).max()
     ctx.close()
+
+
+# ------------------------------------------------ neighbor_win_get (R26) ---
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_window_get(dtype):
+    Wst = _fig2_static()
+    n = Wst.shape[0]
+    count = 10007
+    ctx = _ctx(n)
+    ctx.set_topology(Wst)
+    x = ctx.alloc((n, count), dtype)                       # symmetric heap: readable by the neighbours
+    x.copy_(_gpu(synthetic.agents_x0(n, count), dtype))
+    X = _np(x)
+    ctx.win_create(x, "g", zero_init=True)
+    rng = np.random.default_rng(3)
+    ins = [[j for j in range(n) if j != i and Wst[i, j] != 0] for i in range(n)]
+    Wg = np.zeros((n, n))
+    views = []
+    for i in range(n):
+        sel = {j: float(rng.uniform(0.1, 1.0)) for j in ins[i] if rng.random() < 0.8}
+        for j, w in sel.items():
+            Wg[i, j] = w
+        views.append(sel)
+    ctx.win_get("g", src_weights=views)
+    out = torch.empty_like(x)
+    # win_update with self 0 and unit weights: out_i = sum_j (fetched w_ij x_j)
+    ctx.win_update("g", self_weight=[0.0] * n, src_weights=[{j: 1.0 for j in views[i]} for i in range(n)], out=out)
+    torch.cuda.synchronize()
+    ref = ora.mix(Wg, X)
+    tol = 1e-6 if dtype == torch.float32 else 2e-2
+    assert_parity(_np(out), ref, Wg, X, tol)
+    # default: every in-neighbour, weight 1
+    ctx.win_get("g")
+    ctx.win_update("g", self_weight=[0.0] * n, src_weights=[{j: 1.0 for j in ins[i]} for i in range(n)], out=out)
+    torch.cuda.synchronize()
+    W1 = (Wst != 0).astype(np.float64)
+    np.fill_diagonal(W1, 0.0)
+    assert_parity(_np(out), ora.mix(W1, X), W1, X, tol)
+    ctx.win_free("g")
+    # a window on memory outside the heap cannot be read by the neighbours
+    y = _gpu(synthetic.agents_x0(n, 64), dtype)
+    ctx.win_create(y, "h", zero_init=True)
+    with pytest.raises(BluefogError) as ei:
+        ctx.win_get("h")
+    assert ei.value.name == "BF_ERR_UNSUPPORTED"
+    ctx.win_free("h")
+    ctx.close()

@@ -20,6 +20,9 @@
  * "wait" = synchronize the stream).  Caller-owned buffers must stay valid
  * until the stream work completes; the library never frees them.
  *
+ * Empty inputs.  A data call with count == 0 returns BF_OK without checking its
+ * pointers and without enqueueing anything (the epoch does not advance).
+ *
  * Errors.  Every function returns a bf_status.  Host-side validation is
  * synchronous and enqueues nothing on failure.  Device-side faults (a spin
  * that exceeded BF_TIMEOUT_MS, a topology-check mismatch) are latched in the

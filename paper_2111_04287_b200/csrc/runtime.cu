@@ -699,6 +699,7 @@ bf_status bf_neighbor_allreduce(bf_ctx *c, const void *x, void *y, size_t count,
                                 const bf_weights *weights, void *stream) {
     bf_status s = check_ctx(c);
     if (s) return s;
+    if (count == 0) return BF_OK;   // empty input: nothing to exchange, no kernel
     if (!x || !y) return fail(BF_ERR_ARG, "null tensor");
     if (dtype != BF_FLOAT32 && dtype != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
     return exchange_common(c, x, nullptr, y, nullptr, count, dtype, dtype, dtype, dtype, 0.f, weights,
@@ -709,6 +710,7 @@ bf_status bf_atc_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, size
                       void *x_bf16_shadow, const bf_weights *weights, void *stream) {
     bf_status s = check_ctx(c);
     if (s) return s;
+    if (count == 0) return BF_OK;   // empty input: nothing to exchange, no kernel
     if (!x || !g) return fail(BF_ERR_ARG, "null tensor");
     if ((g_dtype != BF_FLOAT32 && g_dtype != BF_BFLOAT16) || (wire != BF_FLOAT32 && wire != BF_BFLOAT16))
         return fail(BF_ERR_UNSUPPORTED, "dtype");
@@ -741,6 +743,7 @@ bf_status bf_awc_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, size
                       const bf_weights *weights, void *stream) {
     bf_status s = check_ctx(c);
     if (s) return s;
+    if (count == 0) return BF_OK;   // empty input: nothing to exchange, no kernel
     if (!x || !g) return fail(BF_ERR_ARG, "null tensor");
     if (g_dtype != BF_FLOAT32 && g_dtype != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
     if (!std::isfinite(lr)) return fail(BF_ERR_ARG, "non-finite lr");
@@ -753,6 +756,7 @@ bf_status bf_exact_diffusion_step(bf_ctx *c, float *x, const void *g, bf_dtype g
                                   float lr, bf_dtype wire, const bf_weights *weights, void *stream) {
     bf_status s = check_ctx(c);
     if (s) return s;
+    if (count == 0) return BF_OK;   // empty input: nothing to exchange, no kernel
     if (!x || !g || !psi) return fail(BF_ERR_ARG, "null tensor");
     if ((g_dtype != BF_FLOAT32 && g_dtype != BF_BFLOAT16) || (wire != BF_FLOAT32 && wire != BF_BFLOAT16))
         return fail(BF_ERR_UNSUPPORTED, "dtype");
@@ -767,6 +771,7 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
                                              const bf_weights *machine_weights, void *stream) {
     bf_status s = check_ctx(c);
     if (s) return s;
+    if (count == 0) return BF_OK;   // empty input: nothing to exchange, no kernel
     if (!x || !y) return fail(BF_ERR_ARG, "null tensor");
     if (dtype != BF_FLOAT32 && dtype != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
     if (!c->machine_L) return fail(BF_ERR_STATE, "bf_set_machine_topology has not been called");

@@ -766,3 +766,24 @@ def test_window_get(dtype):
     assert ei.value.name == "BF_ERR_UNSUPPORTED"
     ctx.win_free("h")
     ctx.close()
+
+
+def test_empty_inputs_are_noops():
+    # count = 0 (an empty layer, a ragged split): every data call returns without
+    # launching a kernel and without touching the epoch (the next call still works)
+    n = 4
+    ctx = _ctx(n)
+    ctx.set_topology(ora.ring(n))
+    e = torch.empty(n, 0, device="cuda")
+    l0 = ctx.kernel_launches()
+    ctx.neighbor_allreduce(e)
+    ctx.atc_step(e, e, 0.1)
+    ctx.awc_step(e, e, 0.1)
+    ctx.exact_diffusion_step(e, e, e.clone(), 0.1)
+    torch.cuda.synchronize()
+    assert ctx.kernel_launches() == l0
+    x, X = _inputs(n, 4097)
+    y = ctx.neighbor_allreduce(x)
+    torch.cuda.synchronize()
+    assert_parity(_np(y), ora.mix(ora.ring(n), X), ora.ring(n), X, 1e-6)
+    ctx.close()

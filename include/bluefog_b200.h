@@ -92,7 +92,13 @@ typedef struct {
  * `agents_per_proc` agents on CUDA device `cuda_device`, with a symmetric
  * heap of `heap_bytes` device bytes (exchange slots, windows, hierarchical
  * buffers and signal pads all live there; it is exported through CUDA IPC).
- * Env: BF_TIMEOUT_MS (default 10000) bounds every device wait. */
+ * Env: BF_TIMEOUT_MS (default 10000) bounds every device wait.  Tuning /
+ * diagnostics (read at bf_init): BF_EXCH=chunk forces the chunked exchange
+ * kernel (default: the local-agent fused kernel where instantiated,
+ * agents_per_proc 1, 2, 4, or 8 on one GPU), BF_FUSED_GRID (CTAs of the fused
+ * kernel), BF_HIER=staged (sliced hierarchical kernel also on one GPU),
+ * BF_WIN_EF=1 (error feedback on for new bf16 windows), BF_STATS=1 (per-CTA
+ * timings, bf_exchange_stats, with a -DBF_STATS=1 build). */
 bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_device,
                   size_t heap_bytes, bf_ctx **out);
 /* Bootstrap: each process writes its blob (<= bf_ipc_blob_size() bytes) and the

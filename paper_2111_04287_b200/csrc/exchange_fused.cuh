@@ -135,12 +135,14 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     if (threadIdx.x == 0) {
         s_fail = 0;
         s_released = 0;
-        for (int i = 0; i < kNSlot; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kThreads / 32);
+        if (sys) {   // the ring and the publish barriers exist only across processes
+            for (int i = 0; i < kNSlot; ++i) {
+                mbar_init(&full[i], 1);
+                mbar_init(&empty[i], kThreads / 32);
+            }
+            for (int i = 0; i < kPubRing; ++i) mbar_init(&pubbar[i], kThreads);   // every consumer thread arrives
+            fence_mbar_init();
         }
-        for (int i = 0; i < kPubRing; ++i) mbar_init(&pubbar[i], kThreads);   // every consumer thread arrives
-        fence_mbar_init();
     }
     bool ok = war_wait(g, e);
     if (p.wmode == kWDynamic) write_descriptors(p, e);

@@ -113,9 +113,7 @@ struct ExchParams {
     unsigned pub_mask;                      // kernel 3, kWStatic: local agents read by another process
     unsigned long long prog_off;            // kernel 3: u64 [kMaxGrid] per-CTA publish progress
     unsigned long long *stats;              // kernel 3 built with BF_STATS=1: u64 [grid][8] (diagnostics)
-    float *scratch;                         // kernel 3, bf16 y across processes: fp32 partial sums [k][count]
     float *psi;                             // kernel 3 MODE 3 (Exact-Diffusion): psi state [k][count], in place
-    int lag;                                // kernel 3: phase-B lag in sub-items (0 = automatic)
     SrcTab tab;                             // kWStatic: final coefficients; kWDynamic: declared r
     DynDecl dyn;
 };

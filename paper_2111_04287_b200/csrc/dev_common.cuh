@@ -613,6 +613,16 @@ struct VecN<float, 8> {
         Vec4<float>::store(p, v, valid < 4 ? valid : 4, vec);
         Vec4<float>::store(p + 4, v + 4, valid > 4 ? valid - 4 : 0, vec);
     }
+    static __device__ __forceinline__ void load_hint(const float *p, float v[8], int valid, bool vec,
+                                                     unsigned long long pol) {
+        Vec4<float>::load_hint(p, v, valid < 4 ? valid : 4, vec, pol);
+        Vec4<float>::load_hint(p + 4, v + 4, valid > 4 ? valid - 4 : 0, vec, pol);
+    }
+    static __device__ __forceinline__ void store_hint(float *p, const float v[8], int valid, bool vec,
+                                                      unsigned long long pol) {
+        Vec4<float>::store_hint(p, v, valid < 4 ? valid : 4, vec, pol);
+        Vec4<float>::store_hint(p + 4, v + 4, valid > 4 ? valid - 4 : 0, vec, pol);
+    }
 };
 
 // valid elements of the V-vector at offset e of a row with `rem` elements left

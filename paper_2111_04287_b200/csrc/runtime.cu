@@ -105,9 +105,6 @@ struct bf_ctx {
     unsigned long long bar_epoch = 0;
     unsigned long long launches = 0;
     unsigned long long *stats = nullptr;      // BF_STATS=1: per-CTA diagnostics of the fused kernel
-    void *scratch = nullptr;                  // fused kernel, bf16 outputs across GPUs: fp32 partial sums
-    size_t scratch_bytes = 0;
-    int lag = 0;                              // BF_FUSED_LAG (0 = automatic)
     bool hier_staged = false;                 // BF_HIER=staged: always the staged hierarchical kernel
     bool win_ef = false;                      // BF_WIN_EF=1: new windows start with error feedback on
 };
@@ -418,7 +415,6 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     if (const char *x = getenv("BF_EXCH"))
         c->exch_kernel = strcmp(x, "chunk") == 0 ? 2 : 3;
     if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
-    if (const char *x = getenv("BF_FUSED_LAG")) c->lag = std::max(0, atoi(x));
     if (const char *x = getenv("BF_HIER")) c->hier_staged = strcmp(x, "staged") == 0;
     if (const char *x = getenv("BF_WIN_EF")) c->win_ef = atoi(x) != 0;
     if (const char *x = getenv("BF_STATS"))
@@ -499,7 +495,6 @@ bf_status bf_finalize(bf_ctx *c) {
     if (c->stage_x) cudaFree(c->stage_x);
     if (c->stage_g) cudaFree(c->stage_g);
     if (c->stats) cudaFree(c->stats);
-    if (c->scratch) cudaFree(c->scratch);
     if (c->h_err) cudaFreeHost(const_cast<unsigned int *>(c->h_err));
     delete c;
     return BF_OK;
@@ -676,18 +671,12 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     p.ccnt_off = c->ccnt_off;
     p.prog_off = c->prog_off;
     p.stats = c->stats;
-    p.lag = c->lag;
     if (psi) {   // Exact-Diffusion: only the fused kernel implements MODE 3
         if (p.kernel != 3)
             return fail(BF_ERR_UNSUPPORTED, "Exact-Diffusion needs the fused exchange kernel (agents_per_proc 1, 2, 4 "
                                             "or 8 on one GPU)");
         if (!aligned16(psi)) p.geo.vec_ok = 0;
         p.psi = psi;
-    }
-    if (p.kernel == 3 && c->nprocs > 1 && y_kind != 0) {   // fp32 partial sums of a bf16 output
-        s = ensure_stage(&c->scratch, &c->scratch_bytes, static_cast<size_t>(c->k) * count * 4);
-        if (s) return s;
-        p.scratch = static_cast<float *>(c->scratch);
     }
     p.cflag_off = c->cflag_off;
     CU(launch_exchange(p, x_kind, awc_g ? x_kind : g_kind, wire_kind, y_kind, g != nullptr, 0, st));

@@ -46,6 +46,8 @@ def lib():
         L.ora_full.argtypes = [C.c_int, _dp]
         L.ora_one_peer_exp2.argtypes = [C.c_int, C.c_longlong, _dp]
         L.ora_one_peer_exp2_peers.argtypes = [C.c_int, C.c_longlong, C.c_int, _ip, _ip]
+        L.ora_inner_outer_exp2.argtypes = [C.c_int, C.c_int, C.c_longlong, _dp]
+        L.ora_inner_outer_exp2_peers.argtypes = [C.c_int, C.c_int, C.c_longlong, C.c_int, _ip, _ip]
         L.ora_in_neighbors.argtypes = [C.c_int, _dp, C.c_int, _ip]
         L.ora_out_neighbors.argtypes = [C.c_int, _dp, C.c_int, _ip]
         L.ora_classify.argtypes = [C.c_int, _dp, C.c_double]
@@ -108,6 +110,19 @@ def one_peer_exp2(n, k):
 def one_peer_exp2_peers(n, k, i):
     s, d = C.c_int(), C.c_int()
     lib().ora_one_peer_exp2_peers(n, int(k), i, C.byref(s), C.byref(d))
+    return s.value, d.value
+
+
+def inner_outer_exp2(n, local_size, k):
+    """Inner-outer dynamic exp-2 graph at round k (reading R27)."""
+    if local_size < 1 or n % local_size:
+        raise ValueError("machines must tile the agents")
+    return _topo(lib().ora_inner_outer_exp2, n, int(local_size), int(k))
+
+
+def inner_outer_exp2_peers(n, local_size, k, i):
+    s, d = C.c_int(), C.c_int()
+    lib().ora_inner_outer_exp2_peers(n, int(local_size), int(k), i, C.byref(s), C.byref(d))
     return s.value, d.value
 
 

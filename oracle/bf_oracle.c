@@ -81,6 +81,51 @@ void ora_one_peer_exp2(int n, long long k, double *W) {
     }
 }
 
+/* Inner-outer dynamic exponential-2 graph (named, not defined, in P:828 and
+ * the caption at P:869; reading R27).  n agents on M = n / L machines of L.
+ * At round k one local rank per machine, o = k mod L, talks OUTSIDE: agent
+ * (m, o) pulls from machine m - 2^t (same local rank o) and pushes to m + 2^t,
+ * t = (k div L) mod ceil(log2 M).  The other L - 1 agents of the machine talk
+ * INSIDE: relabelled r = (l - o - 1) mod L in [0, L - 2], they run the one-peer
+ * exp-2 rule over a group of L - 1, t' = k mod ceil(log2(L - 1)), and map back
+ * l = (r + o + 1) mod L.  A group of one has no peer (self weight 1). */
+void ora_inner_outer_exp2_peers(int n, int L, long long k, int i, int *src, int *dst) {
+    int M = n / L, m = i / L, l = i % L;
+    int o = (int)(k % L);
+    *src = -1;
+    *dst = -1;
+    if (l == o) {
+        int tau = ceil_log2(M);
+        if (tau == 0) return;
+        int off = 1 << (int)((k / L) % tau);
+        *src = ((m - off) % M + M) % M * L + o;
+        *dst = (m + off) % M * L + o;
+    } else {
+        int G = L - 1;
+        int tau = ceil_log2(G);
+        if (tau == 0) return;
+        int off = 1 << (int)(k % tau);
+        int r = ((l - o - 1) % L + L) % L;
+        int rs = ((r - off) % G + G) % G, rd = (r + off) % G;
+        *src = m * L + (rs + o + 1) % L;
+        *dst = m * L + (rd + o + 1) % L;
+    }
+}
+
+void ora_inner_outer_exp2(int n, int L, long long k, double *W) {
+    memset(W, 0, sizeof(double) * (size_t)n * n);
+    for (int i = 0; i < n; ++i) {
+        int src, dst;
+        ora_inner_outer_exp2_peers(n, L, k, i, &src, &dst);
+        if (src < 0) {
+            W[i * n + i] = 1.0;
+        } else {
+            W[i * n + i] = 0.5;
+            W[i * n + src] += 0.5;
+        }
+    }
+}
+
 /* ========================================================================
  * Neighbour sets, Eq. 6-7: N(i) = {j : (j,i) in E},
  * M(i) = {j : (i,j) in E}; E = {(j,i) : w_ij != 0}.

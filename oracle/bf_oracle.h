@@ -27,6 +27,8 @@ void ora_exp2(int n, double *W);            /* i -> i+2^j, 1/(deg+1) */
 void ora_full(int n, double *W);            /* uniform 1/n */
 void ora_one_peer_exp2(int n, long long k, double *W); /* P:916 dynamic one-peer */
 void ora_one_peer_exp2_peers(int n, long long k, int i, int *src, int *dst);
+void ora_inner_outer_exp2(int n, int L, long long k, double *W); /* P:828, R27 */
+void ora_inner_outer_exp2_peers(int n, int L, long long k, int i, int *src, int *dst);
 
 /* ---- neighbour sets and classes (Eq. 6-8) -------------------- */
 int ora_in_neighbors(int n, const double *W, int i, int *out);   /* ascending */

@@ -104,6 +104,37 @@ def test_one_peer_schedule_and_exact_average():
     assert np.abs(Y - X.mean(axis=0)).max() > 1e-3
 
 
+def test_inner_outer_exp2_schedule():
+    # P:828 / P:869, reading R27: hand-derived tables, then properties.
+    g = golden("inner_outer_exp2_tables.json")
+    for case in g["cases"]:
+        n, L = case["n"], case["local_size"]
+        for k, srcs in enumerate(case["src_by_round"]):
+            for i in range(n):
+                assert ora.inner_outer_exp2_peers(n, L, k, i)[0] == srcs[i], (n, L, k, i)
+    for n, L in ((8, 4), (8, 2), (16, 4), (12, 3), (8, 8), (6, 1), (16, 8)):
+        M = n // L
+        for k in range(2 * n):
+            W = ora.inner_outer_exp2(n, L, k)
+            assert np.allclose(W.sum(axis=0), 1) and np.allclose(W.sum(axis=1), 1)   # doubly stochastic
+            assert ((W != 0).sum(axis=1) <= 2).all() and ((W != 0).sum(axis=0) <= 2).all()  # one peer
+            crossing = 0
+            for i in range(n):
+                s, d = ora.inner_outer_exp2_peers(n, L, k, i)
+                if s < 0:
+                    assert d < 0 and W[i, i] == 1.0
+                    continue
+                assert ora.inner_outer_exp2_peers(n, L, k, d)[0] == i      # dst's source is i
+                if s // L != i // L:
+                    crossing += 1
+                    assert s % L == i % L == k % L                           # the outer rank, same slot
+                    dm = (i // L - s // L) % M
+                    assert dm & (dm - 1) == 0                                # distance 2^t
+            assert crossing == (M if M > 1 else 0)                          # one outer agent per machine
+    for k in range(12):   # L = 1: every agent is its own machine -> the plain one-peer exp-2 graph
+        assert np.array_equal(ora.inner_outer_exp2(8, 1, k), ora.one_peer_exp2(8, k))
+
+
 # ------------------------------------------------------------------- mixing ---
 def test_mix_identity_and_uniform():
     g = golden("spec_scalar_examples.json")

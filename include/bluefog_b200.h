@@ -130,9 +130,20 @@ bf_status bf_topology_matrix(int kind, int n, uint64_t k, double *W);
 /* One-peer dynamic exponential-2 schedule (R5): at round k, t = k mod
  * ceil(log2 n); agent `rank` pulls from rank - 2^t and pushes to rank + 2^t. */
 bf_status bf_schedule_one_peer_exp2(int n, int rank, uint64_t round, int *src, int *dst);
-/* kind 0: none (static W); 1: one-peer exp-2 evaluated ON DEVICE from a
- * device-resident round counter starting at round0, advanced by every
- * schedule-mode call (graph-capturable). */
+/* Inner-outer dynamic exponential-2 schedule (named at P:828 and P:869; the
+ * paper gives no formula -- DESIGN.md reading R27): machines of local_size
+ * consecutive agents.  At round k local rank o = k mod local_size
+ * pulls from machine m - 2^t (same local rank), t = (k div local_size) mod
+ * ceil(log2 M); the other local_size - 1 agents of the machine run the
+ * one-peer exp-2 rule among themselves (relabelled r = (l - o - 1) mod L,
+ * t' = k mod ceil(log2(L - 1))).  *src = *dst = -1: no peer this round.
+ * BF_ERR_ARG if local_size does not divide n. */
+bf_status bf_schedule_inner_outer_exp2(int n, int local_size, int rank, uint64_t round, int *src, int *dst);
+/* kind 0: none (static W); 1: one-peer exp-2; 2: inner-outer exp-2 over the
+ * machine size of the last bf_set_machine_topology (BF_ERR_STATE if none).
+ * Kinds 1 and 2 are evaluated ON DEVICE from a device-resident round counter
+ * starting at round0, advanced by every schedule-mode call (graph-capturable);
+ * every agent with a peer mixes 1/2 self + 1/2 its source. */
 bf_status bf_set_dynamic_schedule(bf_ctx *ctx, int kind, uint64_t round0);
 bf_status bf_set_topology_check(bf_ctx *ctx, int enable);   /* P:613; default on */
 

@@ -6,6 +6,6 @@ topology helpers); there is no CPU fallback -- a missing library raises.
 """
 from . import _lib
 from ._lib import BluefogError
-from .api import Context, one_peer_exp2, topology_matrix
+from .api import Context, inner_outer_exp2, one_peer_exp2, topology_matrix
 
-__all__ = ["Context", "BluefogError", "topology_matrix", "one_peer_exp2"]
+__all__ = ["Context", "BluefogError", "topology_matrix", "one_peer_exp2", "inner_outer_exp2"]

@@ -58,6 +58,7 @@ _SIGS = {
     "bf_out_neighbors": (_i, [_vp, _i, C.POINTER(_i), _i, C.POINTER(_i)]),
     "bf_topology_matrix": (_i, [_i, _i, _u64, C.POINTER(C.c_double)]),
     "bf_schedule_one_peer_exp2": (_i, [_i, _i, _u64, C.POINTER(_i), C.POINTER(_i)]),
+    "bf_schedule_inner_outer_exp2": (_i, [_i, _i, _i, _u64, C.POINTER(_i), C.POINTER(_i)]),
     "bf_set_dynamic_schedule": (_i, [_vp, _i, _u64]),
     "bf_set_topology_check": (_i, [_vp, _i]),
     "bf_neighbor_allreduce": (_i, [_vp, _vp, _vp, _sz, _i, _wp, _vp]),

@@ -65,6 +65,13 @@ def one_peer_exp2(n: int, rank: int, round: int):
     return s.value, d.value
 
 
+def inner_outer_exp2(n: int, local_size: int, rank: int, round: int):
+    """(src, dst) of `rank` at `round` of the inner-outer exp-2 schedule (R27); -1 = none."""
+    s, d = C.c_int(), C.c_int()
+    check(_lib.load().bf_schedule_inner_outer_exp2(n, local_size, rank, int(round), C.byref(s), C.byref(d)))
+    return s.value, d.value
+
+
 class _Views:
     """Keeps a ctypes bf_weights array (and its backing arrays) alive."""
 
@@ -185,7 +192,10 @@ class Context:
         return list(buf[:n.value])
 
     def set_dynamic_schedule(self, kind: str = "one_peer_exp2", round0: int = 0):
-        check(self.lib.bf_set_dynamic_schedule(self.h, {"none": 0, "one_peer_exp2": 1}[kind], int(round0)))
+        """"none", "one_peer_exp2" (P:916) or "inner_outer_exp2" (P:828, R27;
+        machines as set by set_machine_topology)."""
+        kinds = {"none": 0, "one_peer_exp2": 1, "inner_outer_exp2": 2}
+        check(self.lib.bf_set_dynamic_schedule(self.h, kinds[kind], int(round0)))
 
     def set_topology_check(self, enable: bool):
         check(self.lib.bf_set_topology_check(self.h, 1 if enable else 0))

@@ -77,6 +77,44 @@ struct DynDecl {
 
 enum WMode : int { kWStatic = 0, kWSchedule = 1, kWDynamic = 2 };
 
+// Dynamic one-peer schedules, evaluated from a round counter on the host
+// (bf_schedule_*) and inside the kernels (device-resident counter):
+//   kind 1: one-peer exp-2 (R5): t = k mod ceil(log2 n), pull i - 2^t, push i + 2^t
+//   kind 2: inner-outer exp-2 (R27): machines of L agents; local
+//           rank o = k mod L pulls from machine m - 2^t, t = (k div L) mod
+//           ceil(log2 M), same local rank; the other L - 1 agents of the machine,
+//           relabelled r = (l - o - 1) mod L, run kind 1 over a group of L - 1
+//           with t' = k mod ceil(log2(L - 1)).
+// src = dst = -1: no peer this round (self weight 1).  Every agent with a peer
+// mixes 1/2 self + 1/2 source, so each round's W is doubly stochastic.
+__host__ __device__ inline void sched_peers(int kind, int n, int L, unsigned long long k, int i, int &src, int &dst) {
+    src = dst = -1;
+    int grp = n, base = 0, r = i, stride = 1;
+    unsigned long long kk = k;
+    if (kind == 2) {
+        const int M = n / L, m = i / L, l = i % L;
+        const int o = static_cast<int>(k % static_cast<unsigned long long>(L));
+        if (l == o) {              // outer: one-peer exp-2 over the machines, slot o
+            grp = M; base = o; r = m; stride = L; kk = k / static_cast<unsigned long long>(L);
+        } else {                   // inner: one-peer exp-2 over the other L - 1 slots
+            grp = L - 1; r = ((l - o - 1) % L + L) % L;
+            int tau = 0;
+            while ((1 << tau) < grp) ++tau;
+            if (tau == 0) return;
+            const int off = 1 << static_cast<int>(k % static_cast<unsigned long long>(tau));
+            src = m * L + ((r - off + grp) % grp + o + 1) % L;
+            dst = m * L + ((r + off) % grp + o + 1) % L;
+            return;
+        }
+    }
+    int tau = 0;
+    while ((1 << tau) < grp) ++tau;
+    if (tau == 0) return;
+    const int off = 1 << static_cast<int>(kk % static_cast<unsigned long long>(tau));
+    src = base + ((r - off) % grp + grp) % grp * stride;
+    dst = base + (r + off) % grp * stride;
+}
+
 struct Geometry {
     int k;               // local agents
     int n;               // total agents
@@ -111,6 +149,7 @@ struct ExchParams {
     unsigned long long ccnt_off;            // kernels 2, 3: u32 [tmax] per-chunk CTA counters (local)
     unsigned long long cflag_off;           // kernels 2, 3: u64 [tmax] per-chunk release flags
     unsigned pub_mask;                      // kernel 3, kWStatic: local agents read by another process
+    int sched_kind, sched_L;                // kWSchedule: schedule kind (1, 2) and machine size
     unsigned long long prog_off;            // kernel 3: u64 [kMaxGrid] per-CTA publish progress
     unsigned long long *stats;              // kernel 3 built with BF_STATS=1: u64 [grid][8] (diagnostics)
     float *psi;                             // kernel 3 MODE 3 (Exact-Diffusion): psi state [k][count], in place

@@ -38,7 +38,8 @@ __device__ __forceinline__ void publish_done(const Geometry &g, unsigned long lo
 // --------------------------------------------------------------------------
 // Source resolution for one call: fills the shared table of every local agent.
 //   static   : coefficients from the host's W row (Eq. 5)
-//   schedule : one-peer exp-2 from the device round counter (R5)
+//   schedule : one-peer exp-2 (R5) or inner-outer exp-2 (R27)
+//              from the device round counter
 //   dynamic  : declared r (Eq. 11) times the senders' s (Eq. 10) read from their
 //              descriptors; push-only receivers discover their sources there;
 //              topology check on mismatches.
@@ -66,20 +67,13 @@ static __device__ bool resolve_sources(const ExchParams &p, unsigned long long e
     } else if (p.wmode == kWSchedule) {
         const unsigned long long round = *reinterpret_cast<volatile unsigned long long *>(
             &pad_of(g, g.me)->round);
-        int tau = 0;
-        while ((1 << tau) < g.n) ++tau;
         for (int a = threadIdx.x; a < k; a += blockDim.x) {
-            const int gid = g.me * k + a;
-            if (tau == 0) {
-                st.self_w[a] = 1.f;
-                st.nsrc[a] = 0;
-            } else {
-                const int off = 1 << static_cast<int>(round % tau);
-                st.self_w[a] = 0.5f;
-                st.nsrc[a] = 1;
-                st.src[a][0] = static_cast<unsigned char>(((gid - off) % g.n + g.n) % g.n);
-                st.coef[a][0] = 0.5f;
-            }
+            int src, dst;
+            sched_peers(p.sched_kind, g.n, p.sched_L, round, g.me * k + a, src, dst);
+            st.self_w[a] = src < 0 ? 1.f : 0.5f;
+            st.nsrc[a] = src < 0 ? 0 : 1;
+            st.src[a][0] = static_cast<unsigned char>(src < 0 ? 0 : src);
+            st.coef[a][0] = 0.5f;
         }
     } else {
         // one warp per local agent; lanes scan candidate senders j

@@ -175,14 +175,12 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
         if (g.nprocs > 1) {
             if (p.wmode == kWStatic) {
                 pub = p.pub_mask;
-            } else if (p.wmode == kWSchedule) {   // one-peer exp-2: agent i pushes to i + 2^t (R5)
+            } else if (p.wmode == kWSchedule) {   // agent a pushes to its scheduled dst (R5, R27)
                 const unsigned long long round = *reinterpret_cast<volatile unsigned long long *>(&pad->round);
-                int tau = 0;
-                while ((1 << tau) < g.n) ++tau;
-                if (tau > 0) {
-                    const int off = 1 << static_cast<int>(round % tau);
-                    for (int a = 0; a < K; ++a)
-                        if (((g.me * K + a + off) % g.n) / K != g.me) pub |= 1u << a;
+                for (int a = 0; a < K; ++a) {
+                    int src, dst;
+                    sched_peers(p.sched_kind, g.n, p.sched_L, round, g.me * K + a, src, dst);
+                    if (dst >= 0 && dst / K != g.me) pub |= 1u << a;
                 }
             } else {
                 pub = (1u << K) - 1u;   // pull-only readers are not known to the sender

@@ -83,7 +83,7 @@ struct bf_ctx {
     std::vector<double> W;                    // n*n
     int machine_L = 0, n_machines = 0;
     std::vector<double> WM;
-    int sched_kind = 0;
+    int sched_kind = 0, sched_L = 1;
     int topo_check = 1;
     int exch_kernel = 3;                      // BF_EXCH: chunk | fused (default)
     int chunk_tiles = 0;                      // BF_CHUNK_TILES; 0 = 256 on one GPU, 1024 across GPUs
@@ -257,8 +257,10 @@ bf_status fill_weights(bf_ctx *c, const bf_weights *weights, ExchParams &p) {
     memset(&p.dyn, 0, sizeof(p.dyn));
     p.check = c->topo_check;
     if (!weights) {
-        if (c->sched_kind == 1) {
+        if (c->sched_kind) {
             p.wmode = kWSchedule;
+            p.sched_kind = c->sched_kind;
+            p.sched_L = c->sched_L;
             return BF_OK;
         }
         p.wmode = kWStatic;
@@ -535,6 +537,13 @@ bf_status bf_schedule_one_peer_exp2(int n, int rank, uint64_t round, int *src, i
     return BF_OK;
 }
 
+bf_status bf_schedule_inner_outer_exp2(int n, int local_size, int rank, uint64_t round, int *src, int *dst) {
+    if (n < 1 || local_size < 1 || n % local_size || rank < 0 || rank >= n || !src || !dst)
+        return fail(BF_ERR_ARG, "bad schedule request");
+    sched_peers(2, n, local_size, round, rank, *src, *dst);
+    return BF_OK;
+}
+
 bf_status bf_set_topology(bf_ctx *c, int n, const double *W) {
     bf_status s = check_ctx(c, false);
     if (s) return s;
@@ -590,9 +599,12 @@ bf_status bf_out_neighbors(bf_ctx *c, int agent, int *ranks, int cap, int *n_out
 bf_status bf_set_dynamic_schedule(bf_ctx *c, int kind, uint64_t round0) {
     bf_status s = check_ctx(c);
     if (s) return s;
-    if (kind != 0 && kind != 1) return fail(BF_ERR_ARG, "unknown schedule kind %d", kind);
+    if (kind < 0 || kind > 2) return fail(BF_ERR_ARG, "unknown schedule kind %d", kind);
+    if (kind == 2 && !c->machine_L)
+        return fail(BF_ERR_STATE, "inner-outer schedule needs bf_set_machine_topology (machine size)");
     c->sched_kind = kind;
-    if (kind == 1) {
+    c->sched_L = kind == 2 ? c->machine_L : 1;
+    if (kind) {
         Pad *pad = reinterpret_cast<Pad *>(c->heap);
         CU(launch_set_u64(&pad->round, round0, nullptr));
         c->launches++;

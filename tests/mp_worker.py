@@ -89,6 +89,20 @@ def main():
         check(f"schedule round {kk}", np_(x), Y, Wk, X, 1e-6)
         X = Y   # continue from the oracle state (rows of other ranks are not visible here)
         x = torch.from_numpy(X[rows].astype(np.float32)).cuda()
+    # ---- inner-outer exp-2 schedule (R27): machines of 2 agents ----------------------
+    if n % 2 == 0:
+        ctx.set_machine_topology(ora.exp2(n // 2) if n > 2 else np.ones((1, 1)), 2)
+        ctx.set_dynamic_schedule("inner_outer_exp2", 1)
+        x, X = inputs(60013)
+        for kk in range(1, 5):
+            x = ctx.neighbor_allreduce(x)
+            torch.cuda.synchronize()
+            Wk = ora.inner_outer_exp2(n, 2, kk)
+            Y = ora.mix(Wk, X)
+            check(f"inner-outer round {kk}", np_(x), Y, Wk, X, 1e-6)
+            X = Y
+            x = torch.from_numpy(X[rows].astype(np.float32)).cuda()
+        ctx.set_dynamic_schedule("one_peer_exp2", 4)
     # ---- fused ATC --------------------------------------------------------------
     for wire, tol in ((torch.float32, 1e-6), (torch.bfloat16, 1e-2)):
         x, X = inputs(123457)

@@ -180,6 +180,31 @@ def test_nar_schedule_one_peer_exact_average():
     ctx.close()
 
 
+@pytest.mark.parametrize("L", [4, 2, 8])
+@pytest.mark.parametrize("op", ["nar", "atc"])
+def test_schedule_inner_outer_exp2(L, op):
+    # inner-outer dynamic exp-2 (R27), evaluated on device
+    n = 8
+    ctx = _ctx(n)
+    ctx.set_machine_topology(ora.exp2(n // L) if n // L > 1 else np.ones((1, 1)), L)
+    ctx.set_dynamic_schedule("inner_outer_exp2", 3)
+    x, X = _inputs(n, 40003)
+    for k in range(3, 3 + 2 * L):
+        Wk = ora.inner_outer_exp2(n, L, k)
+        if op == "nar":
+            x = ctx.neighbor_allreduce(x)
+            torch.cuda.synchronize()
+            assert_parity(_np(x), ora.mix(Wk, X), Wk, X, 1e-6)
+        else:
+            g = _gpu(synthetic.agents_grad(n, 40003, k))
+            G = _np(g)
+            ctx.atc_step(x, g, 0.05)
+            torch.cuda.synchronize()
+            assert_parity(_np(x), ora.atc(Wk, X, G, 0.05), Wk, X, 1e-6, np.abs(Wk) @ (0.05 * np.abs(G)))
+        X = _np(x).astype(np.float64)
+    ctx.close()
+
+
 # ---------------------------------------------------------------------- ATC ---
 @pytest.mark.parametrize("wire", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("gdt", [torch.float32, torch.bfloat16])

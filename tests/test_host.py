@@ -59,6 +59,17 @@ def test_host_one_peer_schedule_matches_oracle(n):
             assert bfp.one_peer_exp2(n, i, k) == ora.one_peer_exp2_peers(n, k, i)
 
 
+@pytest.mark.parametrize("n,L", [(8, 4), (8, 2), (12, 3), (16, 8), (6, 1), (8, 8)])
+def test_host_inner_outer_schedule_matches_oracle(n, L):
+    # the library's sched_peers (host side of the device evaluation) vs the oracle (R27)
+    for k in range(3 * n):
+        for i in range(n):
+            assert bfp.inner_outer_exp2(n, L, i, k) == ora.inner_outer_exp2_peers(n, L, k, i)
+    for bad_n, bad_L in ((n, 0), (n + 1, 2 * L) if L < n else (n, n + 1)):
+        with pytest.raises(bfp.BluefogError):
+            bfp.inner_outer_exp2(bad_n, bad_L, 0, 0)
+
+
 def test_status_strings_and_errors():
     lib = _lib.load()
     assert lib.bf_status_string(3) == b"BF_ERR_TOPOLOGY"

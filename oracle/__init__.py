@@ -240,6 +240,20 @@ def hier(WM, local_size, X):
     return Y
 
 
+def hier_atc(WM, local_size, X, G, lr):
+    """H-ATC (caption P:869): the ATC step of Eq. 17 with the hierarchical
+    combine of P:660 in place of W: (W_M kron J_L/L)(X - lr G), the adapted
+    copy held as fp32 (reading R18, as in `atc`)."""
+    adapted = (_f64(X) - float(np.float32(lr)) * _f64(G)).astype(np.float32).astype(np.float64)
+    return hier(WM, local_size, adapted)
+
+
+def hier_awc(WM, local_size, X, G, lr):
+    """H-AWC (caption P:869): Eq. 16 with the hierarchical combine:
+    (W_M kron J_L/L) X - lr G."""
+    return hier(WM, local_size, X) - float(np.float32(lr)) * _f64(G)
+
+
 def bf16_rne(values) -> np.ndarray:
     v = np.asarray(values, np.float32).ravel()
     f = lib().ora_bf16_rne

@@ -135,6 +135,22 @@ def test_inner_outer_exp2_schedule():
         assert np.array_equal(ora.inner_outer_exp2(8, 1, k), ora.one_peer_exp2(8, k))
 
 
+def test_hierarchical_atc_awc_special_cases():
+    # H-ATC / H-AWC: L = 1 reduces to the plain ATC / AWC over W_M
+    # (Eqs. 17, 16); one machine (L = n) gives every agent the exact average.
+    n, d, lr = 8, 333, 0.25
+    X = synthetic.agents_x0(n, d).astype(np.float64)
+    G = synthetic.agents_grad(n, d, 5).astype(np.float64)
+    W = ora.exp2(n)
+    assert np.allclose(ora.hier_atc(W, 1, X, G, lr), ora.atc(W, X, G, lr), rtol=0, atol=1e-14)
+    assert np.allclose(ora.hier_awc(W, 1, X, G, lr), ora.awc(W, X, G, lr), rtol=0, atol=1e-14)
+    one = np.ones((1, 1))
+    mean_adapted = (X - lr * G).astype(np.float32).astype(np.float64).mean(axis=0)   # fp32 adapted copy (R18)
+    assert np.allclose(ora.hier_atc(one, n, X, G, lr), np.broadcast_to(mean_adapted, X.shape), rtol=0, atol=1e-14)
+    assert np.allclose(ora.hier_awc(one, n, X, G, lr), X.mean(axis=0) - lr * G, rtol=0, atol=1e-14)
+    assert np.array_equal(ora.hier_atc(ora.ring(4), 2, X, G, 0.0), ora.hier(ora.ring(4), 2, X))
+
+
 # ------------------------------------------------------------------- mixing ---
 def test_mix_identity_and_uniform():
     g = golden("spec_scalar_examples.json")

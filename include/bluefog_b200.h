@@ -32,7 +32,7 @@
  *
  * Collectives: bf_connect_peers, bf_set_topology, bf_set_machine_topology,
  * bf_reserve, bf_neighbor_allreduce, bf_atc_step,
- * bf_hierarchical_neighbor_allreduce, bf_win_create, bf_win_free and
+ * bf_hierarchical_neighbor_allreduce (and its ATC / AWC steps), bf_win_create, bf_win_free and
  * bf_barrier must be called by every process in the same order.  Window
  * data calls (put / accumulate / update / collect) are one-sided and need
  * no matching call.
@@ -193,6 +193,17 @@ bf_status bf_exact_diffusion_step(bf_ctx *ctx, float *x, const void *g, bf_dtype
 bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *ctx, const void *x, void *y, size_t count,
                                              bf_dtype dtype, const bf_weights *machine_weights,
                                              void *stream);
+/* Hierarchical ATC / AWC steps (H-ATC, H-AWC: caption P:869, Table):
+ *   H-ATC (Eq. 17 with the hierarchical combine):  x <- (W_M kron J_L/L)(x - lr g)
+ *   H-AWC (Eq. 16 with the hierarchical combine):  x <- (W_M kron J_L/L) x - lr g
+ * x: fp32 [agents_per_proc][count], updated in place; g: fp32 or bf16, same
+ * layout.  One kernel per call: the adapt is fused into the publish (H-ATC)
+ * or the final write (H-AWC).  Device tensors only; machine_weights and errors
+ * as bf_hierarchical_neighbor_allreduce; collective like it. */
+bf_status bf_hierarchical_atc_step(bf_ctx *ctx, float *x, const void *g, bf_dtype g_dtype, size_t count, float lr,
+                                   const bf_weights *machine_weights, void *stream);
+bf_status bf_hierarchical_awc_step(bf_ctx *ctx, float *x, const void *g, bf_dtype g_dtype, size_t count, float lr,
+                                   const bf_weights *machine_weights, void *stream);
 
 /* ---- one-sided windows (async push-sum P:551-585) -------------------
  * bf_win_create (collective): registers the stacked tensor x (borrowed until

@@ -65,6 +65,8 @@ _SIGS = {
     "bf_atc_step": (_i, [_vp, _vp, _vp, _i, _sz, C.c_float, _i, _vp, _wp, _vp]),
     "bf_awc_step": (_i, [_vp, _vp, _vp, _i, _sz, C.c_float, _wp, _vp]),
     "bf_hierarchical_neighbor_allreduce": (_i, [_vp, _vp, _vp, _sz, _i, _wp, _vp]),
+    "bf_hierarchical_atc_step": (_i, [_vp, _vp, _vp, _i, _sz, C.c_float, _wp, _vp]),
+    "bf_hierarchical_awc_step": (_i, [_vp, _vp, _vp, _i, _sz, C.c_float, _wp, _vp]),
     "bf_win_create": (_i, [_vp, C.c_char_p, _vp, _sz, _i, _i, _i]),
     "bf_win_free": (_i, [_vp, C.c_char_p]),
     "bf_win_put": (_i, [_vp, C.c_char_p, _wp, _u64, _vp]),

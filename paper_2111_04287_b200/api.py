@@ -289,6 +289,27 @@ class Context:
                                                           v.ptr() if v else None, _stream_ptr(stream, self.device)))
         return y
 
+    def hierarchical_atc_step(self, x: torch.Tensor, g: torch.Tensor, lr: float, self_weight=None,
+                              src_machine_weights=None, stream=None) -> torch.Tensor:
+        """H-ATC: x <- (W_M kron J_L/L)(x - lr g), in place on the fp32 master x."""
+        return self._hier_step(self.lib.bf_hierarchical_atc_step, x, g, lr, self_weight, src_machine_weights, stream)
+
+    def hierarchical_awc_step(self, x: torch.Tensor, g: torch.Tensor, lr: float, self_weight=None,
+                              src_machine_weights=None, stream=None) -> torch.Tensor:
+        """H-AWC: x <- (W_M kron J_L/L) x - lr g, in place on the fp32 master x."""
+        return self._hier_step(self.lib.bf_hierarchical_awc_step, x, g, lr, self_weight, src_machine_weights, stream)
+
+    def _hier_step(self, fn, x, g, lr, self_weight, src_machine_weights, stream):
+        if x.dtype != torch.float32:
+            raise ValueError("x must be the fp32 master copy")
+        count = self._rows(x)
+        if g.shape != x.shape or not g.is_contiguous():
+            raise ValueError("g must be contiguous with the shape of x")
+        v = self._views(self_weight, src_machine_weights, None)
+        check(fn(self.h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()), _DT[g.dtype], count, float(lr),
+                 v.ptr() if v else None, _stream_ptr(stream, self.device)))
+        return x
+
     # ---- windows (P:388-423) ---------------------------------------------------
     def win_create(self, tensor: torch.Tensor, name: str, zero_init: bool = True, with_p: bool = False) -> bool:
         count = self._rows(tensor)

@@ -165,6 +165,10 @@ struct HierParams {
     const void *x;
     void *y;
     int L;                                  // agents per machine
+    int hmode;                              // 0 plain, 1 H-ATC, 2 H-AWC (Eqs. 16-17)
+    const void *g;                          // hmode 1, 2: gradient [k][count]
+    int g_bf16;
+    float lr;
     int TS;                                 // tiles per slice
     unsigned long long slot_off, slot_agent_stride, slot_parity_stride;   // stage A (x dtype)
     unsigned long long ready_off;

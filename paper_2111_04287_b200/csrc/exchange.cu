@@ -267,11 +267,20 @@ __global__ void __launch_bounds__(kThreads, BF_MINB) exchange_chunk_kernel(const
 }
 
 // --------------------------------------------------------------------------
+// Gradient row a of the hierarchical ATC / AWC step, fp32 or bf16.
+static __device__ __forceinline__ void load_grad(const HierParams &p, int a, long long off, float v[4], int vl,
+                                                 bool vec) {
+    if (p.g_bf16)
+        Vec4<bf16>::load(static_cast<const bf16 *>(p.g) + static_cast<long long>(a) * p.geo.count + off, v, vl, vec);
+    else
+        Vec4<float>::load(static_cast<const float *>(p.g) + static_cast<long long>(a) * p.geo.count + off, v, vl, vec);
+}
+
 // Hierarchical neighbour allreduce: leader-free, sliced.
-//   A: publish x tile t -> slot, flag
+//   A: publish x tile t -> slot, flag (H-ATC: x - lr g)
 //   B: agent (m,l) averages slice l over its machine's L agents (1/L, R12)
 //   C: agent (m,l) combines slice l with the machine neighbours' slice l (W_M)
-//   D: every agent gathers all slices of its machine's result
+//   D: every agent gathers all slices of its machine's result (H-AWC: - lr g)
 // Every CTA finishes a stage before starting the next, and a stage only waits
 // on the previous stage, so co-resident CTAs cannot deadlock.
 template <typename XT>
@@ -317,6 +326,12 @@ __global__ void __launch_bounds__(kThreads, 2) hier_kernel(const __grid_constant
             float v[4];
             const int vl = clamp_valid(rem, tile_elem(j));
             Vec4<XT>::load(xr + tile_elem(j), v, vl, vec);
+            if (p.hmode == 1) {   // H-ATC: publish the adapted x - lr g (Eq. 17)
+                float gv[4];
+                load_grad(p, a, base + tile_elem(j), gv, vl, vec);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = fmaf(-p.lr, gv[i], v[i]);
+            }
             Vec4<XT>::store(mine + tile_elem(j), v, vl, vec);
         }
         __syncthreads();
@@ -414,6 +429,12 @@ __global__ void __launch_bounds__(kThreads, 2) hier_kernel(const __grid_constant
             float v[4];
             const int vl = clamp_valid(rem, tile_elem(j));
             Vec4<float>::load_cg(cp + tile_elem(j), v, vl, true);
+            if (p.hmode == 2) {   // H-AWC: combine, then subtract lr g (Eq. 16)
+                float gv[4];
+                load_grad(p, a, base + tile_elem(j), gv, vl, vec);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = fmaf(-p.lr, gv[i], v[i]);
+            }
             Vec4<XT>::store(yr + tile_elem(j), v, vl, vec);
         }
     }

@@ -768,15 +768,20 @@ bf_status bf_exact_diffusion_step(bf_ctx *c, float *x, const void *g, bf_dtype g
                            static_cast<cudaStream_t>(stream), nullptr, nullptr, psi);
 }
 
-bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, size_t count, bf_dtype dtype,
-                                             const bf_weights *machine_weights, void *stream) {
+// hmode 0: y = (W_M (x) J_L/L) x; 1 (H-ATC): x <- (W_M (x) J_L/L)(x - lr g);
+// 2 (H-AWC): x <- (W_M (x) J_L/L) x - lr g.
+static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf_dtype dtype, int hmode,
+                             const void *g, bf_dtype g_dtype, float lr, const bf_weights *machine_weights,
+                             void *stream) {
     bf_status s = check_ctx(c);
     if (s) return s;
     if (count == 0) return BF_OK;   // empty input: nothing to exchange, no kernel
-    if (!x || !y) return fail(BF_ERR_ARG, "null tensor");
+    if (!x || !y || (hmode && !g)) return fail(BF_ERR_ARG, "null tensor");
     if (dtype != BF_FLOAT32 && dtype != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
+    if (hmode && (g_dtype != BF_FLOAT32 && g_dtype != BF_BFLOAT16)) return fail(BF_ERR_UNSUPPORTED, "dtype");
+    if (hmode && !std::isfinite(lr)) return fail(BF_ERR_ARG, "non-finite lr");
+    if (hmode && (is_host_ptr(x) || is_host_ptr(g))) return fail(BF_ERR_ARG, "hierarchical steps take device tensors");
     if (!c->machine_L) return fail(BF_ERR_STATE, "bf_set_machine_topology has not been called");
-    if (count == 0) return BF_OK;
     const int L = c->machine_L, NM = c->n_machines;
     HierParams p;
     memset(&p, 0, sizeof(p));
@@ -831,8 +836,10 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
             for (int q = 0; q < p.mtab.nsrc[a]; ++q) add(p.mtab.src[a][q], p.mtab.coef[a][q]);
             tab.nsrc[a] = static_cast<unsigned char>(cnt);
         }
-        return exchange_common(c, x, nullptr, y, nullptr, count, dtype, dtype, dtype, dtype, 0.f, nullptr,
-                               static_cast<cudaStream_t>(stream), nullptr, &tab);
+        const int gk = hmode ? static_cast<int>(g_dtype) : static_cast<int>(dtype);
+        return exchange_common(c, x, hmode == 1 ? g : nullptr, y, nullptr, count, dtype, gk, dtype, dtype,
+                               hmode ? lr : 0.f, nullptr, static_cast<cudaStream_t>(stream),
+                               hmode == 2 ? g : nullptr, &tab);
     }
     const size_t es = dtype == BF_FLOAT32 ? 4 : 2;
     s = ensure_exchange(c, count * es);
@@ -867,10 +874,14 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
         c->hier_ready = true;
     }
     p.geo = make_geo(c, count);
-    p.geo.vec_ok = (count % 4 == 0) && aligned16(x) && aligned16(y);
+    p.geo.vec_ok = (count % 4 == 0) && aligned16(x) && aligned16(y) && (!hmode || aligned16(g));
     p.x = x;
     p.y = y;
     p.L = L;
+    p.hmode = hmode;
+    p.g = g;
+    p.g_bf16 = hmode && g_dtype == BF_BFLOAT16;
+    p.lr = lr;
     p.TS = (p.geo.T + L - 1) / L;
     p.slot_off = c->slot_off;
     p.slot_agent_stride = 2 * c->exch_cap;
@@ -886,6 +897,21 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, 
     CU(launch_hier(p, dtype, 0, static_cast<cudaStream_t>(stream)));
     c->launches++;
     return BF_OK;
+}
+
+bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *c, const void *x, void *y, size_t count, bf_dtype dtype,
+                                             const bf_weights *machine_weights, void *stream) {
+    return hier_common(c, x, y, count, dtype, 0, nullptr, BF_FLOAT32, 0.f, machine_weights, stream);
+}
+
+bf_status bf_hierarchical_atc_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, size_t count, float lr,
+                                   const bf_weights *machine_weights, void *stream) {
+    return hier_common(c, x, x, count, BF_FLOAT32, 1, g, g_dtype, lr, machine_weights, stream);
+}
+
+bf_status bf_hierarchical_awc_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, size_t count, float lr,
+                                   const bf_weights *machine_weights, void *stream) {
+    return hier_common(c, x, x, count, BF_FLOAT32, 2, g, g_dtype, lr, machine_weights, stream);
 }
 
 // ---- windows ----------------------------------------------------------------

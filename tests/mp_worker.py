@@ -141,6 +141,18 @@ def main():
         y = ctx.hierarchical_neighbor_allreduce(x)
         torch.cuda.synchronize()
         check(f"hier L={L}", np_(y), ora.hier(WM, L, X), np.kron(WM, np.full((L, L), 1.0 / L)), X, 1e-6)
+        Gh = np.stack([synthetic.uniform(synthetic.grad_seed(6, r), 40000, scale=2.0 ** -7) for r in range(n)])
+        gh = torch.from_numpy(Gh[rows].copy()).cuda()
+        Kh = np.kron(WM, np.full((L, L), 1.0 / L))
+        ctx.hierarchical_atc_step(x, gh, 0.1)
+        torch.cuda.synchronize()
+        check(f"H-ATC L={L}", np_(x), ora.hier_atc(WM, L, X, Gh, 0.1), Kh, X, 1e-6,
+              np.abs(Kh) @ (0.1 * np.abs(Gh.astype(np.float64))))
+        x, X = inputs(40000)
+        ctx.hierarchical_awc_step(x, gh, 0.1)
+        torch.cuda.synchronize()
+        check(f"H-AWC L={L}", np_(x), ora.hier_awc(WM, L, X, Gh, 0.1), Kh, X, 1e-6,
+              0.1 * np.abs(Gh.astype(np.float64)))
 
     # ---- neighbor_win_get on a symmetric-heap tensor (reads over NVLink) ------------
     Wst = ora.exp2(n)

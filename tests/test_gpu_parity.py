@@ -339,6 +339,34 @@ def test_hierarchical(nm, L, dtype, impl, monkeypatch):
     ctx.close()
 
 
+@pytest.mark.parametrize("impl", ["fused", "staged"])
+@pytest.mark.parametrize("gdt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("nm,L", [(4, 2), (2, 4), (1, 8)])
+@pytest.mark.parametrize("style", ["atc", "awc"])
+def test_hierarchical_atc_awc(style, nm, L, gdt, impl, monkeypatch):
+    # H-ATC / H-AWC (caption P:869): the adapt fused into the hierarchical combine
+    monkeypatch.setenv("BF_HIER", impl)
+    n = nm * L
+    WM = ora.exp2(nm)
+    ctx = _ctx(n)
+    ctx.set_machine_topology(WM, L)
+    K = np.kron(WM, np.full((L, L), 1.0 / L))
+    lr = 0.1
+    for count in (3, 4096 * 3 + 1, 50000):
+        x, X = _inputs(n, count)
+        g = _gpu(synthetic.agents_grad(n, count, 7), gdt)
+        G = _np(g)
+        if style == "atc":
+            ctx.hierarchical_atc_step(x, g, lr)
+            ref, extra = ora.hier_atc(WM, L, X, G, lr), np.abs(K) @ (np.float32(lr) * np.abs(G))
+        else:
+            ctx.hierarchical_awc_step(x, g, lr)
+            ref, extra = ora.hier_awc(WM, L, X, G, lr), np.float32(lr) * np.abs(G)
+        torch.cuda.synchronize()
+        assert_parity(_np(x), ref, K, X, 1e-6, extra)
+    ctx.close()
+
+
 def test_hierarchical_spec_example():
     gd = golden("hier_2x2_example.json")
     ctx = _ctx(4)

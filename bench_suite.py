@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c3,c5,h,o,e,c2")
+    ap.add_argument("--only", default="c1,c3,c5,h,io,o,e,c2")
     ap.add_argument("--agents", type=int, default=8)
     ap.add_argument("--max-bytes", type=int, default=1 << 30)
     ap.add_argument("--out", default=None)
@@ -162,6 +162,8 @@ def main():
 
     # ----------------------------------------------------------------- H ----
     if "h" in only:
+        hier_env = os.environ.get("BF_HIER", "")
+        hier_fused = (world == 1 and hier_env != "staged") or hier_env == "fused"
         n = a.agents
         k = n // world
         count = 25_600_000
@@ -175,7 +177,7 @@ def main():
             ctx.set_machine_topology(bfp.topology_matrix("exp2", nm), L)
             ms = timed(lambda: ctx.hierarchical_neighbor_allreduce(x, out=y), 20)
             dm = 1 if nm == 2 else (2 if nm in (3, 4) else 3)
-            if world == 1:
+            if hier_fused:
                 # one GPU: the Kronecker mix W_M (x) J/L in the fused kernel -- read x, write y
                 per_agent, path = 2 * count * 4, "fused kernel, W = W_M (x) J_L/L (read x + write y)"
             else:
@@ -184,6 +186,45 @@ def main():
             emit({"config": f"H hierarchical_neighbor_allreduce 25.6M fp32, {nm} machines x {L}", "ms": ms,
                   "path": path, "gbs_per_gpu": k * per_agent / (ms * 1e-3) / 1e9,
                   "hbm_frac": k * per_agent / (ms * 1e-3) / 1e9 / peak if world == 1 else None})
+        # H-ATC / H-AWC (caption P:869): the step of Table, in place on x
+        g = torch.empty_like(x)
+        for la in range(k):
+            bfp.Context.fill_uniform(g[la], synthetic.grad_seed(0, ctx.rank + la), 2.0 ** -7)
+        for L in (2, 4):
+            nm = n // L
+            ctx.set_machine_topology(bfp.topology_matrix("exp2", nm), L)
+            for style, fn in (("H-ATC", ctx.hierarchical_atc_step), ("H-AWC", ctx.hierarchical_awc_step)):
+                ms = timed(lambda: fn(x, g, 1e-3), 20)
+                dm = 1 if nm == 2 else (2 if nm in (3, 4) else 3)
+                if hier_fused:
+                    per_agent, path = 3 * count * 4, "fused kernel, W = W_M (x) J_L/L (read x, g + write x)"
+                else:
+                    per_agent = (2 * (L - 1) + dm) * count * 4 / L + 4 * count * 4
+                    path = "staged kernel, adapt fused into the publish (ATC) / final write (AWC)"
+                emit({"config": f"{style} step 25.6M fp32, {nm} machines x {L}", "ms": ms, "path": path,
+                      "gbs_per_gpu": k * per_agent / (ms * 1e-3) / 1e9,
+                      "hbm_frac": k * per_agent / (ms * 1e-3) / 1e9 / peak if world == 1 else None})
+        ctx.close()
+
+    # ------------------------------------------- inner-outer exp-2 schedule ----
+    if "io" in only:
+        n = a.agents
+        k = n // world
+        count = 25_600_000
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=8 * k * count * 4 + (1 << 30), device=local)
+        x = torch.empty(k, count, device="cuda")
+        g = torch.empty_like(x)
+        for la in range(k):
+            bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + ctx.rank + la)
+            bfp.Context.fill_uniform(g[la], synthetic.grad_seed(0, ctx.rank + la), 2.0 ** -7)
+        for L in (2, 4):
+            ctx.set_machine_topology(bfp.topology_matrix("exp2", n // L), L)
+            ctx.set_dynamic_schedule("inner_outer_exp2", 0)
+            ms = timed(lambda: ctx.atc_step(x, g, 1e-3), 4 * L)   # whole periods of the outer rotation
+            emit({"config": f"ATC step, inner-outer exp-2 schedule (P:828, R27), 25.6M fp32 x {n}, machines of {L}",
+                  "ms": ms, "gbs_per_gpu": k * 12 * count / (ms * 1e-3) / 1e9,
+                  "hbm_frac": k * 12 * count / (ms * 1e-3) / 1e9 / peak if world == 1 else None})
+        ctx.set_dynamic_schedule("none")
         ctx.close()
 
     # ---------------------------------------------------------------- C5 ----

@@ -96,7 +96,8 @@ typedef struct {
  * diagnostics (read at bf_init): BF_EXCH=chunk forces the chunked exchange
  * kernel (default: the local-agent fused kernel where instantiated,
  * agents_per_proc 1, 2, 4, or 8 on one GPU), BF_FUSED_GRID (CTAs of the fused
- * kernel), BF_HIER=staged (sliced hierarchical kernel also on one GPU),
+ * kernel), BF_HIER=staged (sliced hierarchical kernel also on one GPU) or
+ * BF_HIER=fused (Kronecker mix in the fused kernel also across GPUs),
  * BF_WIN_EF=1 (error feedback on for new bf16 windows), BF_STATS=1 (per-CTA
  * timings, bf_exchange_stats, with a -DBF_STATS=1 build). */
 bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_device,

@@ -105,7 +105,7 @@ struct bf_ctx {
     unsigned long long bar_epoch = 0;
     unsigned long long launches = 0;
     unsigned long long *stats = nullptr;      // BF_STATS=1: per-CTA diagnostics of the fused kernel
-    bool hier_staged = false;                 // BF_HIER=staged: always the staged hierarchical kernel
+    int hier_mode = 0;                        // BF_HIER: 0 auto, 1 staged (always), 2 fused (also across GPUs)
     bool win_ef = false;                      // BF_WIN_EF=1: new windows start with error feedback on
 };
 
@@ -417,7 +417,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     if (const char *x = getenv("BF_EXCH"))
         c->exch_kernel = strcmp(x, "chunk") == 0 ? 2 : 3;
     if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
-    if (const char *x = getenv("BF_HIER")) c->hier_staged = strcmp(x, "staged") == 0;
+    if (const char *x = getenv("BF_HIER")) c->hier_mode = strcmp(x, "staged") == 0 ? 1 : strcmp(x, "fused") == 0 ? 2 : 0;
     if (const char *x = getenv("BF_WIN_EF")) c->win_ef = atoi(x) != 0;
     if (const char *x = getenv("BF_STATS"))
         if (atoi(x) && cudaMalloc(&c->stats, static_cast<size_t>(kMaxGrid) * 8 * 8) == cudaSuccess)
@@ -629,13 +629,14 @@ bf_status bf_reserve(bf_ctx *c, size_t bytes_per_agent) {
 static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *y, void *shadow, size_t count,
                                  int x_kind, int g_kind, int wire_kind, int y_kind, float lr,
                                  const bf_weights *weights, cudaStream_t st, const void *awc_g = nullptr,
-                                 const SrcTab *static_tab = nullptr, float *psi = nullptr) {
+                                 const SrcTab *static_tab = nullptr, float *psi = nullptr,
+                                 unsigned static_pub = 0) {
     if (count == 0) return BF_OK;
     if (count > (1ull << 40)) return fail(BF_ERR_ARG, "count too large");
     ExchParams p;
     memset(&p, 0, sizeof(p));
     bf_status s = BF_OK;
-    if (static_tab) {   // a W assembled by the caller (hierarchical on one GPU)
+    if (static_tab) {   // a W assembled by the caller (hierarchical: W_M (x) J_L/L)
         p.wmode = kWStatic;
         p.tab = *static_tab;
     } else {
@@ -665,7 +666,9 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     p.ready_stride = c->ready_stride;
     // kernel 3 (local-agent fused) is instantiated for k = 1, 2, 4, 8; other k use the chunked kernel
     p.kernel = c->exch_kernel == 3 && !fused_supported(c->k, c->nprocs) ? 2 : c->exch_kernel;
-    if (p.wmode == kWStatic && c->nprocs > 1) {   // local agents whose x_half another process reads
+    if (static_tab) {
+        p.pub_mask = c->nprocs > 1 ? static_pub : 0u;   // the caller knows who reads its agents
+    } else if (p.wmode == kWStatic && c->nprocs > 1) {   // local agents whose x_half another process reads
         for (int a = 0; a < c->k; ++a) {
             const int gid = c->proc * c->k + a;
             for (int j = 0; j < c->n; ++j)
@@ -785,11 +788,27 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
     const int L = c->machine_L, NM = c->n_machines;
     HierParams p;
     memset(&p, 0, sizeof(p));
-    // One process hosting every agent (N = 1): the hierarchical average is the
-    // plain mix with W = W_M (x) J_L / L (R12), applied in registers by
-    // the fused exchange kernel (read x, write y) instead of the staged kernel.
-    const bool as_mix = c->nprocs == 1 && !c->hier_staged && c->exch_kernel == 3 && fused_supported(c->k, 1) &&
-                        L * NM - 1 <= kMaxS;
+    // The hierarchical average is the plain mix with W = W_M (x) J_L / L (P:660,
+    // R12).  When that W fits the fused exchange kernel (in-degree <= kMaxS,
+    // agents_per_proc it is instantiated for) it is applied there: in registers
+    // on one GPU (read x, write y), and across GPUs with the same pull pipeline
+    // as any static W.  Otherwise (or BF_HIER=staged) the staged sliced kernel.
+    int kron_deg = 0;
+    if (!machine_weights) {
+        for (int m = 0; m < NM; ++m) {
+            int d = 0;
+            for (int q = 0; q < NM; ++q) d += (q != m && c->WM[static_cast<size_t>(m) * NM + q] != 0.0);
+            kron_deg = std::max(kron_deg, L - 1 + d * L);
+        }
+    } else {
+        for (int a = 0; a < c->k; ++a) kron_deg = std::max(kron_deg, L - 1 + std::max(machine_weights[a].n_src, 0) * L);
+    }
+    // Across GPUs the Kronecker W pulls every remote agent of the machine
+    // neighbourhood in full (L rows per machine instead of one slice average):
+    // measured slower than the staged kernel at N = 2, so it
+    // is used there only when forced (BF_HIER=fused).
+    const bool as_mix = c->hier_mode != 1 && (c->nprocs == 1 || c->hier_mode == 2) && c->exch_kernel == 3 &&
+                        fused_supported(c->k, c->nprocs) && kron_deg <= kMaxS;
     for (int a = 0; a < c->k; ++a) {
         const int gid = c->proc * c->k + a, m = gid / L;
         if (!machine_weights) {
@@ -820,13 +839,13 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
         SrcTab tab;
         memset(&tab, 0, sizeof(tab));
         for (int a = 0; a < c->k; ++a) {
-            const int m = a / L;   // gid == a on one process
+            const int gid = c->proc * c->k + a, m = gid / L;
             tab.self_w[a] = p.mtab.self_w[a] / static_cast<float>(L);
             int cnt = 0;
             auto add = [&](int mm, float w) {
                 for (int l = 0; l < L; ++l) {
                     const int j = mm * L + l;
-                    if (j == a) continue;
+                    if (j == gid) continue;
                     tab.src[a][cnt] = static_cast<unsigned char>(j);
                     tab.coef[a][cnt] = w / static_cast<float>(L);
                     ++cnt;
@@ -836,10 +855,23 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
             for (int q = 0; q < p.mtab.nsrc[a]; ++q) add(p.mtab.src[a][q], p.mtab.coef[a][q]);
             tab.nsrc[a] = static_cast<unsigned char>(cnt);
         }
+        // local agents another process reads: static machine topology -> from W_M;
+        // per-call machine views -> every agent (the readers are not known here)
+        unsigned pub = 0;
+        for (int a = 0; a < c->k; ++a) {
+            const int gid = c->proc * c->k + a, m = gid / L;
+            bool read = machine_weights != nullptr;
+            for (int i = 0; i < c->n && !read; ++i) {
+                if (i / c->k == c->proc) continue;
+                const int mi = i / L;
+                read = mi == m || c->WM[static_cast<size_t>(mi) * NM + m] != 0.0;
+            }
+            if (read) pub |= 1u << a;
+        }
         const int gk = hmode ? static_cast<int>(g_dtype) : static_cast<int>(dtype);
         return exchange_common(c, x, hmode == 1 ? g : nullptr, y, nullptr, count, dtype, gk, dtype, dtype,
                                hmode ? lr : 0.f, nullptr, static_cast<cudaStream_t>(stream),
-                               hmode == 2 ? g : nullptr, &tab);
+                               hmode == 2 ? g : nullptr, &tab, nullptr, pub);
     }
     const size_t es = dtype == BF_FLOAT32 ? 4 : 2;
     s = ensure_exchange(c, count * es);

@@ -131,7 +131,7 @@ def main():
           np.abs(We) @ (np.abs(X) + 0.1 * np.abs(Ge.astype(np.float64)) + np.abs(Pe.astype(np.float64))))
 
     # ---- hierarchical -------------------------------------------------------------
-    for L in (2, n):
+    for L in sorted({1, 2, n}):
         if n % L or n // L < 1:
             continue
         nm = n // L

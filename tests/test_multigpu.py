@@ -16,11 +16,14 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("nproc,k", [(2, 1), (2, 2), (4, 1), (4, 2)])
-def test_multiprocess_parity(nproc, k):
+@pytest.mark.parametrize("nproc,k,hier", [(2, 1, "auto"), (2, 2, "auto"), (2, 4, "auto"), (2, 2, "fused"),
+                                          (4, 1, "auto"), (4, 2, "auto")])
+def test_multiprocess_parity(nproc, k, hier):
+    # hier="fused": the hierarchical calls take the Kronecker mix in the fused
+    # kernel across GPUs (BF_HIER=fused) instead of the staged kernel
     if _ngpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    env = dict(os.environ, BF_TEST_K=str(k), BF_TIMEOUT_MS="8000")
+    env = dict(os.environ, BF_TEST_K=str(k), BF_TIMEOUT_MS="8000", BF_HIER=hier)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mp_worker.py")]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)

@@ -166,6 +166,7 @@ struct HierParams {
     void *y;
     int L;                                  // agents per machine
     int hmode;                              // 0 plain, 1 H-ATC, 2 H-AWC (Eqs. 16-17)
+    unsigned pubA;                          // local agents stage A publishes (machine spans processes)
     const void *g;                          // hmode 1, 2: gradient [k][count]
     int g_bf16;
     float lr;

@@ -277,7 +277,8 @@ static __device__ __forceinline__ void load_grad(const HierParams &p, int a, lon
 }
 
 // Hierarchical neighbour allreduce: leader-free, sliced.
-//   A: publish x tile t -> slot, flag (H-ATC: x - lr g)
+//   A: publish x tile t -> slot, flag (H-ATC: x - lr g), only for agents a
+//      machine member on another process reads; local members read x in B
 //   B: agent (m,l) averages slice l over its machine's L agents (1/L, R12)
 //   C: agent (m,l) combines slice l with the machine neighbours' slice l (W_M)
 //   D: every agent gathers all slices of its machine's result (H-AWC: - lr g)
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 2) hier_kernel(const __grid_constant
     const long long itemsA = static_cast<long long>(k) * g.T;
     for (long long w = blockIdx.x; w < itemsA; w += gridDim.x) {
         const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
+        if (!((p.pubA >> a) & 1u)) continue;   // no member of its machine on another process
         const long long base = static_cast<long long>(t) * kTile, rem = count - base;
         const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(a) * count + base;
         XT *mine = const_cast<XT *>(slotA(g.me * k + a)) + base;
@@ -345,13 +347,35 @@ __global__ void __launch_bounds__(kThreads, 2) hier_kernel(const __grid_constant
         const int gid = g.me * k + a, m = gid / L, l = gid % L;
         const int t = l * TS + tt;
         if (t >= g.T) continue;
-        if (threadIdx.x < L) wait_all(ready_ptr(g, p.ready_off, p.ready_stride, m * L + threadIdx.x, t));
+        // members on another process: their published copy (stage A flag)
+        if (threadIdx.x < L && (m * L + static_cast<int>(threadIdx.x)) / k != g.me)
+            wait_all(ready_ptr(g, p.ready_off, p.ready_stride, m * L + threadIdx.x, t));
         __syncthreads();
         if (s_fail) return;
         const long long base = static_cast<long long>(t) * kTile, rem = count - base;
         float acc[kVecPerThread][4] = {};
         for (int lp = 0; lp < L; ++lp) {
-            const XT *sp = slotA(m * L + lp) + base;
+            const int j_agent = m * L + lp;
+            if (j_agent / k == g.me) {   // member on this process: straight from x (adapted as in stage A)
+                const int aj = j_agent % k;
+                const XT *xr = static_cast<const XT *>(p.x) + static_cast<long long>(aj) * count + base;
+#pragma unroll
+                for (int j = 0; j < kVecPerThread; ++j) {
+                    float v[4];
+                    const int vl = clamp_valid(rem, tile_elem(j));
+                    Vec4<XT>::load(xr + tile_elem(j), v, vl, vec);
+                    if (p.hmode == 1) {
+                        float gv[4];
+                        load_grad(p, aj, base + tile_elem(j), gv, vl, vec);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) v[i] = fmaf(-p.lr, gv[i], v[i]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[j][i] += v[i];
+                }
+                continue;
+            }
+            const XT *sp = slotA(j_agent) + base;
 #pragma unroll
             for (int j = 0; j < kVecPerThread; ++j) {
                 float v[4];

@@ -911,6 +911,10 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
     p.y = y;
     p.L = L;
     p.hmode = hmode;
+    for (int a = 0; a < c->k; ++a) {   // stage A: only agents whose machine spans other processes
+        const int m = (c->proc * c->k + a) / L;
+        if ((m * L) / c->k != c->proc || (m * L + L - 1) / c->k != c->proc) p.pubA |= 1u << a;
+    }
     p.g = g;
     p.g_bf16 = hmode && g_dtype == BF_BFLOAT16;
     p.lr = lr;

@@ -205,6 +205,40 @@ def test_schedule_inner_outer_exp2(L, op):
     ctx.close()
 
 
+@pytest.mark.parametrize("sched", ["one_peer_exp2", "inner_outer_exp2"])
+def test_schedule_step_in_cuda_graph(sched):
+    # The schedule round lives on the device (bf_set_dynamic_schedule), so one
+    # captured ATC step replays as successive rounds (header: graph-capturable).
+    n, L, count, lr = 8, 4, 20011, 0.05
+    ctx = _ctx(n)
+    ctx.set_machine_topology(ora.exp2(n // L), L)
+    x, X = _inputs(n, count)
+    g = _gpu(synthetic.agents_grad(n, count, 2))
+    G = _np(g)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        ctx.atc_step(x, g, lr)                   # warm-up (allocates the exchange region)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    X = _np(x)
+    ctx.set_dynamic_schedule(sched, 5)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        ctx.atc_step(x, g, lr)
+    torch.cuda.synchronize()
+    ctx.set_dynamic_schedule(sched, 5)           # capture does not run the kernel: restart at round 5
+    for k in range(5, 5 + 2 * L):
+        graph.replay()
+        torch.cuda.synchronize()
+        Wk = ora.one_peer_exp2(n, k) if sched == "one_peer_exp2" else ora.inner_outer_exp2(n, L, k)
+        assert_parity(_np(x), ora.atc(Wk, X, G, lr), Wk, X, 1e-6, np.abs(Wk) @ (lr * np.abs(G)))
+        X = _np(x)
+    ctx.poll_error()
+    del graph
+    ctx.close()
+
+
 # ---------------------------------------------------------------------- ATC ---
 @pytest.mark.parametrize("wire", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("gdt", [torch.float32, torch.bfloat16])

@@ -145,3 +145,33 @@ def test_resnet50_shapes():
     s = resnet50_param_shapes()
     # torchvision ResNet-50: 161 parameter tensors, 25 557 032 parameters (the model of P:892)
     assert len(s) == 161 and sum(math.prod(x) for x in s) == 25_557_032
+
+
+def _run_bench(args, env_extra=None):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **(env_extra or {}))
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, cwd=root, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    return [json.loads(l) for l in lines]
+
+
+def test_bench_reference_arm_contract():
+    """--impl reference: one JSON line in the same metric/unit as our arm, oracle timed on the host."""
+    (d,) = _run_bench(["--impl", "reference", "--steps", "1", "--warmup", "3"])
+    assert d["impl"] == "reference" and d["unit"] == "iters/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["steps"] == 1 and d["warmup"] == 3
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": "iters/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["config"]["workload"].startswith("C4")
+
+
+def test_bench_reference_arm_nonzero_rank_is_silent():
+    """Under torchrun only rank 0 runs the reference arm; other ranks exit 0 without output."""
+    assert _run_bench(["--impl", "reference", "--steps", "1", "--warmup", "3", "--gpus", "2"],
+                      {"RANK": "1", "WORLD_SIZE": "2"}) == []

@@ -53,8 +53,25 @@ struct WinVec {
 template <int V>
 __device__ __forceinline__ int win_elem(int j) { return (j * kThreads + threadIdx.x) * V; }
 
+// min CTAs per SM for the streaming window kernels (0 = no bound; tuning variants: -DBF_WIN_COLLECT_MINB=6)
+#ifndef BF_WIN_PUSH_MINB
+#define BF_WIN_PUSH_MINB 4   // C5 A/B (profiles/r01_window_minblocks_ab.txt): 7.17 -> 7.09 ms per round
+#endif
+#ifndef BF_WIN_COLLECT_MINB
+#define BF_WIN_COLLECT_MINB 0
+#endif
+#if BF_WIN_PUSH_MINB > 0
+#define BF_PUSH_LB __launch_bounds__(kThreads, BF_WIN_PUSH_MINB)
+#else
+#define BF_PUSH_LB __launch_bounds__(kThreads)
+#endif
+#if BF_WIN_COLLECT_MINB > 0
+#define BF_COLLECT_LB __launch_bounds__(kThreads, BF_WIN_COLLECT_MINB)
+#else
+#define BF_COLLECT_LB __launch_bounds__(kThreads)
+#endif
 template <typename T>
-__global__ void __launch_bounds__(kThreads) win_push_kernel(const __grid_constant__ WinParams p) {
+__global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) {
     constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV;
     const Geometry &g = p.geo;
     const unsigned long long me = g.peer_base[g.me];
@@ -204,7 +221,7 @@ __global__ void win_collect_decide(const __grid_constant__ WinParams p) {
 // update == 0: update_then_collect (x += sum of ready payloads, R9)
 // update == 1: win_update (out = self*x + sum r_j * latest payload, R10)
 template <typename T>
-__global__ void __launch_bounds__(kThreads) win_collect_kernel(const __grid_constant__ WinParams p, int update) {
+__global__ void BF_COLLECT_LB win_collect_kernel(const __grid_constant__ WinParams p, int update) {
     const Geometry &g = p.geo;
     const unsigned long long me = g.peer_base[g.me];
     Pad *pad = pad_of(g, g.me);

@@ -60,6 +60,17 @@ __device__ __forceinline__ int win_elem(int j) { return (j * kThreads + threadId
 #ifndef BF_WIN_COLLECT_MINB
 #define BF_WIN_COLLECT_MINB 0
 #endif
+// BF_WIN_HINTS=1: x / out / slot streams carry an L2 evict-first policy (tuning variant)
+#ifndef BF_WIN_HINTS
+#define BF_WIN_HINTS 0
+#endif
+#if BF_WIN_HINTS
+#define WIN_LD(T_, V_, p_, v_, n_, vec_) VecN<T_, V_>::load_hint(p_, v_, n_, vec_, policy_evict_first())
+#define WIN_ST(T_, V_, p_, v_, n_, vec_) VecN<T_, V_>::store_hint(p_, v_, n_, vec_, policy_evict_first())
+#else
+#define WIN_LD(T_, V_, p_, v_, n_, vec_) VecN<T_, V_>::load(p_, v_, n_, vec_)
+#define WIN_ST(T_, V_, p_, v_, n_, vec_) VecN<T_, V_>::store(p_, v_, n_, vec_)
+#endif
 #if BF_WIN_PUSH_MINB > 0
 #define BF_PUSH_LB __launch_bounds__(kThreads, BF_WIN_PUSH_MINB)
 #else
@@ -95,7 +106,7 @@ __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) 
                             static_cast<long long>(a * p.maxdout + (p.nout[a] > 0 ? p.out_q[a][0] : 0)) * p.cpad + base;
 #pragma unroll
         for (int j = 0; j < NV; ++j)
-            VecN<T, V>::load(xr + win_elem<V>(j), xv[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+            WIN_LD(T, V, xr + win_elem<V>(j), xv[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
         if (ob0_used) {
 #pragma unroll
             for (int j = 0; j < NV; ++j)
@@ -131,7 +142,7 @@ __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) 
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int vl = clamp_valid_v<V>(rem, win_elem<V>(j));
-                    VecN<T, V>::store(slot + win_elem<V>(j), pay[j], vl, vec);
+                    WIN_ST(T, V, slot + win_elem<V>(j), pay[j], vl, vec);
                     if (p.ef) {   // keep the wire rounding residual (bf16) in the outbox (R24)
                         float r[V];
 #pragma unroll
@@ -154,7 +165,7 @@ __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) 
             for (int j = 0; j < NV; ++j) {
 #pragma unroll
                 for (int i = 0; i < V; ++i) xv[j][i] *= sw;
-                VecN<T, V>::store(xr + win_elem<V>(j), xv[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+                WIN_ST(T, V, xr + win_elem<V>(j), xv[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
             }
         }
     }
@@ -256,7 +267,7 @@ __global__ void BF_COLLECT_LB win_collect_kernel(const __grid_constant__ WinPara
         float acc[NV][V], pre[NV][V];
 #pragma unroll
         for (int j = 0; j < NV; ++j)
-            VecN<T, V>::load(xr + win_elem<V>(j), acc[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+            WIN_LD(T, V, xr + win_elem<V>(j), acc[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
         if (pre_h) {
 #pragma unroll
             for (int j = 0; j < NV; ++j)
@@ -295,7 +306,7 @@ __global__ void BF_COLLECT_LB win_collect_kernel(const __grid_constant__ WinPara
         }
 #pragma unroll
         for (int j = 0; j < NV; ++j)
-            VecN<T, V>::store(outr + win_elem<V>(j), acc[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+            WIN_ST(T, V, outr + win_elem<V>(j), acc[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
     }
 
     __syncthreads();

@@ -90,6 +90,10 @@ typedef struct {
 /* ---- context ------------------------------------------------------------------
  * bf_init: create the context of process `proc_rank` of `n_procs`, hosting
  * `agents_per_proc` agents on CUDA device `cuda_device`, with a symmetric
+ * (SURVEY 8(b) names the fourth argument local_size, the paper's agents per
+ * machine.  Here one process hosts agents_per_proc agents on one GPU --
+ * 1 on an 8-GPU box, as in the paper; the machine size of the hierarchical
+ * calls is set separately by bf_set_machine_topology.)  With a symmetric
  * heap of `heap_bytes` device bytes (exchange slots, windows, hierarchical
  * buffers and signal pads all live there; it is exported through CUDA IPC).
  * Env: BF_TIMEOUT_MS (default 10000) bounds every device wait.  Tuning /
@@ -120,6 +124,20 @@ const char *bf_status_string(bf_status s);
  * W[i*n + j] = w_ij, the weight agent i applies to x_j (Eq. 8).  Every process
  * passes the same W.  Default before any call: fully connected 1/n (R15). */
 bf_status bf_set_topology(bf_ctx *ctx, int n, const double *W);
+/* Static topology from LOCAL views (Eq. 9; SURVEY 8(b)
+ * "bf_set_topology_local"): weights[a] is the view of local agent a
+ * (self_weight required; src ranks / r_ij and / or dst ranks / s_ji, the same
+ * four configurations as the per-call views).  Collective: every process passes
+ * its agents' views; the library exchanges them through the peers' signal pads
+ * and every process assembles the same global W:
+ *   w_ii = self_weight;  j in src_i: w_ij = r_ij * (s_ij if j lists i as a
+ *   destination, else 1) (R1);  no src list (push only): w_ij = s_ij for every
+ *   j that lists i (R16).
+ * With the topology check on (default), a receiver's src list must name exactly
+ * the senders that list it: else BF_ERR_TOPOLOGY (on every process, nothing
+ * changed).  On success it replaces the topology like bf_set_topology (and
+ * turns a dynamic schedule off). */
+bf_status bf_set_topology_local(bf_ctx *ctx, const bf_weights *weights);
 /* Hierarchical machine topology: machines of `local_size` consecutive
  * agents (machine_rank = rank // local_size); WM is n_machines^2. */
 bf_status bf_set_machine_topology(bf_ctx *ctx, int local_size, int n_machines, const double *WM);
@@ -242,7 +260,10 @@ bf_status bf_win_get(bf_ctx *ctx, const char *name, const bf_weights *weights, u
  * and round.  Off by default (BF_WIN_EF=1 at bf_init turns it on for new
  * windows).  Local, not collective; BF_ERR_WINDOW for an unknown name. */
 bf_status bf_win_set_error_feedback(bf_ctx *ctx, const char *name, int enable);
-/* put / accumulate by the local agents selected in agent_mask (bit a = local
+/* put / accumulate of the REGISTERED window tensor (the paper's win_put(tensor,
+ * name) passes the tensor given to win_create, Listing 3; SURVEY
+ * 8(b)'s optional x argument is therefore not taken) by the local agents
+ * selected in agent_mask (bit a = local
  * agent a; 0 = all): for each dst j in weights[a] (self + dst only; dst must
  * be out-neighbours at creation) deliver s_ja * x_a into j's slot for a
  * (put: overwrite, accumulate: add), then x_a <- self_weight * x_a
@@ -269,6 +290,12 @@ bf_status bf_win_update_then_collect(bf_ctx *ctx, const char *name, uint64_t age
 bf_status bf_win_get_p(bf_ctx *ctx, const char *name, double *p_host, void *stream);
 bf_status bf_win_counters(bf_ctx *ctx, const char *name, int dst_local, int src_rank,
                           uint64_t *version, uint64_t *consumed);
+/* SURVEY 8(b) bf_win_version: the version counter (payloads delivered so far) of
+ * the slot that receives from src_rank, for the first local agent (ascending)
+ * that has src_rank as an in-neighbour at window creation -- with one agent per
+ * process (the paper's model) that is the process's agent.  bf_win_counters
+ * gives both counters of any (local agent, source) pair. */
+bf_status bf_win_version(bf_ctx *ctx, const char *name, int src_rank, uint64_t *version);
 /* Slot layout of agent `agent` (P:388 pin): element offset of the slot that
  * receives from `src_rank` in the paper's logical numel*d_in layout, or -1. */
 long long bf_win_slot_offset(bf_ctx *ctx, const char *name, int agent, int src_rank);

@@ -72,6 +72,19 @@ def lib():
                                        C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
         L.ora_lsq_grad.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _dp]
         L.ora_lsq_solve.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double, C.c_int, _dp]
+        L.ora_hier_atc.argtypes = [C.c_int, C.c_int, C.c_longlong, _dp, _dp, _dp, C.c_double, _dp]
+        L.ora_hier_awc.argtypes = [C.c_int, C.c_int, C.c_longlong, _dp, _dp, _dp, C.c_double, _dp]
+        L.ora_gt_uv.argtypes = [C.c_int, C.c_longlong, C.c_longlong, _dp, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp]
+        L.ora_gt_y.argtypes = [C.c_int, C.c_longlong, _dp, _dp, _dp, _dp, _dp]
+        L.ora_winp_create.argtypes = [C.c_int, C.c_longlong, _dp, _dp, C.c_int]
+        L.ora_winp_create.restype = C.c_void_p
+        L.ora_winp_free.argtypes = [C.c_void_p]
+        L.ora_winp_accumulate.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, _ip, C.c_int]
+        L.ora_winp_collect.argtypes = [C.c_void_p, C.c_int]
+        L.ora_winp_update.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, _dp]
+        L.ora_winp_get_x.argtypes = [C.c_void_p, _dp]
+        L.ora_atc_fixed_point.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, C.c_double, C.c_double,
+                                          C.c_int, _dp]
     return _lib
 
 
@@ -213,16 +226,32 @@ def exact_diffusion(W, X, G, Psi_prev, lr, wire_bf16=False):
     return Y, Pout
 
 
+def gt_uv(W, U, V, Y, lr):
+    """First half of a push-sum gradient-tracking round (appendix, PAPER.md lines
+    1002-1004): u+ = W(u - lr y), v+ = W v, x+ = u+ / v+.  V: (n, d) or (n, 1)."""
+    W, U, V, Y = _f64(W), _f64(U), _f64(V), _f64(Y)
+    n, d = U.shape
+    Un, Vn, Xn = np.zeros_like(U), np.zeros_like(V), np.zeros_like(U)
+    lib().ora_gt_uv(n, d, V.shape[1], _d(W), _d(U), _d(V), _d(Y), float(lr), _d(Un), _d(Vn), _d(Xn))
+    return Un, Vn, Xn
+
+
+def gt_y(W, Y, Gnew, Gprev):
+    """Second half (line 1006): y+ = W(y + g+ - g)."""
+    W, Y, Gn, Gp = _f64(W), _f64(Y), _f64(Gnew), _f64(Gprev)
+    Yn = np.zeros_like(Y)
+    lib().ora_gt_y(Y.shape[0], Y.shape[1], _d(W), _d(Y), _d(Gn), _d(Gp), _d(Yn))
+    return Yn
+
+
 def gradient_tracking_step(W, U, V, Y, Gprev, grad, lr):
-    """One round of push-sum gradient tracking (appendix),
-    written out with the oracle's W-mix (ora_mix) for every partial averaging:
+    """One round of push-sum gradient tracking (appendix):
         u+ = W (u - lr y);  v+ = W v;  x+ = u+ / v+;  g+ = grad(x+);  y+ = W (y + g+ - g).
-    U, Y, Gprev: (n, d); V: (n, 1).  Returns (x+, u+, v+, y+, g+)."""
-    Un = mix(W, _f64(U) - lr * _f64(Y))
-    Vn = mix(W, _f64(V))
-    Xn = Un / Vn
+    U, Y, Gprev: (n, d); V: (n, 1) or (n, d).  Returns (x+, u+, v+, y+, g+).
+    The arithmetic is ora_gt_uv / ora_gt_y; `grad` is the caller's gradient."""
+    Un, Vn, Xn = gt_uv(W, U, V, Y, lr)
     Gn = _f64(grad(Xn))
-    Yn = mix(W, _f64(Y) + Gn - _f64(Gprev))
+    Yn = gt_y(W, Y, Gn, Gprev)
     return Xn, Un, Vn, Yn, Gn
 
 
@@ -241,17 +270,19 @@ def hier(WM, local_size, X):
 
 
 def hier_atc(WM, local_size, X, G, lr):
-    """H-ATC (caption P:869): the ATC step of Eq. 17 with the hierarchical
-    combine of P:660 in place of W: (W_M kron J_L/L)(X - lr G), the adapted
-    copy held as fp32 (reading R18, as in `atc`)."""
-    adapted = (_f64(X) - float(np.float32(lr)) * _f64(G)).astype(np.float32).astype(np.float64)
-    return hier(WM, local_size, adapted)
+    """H-ATC (caption P:869): (W_M kron J_L/L) fp32(X - lr G) (ora_hier_atc)."""
+    WM, X, G = _f64(WM), _f64(X), _f64(G)
+    Y = np.zeros_like(X)
+    lib().ora_hier_atc(WM.shape[0], local_size, X.shape[1], _d(WM), _d(X), _d(G), float(np.float32(lr)), _d(Y))
+    return Y
 
 
 def hier_awc(WM, local_size, X, G, lr):
-    """H-AWC (caption P:869): Eq. 16 with the hierarchical combine:
-    (W_M kron J_L/L) X - lr G."""
-    return hier(WM, local_size, X) - float(np.float32(lr)) * _f64(G)
+    """H-AWC (caption P:869): (W_M kron J_L/L) X - lr G (ora_hier_awc)."""
+    WM, X, G = _f64(WM), _f64(X), _f64(G)
+    Y = np.zeros_like(X)
+    lib().ora_hier_awc(WM.shape[0], local_size, X.shape[1], _d(WM), _d(X), _d(G), float(np.float32(lr)), _d(Y))
+    return Y
 
 
 def bf16_rne(values) -> np.ndarray:
@@ -314,6 +345,51 @@ class Window:
         return v.value, c.value
 
 
+class WindowPaper:
+    """Paper-semantics window: one plain buffer per
+    in-neighbour, put overwrites, accumulate adds, collect sums then zeroes,
+    update reads without reset (ora_winp_*)."""
+
+    def __init__(self, W_static, X0, zero_init=True):
+        W_static, X0 = _f64(W_static), _f64(X0)
+        self.n, self.count = X0.shape
+        self._h = lib().ora_winp_create(self.n, self.count, _d(W_static), _d(X0), 1 if zero_init else 0)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().ora_winp_free(self._h)
+            self._h = None
+
+    def accumulate(self, i, self_weight, dst_weights, overwrite=False):
+        s = np.zeros(self.n, np.float64)
+        mask = np.zeros(self.n, np.int32)
+        for j, w in dst_weights.items():
+            s[j] = w
+            mask[j] = 1
+        if lib().ora_winp_accumulate(self._h, i, float(self_weight), _d(s), mask.ctypes.data_as(_ip),
+                                     1 if overwrite else 0):
+            raise ValueError("destination outside the creation topology (P:398)")
+
+    def put(self, i, self_weight, dst_weights):
+        self.accumulate(i, self_weight, dst_weights, overwrite=True)
+
+    def collect(self, i):
+        lib().ora_winp_collect(self._h, i)
+
+    def update(self, i, self_weight, src_weights):
+        r = np.zeros(self.n, np.float64)
+        for j, w in src_weights.items():
+            r[j] = w
+        out = np.zeros(self.count, np.float64)
+        lib().ora_winp_update(self._h, i, float(self_weight), _d(r), _d(out))
+        return out
+
+    def x(self):
+        X = np.zeros((self.n, self.count), np.float64)
+        lib().ora_winp_get_x(self._h, _d(X))
+        return X
+
+
 # ---- least squares ------------------------------------------------------------
 def lsq_grad(A, b, x):
     A, b, x = _f64(A), _f64(b), _f64(x)
@@ -329,3 +405,16 @@ def lsq_solve(A_stack, b_stack, tol=1e-13, max_iter=10000):
     x = np.zeros(d, np.float64)
     it = lib().ora_lsq_solve(n, m, d, _d(A), _d(b), tol, max_iter, _d(x))
     return x, it
+
+
+def atc_fixed_point(W, A_stack, b_stack, lr, X0=None, tol=1e-15, max_iter=200000):
+    """ATC-DSGD fixed point x_inf on least squares (Eq. 12-14,
+    Eq. 17): iterate X <- W(X - lr g(X)) in fp64 to stationarity (ora_atc_fixed_point).
+    Returns (X_inf, iterations); raises if it did not converge."""
+    W, A, b = _f64(W), _f64(A_stack), _f64(b_stack)
+    n, m, d = A.shape
+    X = np.zeros((n, d), np.float64) if X0 is None else _f64(X0).copy()
+    it = lib().ora_atc_fixed_point(n, m, d, _d(W), _d(A), _d(b), float(lr), float(tol), int(max_iter), _d(X))
+    if it < 0:
+        raise RuntimeError("ATC fixed-point iteration did not converge")
+    return X, it

@@ -327,6 +327,57 @@ void ora_hier(int n_machines, int L, long long count, const double *WM,
     free(avg);
 }
 
+/* H-ATC (caption P:869; Table): the ATC step of Eq. 17 with
+ * the hierarchical combine of P:660 in place of W.  The adapted copy is held as
+ * fp32 (reading R18, as in ora_atc):  Y = (W_M kron J_L/L) fp32(X - lr G). */
+void ora_hier_atc(int n_machines, int L, long long count, const double *WM,
+                  const double *X, const double *G, double lr, double *Y) {
+    const long long N = (long long)n_machines * L * count;
+    double *xh = (double *)malloc(sizeof(double) * (size_t)N);
+    for (long long q = 0; q < N; ++q) xh[q] = (double)ora_f32(X[q] - lr * G[q]);   /* Eq. 4 */
+    ora_hier(n_machines, L, count, WM, xh, Y);
+    free(xh);
+}
+
+/* H-AWC (caption P:869): Eq. 16 with the hierarchical combine:
+ * Y = (W_M kron J_L/L) X - lr G. */
+void ora_hier_awc(int n_machines, int L, long long count, const double *WM,
+                  const double *X, const double *G, double lr, double *Y) {
+    const long long N = (long long)n_machines * L * count;
+    ora_hier(n_machines, L, count, WM, X, Y);
+    for (long long q = 0; q < N; ++q) Y[q] -= lr * G[q];
+}
+
+/* ========================================================================
+ * Push-sum gradient tracking (appendix "Push-sum gradient tracking",
+ * PAPER.md lines 1000-1006, listing GT-varying), split at the gradient
+ * evaluation the caller performs between the two halves of a round:
+ *   (a) u_i^{k+1} = sum_j w_ij (u_j^k - gamma y_j^k)          (line 1002)
+ *       v_i^{k+1} = sum_j w_ij v_j^k                            (line 1003)
+ *       x_i^{k+1} = u_i^{k+1} / v_i^{k+1}                       (line 1004)
+ *   (b) y_i^{k+1} = sum_j w_ij (y_j^k + g_j^{k+1} - g_j^k)     (line 1006)
+ * U, Y, G*: n x d; V: n x dv with dv = d (the paper's vector v) or dv = 1 (one
+ * push-sum weight per agent: v^0 = 1 keeps every entry of v equal). */
+void ora_gt_uv(int n, long long d, long long dv, const double *W, const double *U, const double *V,
+               const double *Y, double lr, double *Un, double *Vn, double *Xn) {
+    double *w = (double *)malloc(sizeof(double) * (size_t)n * d);
+    for (long long q = 0; q < (long long)n * d; ++q) w[q] = U[q] - lr * Y[q];
+    ora_mix(n, d, W, w, Un);
+    ora_mix(n, dv, W, V, Vn);
+    for (int i = 0; i < n; ++i)
+        for (long long e = 0; e < d; ++e)
+            Xn[(long long)i * d + e] = Un[(long long)i * d + e] / Vn[(long long)i * dv + (dv == 1 ? 0 : e)];
+    free(w);
+}
+
+void ora_gt_y(int n, long long d, const double *W, const double *Y, const double *Gnew,
+              const double *Gprev, double *Yn) {
+    double *q = (double *)malloc(sizeof(double) * (size_t)n * d);
+    for (long long e = 0; e < (long long)n * d; ++e) q[e] = Y[e] + Gnew[e] - Gprev[e];
+    ora_mix(n, d, W, q, Yn);
+    free(q);
+}
+
 /* ========================================================================
  * Window protocol event model (P:388-423 windows; P:551-585 async push-sum).
  * One slot per static in-neighbour in ascending rank, each with two
@@ -538,4 +589,120 @@ int ora_lsq_solve(int n, int m, int d, const double *A, const double *b, double 
     }
     free(rhs); free(r); free(p); free(Ap);
     return it;
+}
+
+/* ========================================================================
+ * Paper-semantics window (P:388-403 windows, P:417-423 win_update, P:585
+ * collect), written as the paper states it, with NO protocol: one buffer per
+ * static in-neighbour (ascending rank);
+ *   put        : buffer_i[j] <- s_ji x_j
+ *   accumulate : buffer_i[j] <- buffer_i[j] + s_ji x_j
+ *   both then  : x_j <- self_weight x_j                      (reading R8)
+ *   collect    : x_i <- x_i + sum_j buffer_i[j]; buffers <- 0 (R9)
+ *   update     : out = self_w x_i + sum_j r_j buffer_i[j]     (no reset)
+ * It is the reference the double-buffered / outbox event model above must
+ * equal whenever no payload waits in an outbox (tests/test_oracle.py).
+ * ====================================================================== */
+struct ora_winp {
+    int n;
+    long long count;
+    int *nin, *in;          /* in[i*n + q] */
+    double *x;              /* n * count */
+    double *buf;            /* [i][q][count] */
+};
+
+ora_winp *ora_winp_create(int n, long long count, const double *Wstatic, const double *X0, int zero_init) {
+    ora_winp *w = (ora_winp *)calloc(1, sizeof(ora_winp));
+    w->n = n;
+    w->count = count;
+    w->nin = (int *)calloc(n, sizeof(int));
+    w->in = (int *)calloc((size_t)n * n, sizeof(int));
+    for (int i = 0; i < n; ++i) w->nin[i] = ora_in_neighbors(n, Wstatic, i, w->in + (size_t)i * n);
+    w->x = (double *)malloc(sizeof(double) * (size_t)n * count);
+    memcpy(w->x, X0, sizeof(double) * (size_t)n * count);
+    w->buf = (double *)calloc((size_t)n * n * count, sizeof(double));
+    if (!zero_init)   /* buffers start as the local tensor (reading R10; P:567 zero_init) */
+        for (int i = 0; i < n; ++i)
+            for (int q = 0; q < w->nin[i]; ++q)
+                memcpy(w->buf + ((size_t)i * n + q) * count, w->x + (size_t)i * count, sizeof(double) * count);
+    return w;
+}
+
+void ora_winp_free(ora_winp *w) {
+    if (!w) return;
+    free(w->nin); free(w->in); free(w->x); free(w->buf); free(w);
+}
+
+int ora_winp_accumulate(ora_winp *w, int j, double self_weight, const double *s, const int *dst_mask,
+                        int overwrite) {
+    const long long C = w->count;
+    for (int i = 0; i < w->n; ++i) {
+        if (!dst_mask[i]) continue;
+        int q = -1;
+        for (int t = 0; t < w->nin[i]; ++t)
+            if (w->in[(size_t)i * w->n + t] == j) q = t;
+        if (q < 0) return -1;   /* dst outside the creation topology */
+        double *b = w->buf + ((size_t)i * w->n + q) * C;
+        for (long long e = 0; e < C; ++e)
+            b[e] = (overwrite ? 0.0 : b[e]) + s[i] * w->x[(size_t)j * C + e];
+    }
+    for (long long e = 0; e < C; ++e) w->x[(size_t)j * C + e] *= self_weight;
+    return 0;
+}
+
+void ora_winp_collect(ora_winp *w, int i) {
+    const long long C = w->count;
+    for (int q = 0; q < w->nin[i]; ++q) {
+        double *b = w->buf + ((size_t)i * w->n + q) * C;
+        for (long long e = 0; e < C; ++e) {
+            w->x[(size_t)i * C + e] += b[e];
+            b[e] = 0.0;
+        }
+    }
+}
+
+void ora_winp_update(const ora_winp *w, int i, double self_weight, const double *r, double *out) {
+    const long long C = w->count;
+    for (long long e = 0; e < C; ++e) out[e] = self_weight * w->x[(size_t)i * C + e];
+    for (int q = 0; q < w->nin[i]; ++q) {
+        const int j = w->in[(size_t)i * w->n + q];
+        const double *b = w->buf + ((size_t)i * w->n + q) * C;
+        for (long long e = 0; e < C; ++e) out[e] += r[j] * b[e];
+    }
+}
+
+void ora_winp_get_x(const ora_winp *w, double *X) {
+    memcpy(X, w->x, sizeof(double) * (size_t)w->n * w->count);
+}
+
+/* ========================================================================
+ * ATC-DSGD fixed point on the decentralized least-squares problem (Eq. 12
+ * P:432-435, DGD/ATC Eq. 13-14 P:440-441 with Eq. 17): the unique X with
+ *     x_i = sum_j w_ij (x_j - gamma A_j^T (A_j x_j - b_j)),
+ * found by iterating that map in fp64 from X (in: start, out: x_inf) until the
+ * largest change is <= tol * max|X|.  Returns the iterations used, or -1 if
+ * max_iter was reached.  A: n x m x d, b: n x m, X: n x d.
+ * ====================================================================== */
+int ora_atc_fixed_point(int n, int m, int d, const double *W, const double *A, const double *b, double lr,
+                        double tol, int max_iter, double *X) {
+    double *xh = (double *)malloc(sizeof(double) * (size_t)n * d);
+    double *Xn = (double *)malloc(sizeof(double) * (size_t)n * d);
+    double *g = (double *)malloc(sizeof(double) * (size_t)d);
+    int it = 0;
+    for (; it < max_iter; ++it) {
+        for (int i = 0; i < n; ++i) {   /* Eq. 4 in fp64: x_half = x - gamma g_i(x_i) */
+            ora_lsq_grad(m, d, A + (size_t)i * m * d, b + (size_t)i * m, X + (size_t)i * d, g);
+            for (int c = 0; c < d; ++c) xh[(size_t)i * d + c] = X[(size_t)i * d + c] - lr * g[c];
+        }
+        ora_mix(n, d, W, xh, Xn);       /* Eq. 5 */
+        double dmax = 0.0, xmax = 0.0;
+        for (long long q = 0; q < (long long)n * d; ++q) {
+            dmax = fmax(dmax, fabs(Xn[q] - X[q]));
+            xmax = fmax(xmax, fabs(Xn[q]));
+            X[q] = Xn[q];
+        }
+        if (dmax <= tol * xmax) { ++it; break; }
+    }
+    free(xh); free(Xn); free(g);
+    return it >= max_iter ? -1 : it;
 }

@@ -66,6 +66,20 @@ void ora_awc(int n, long long count, const double *W, const double *X,
 void ora_hier(int n_machines, int local_size, long long count, const double *WM,
               const double *X, double *Y);
 
+/* H-ATC / H-AWC (caption P:869): Eq. 17 / Eq. 16 with the hierarchical combine */
+void ora_hier_atc(int n_machines, int local_size, long long count, const double *WM,
+                  const double *X, const double *G, double lr, double *Y);
+void ora_hier_awc(int n_machines, int local_size, long long count, const double *WM,
+                  const double *X, const double *G, double lr, double *Y);
+
+/* ---- push-sum gradient tracking (appendix) -------
+ * (a) u+ = W(u - lr y), v+ = W v, x+ = u+ / v+ ; (b) y+ = W(y + g+ - g).
+ * V has dv = d columns (the paper's vector v) or dv = 1 (one weight per agent). */
+void ora_gt_uv(int n, long long d, long long dv, const double *W, const double *U, const double *V,
+               const double *Y, double lr, double *Un, double *Vn, double *Xn);
+void ora_gt_y(int n, long long d, const double *W, const double *Y, const double *Gnew,
+              const double *Gprev, double *Yn);
+
 /* ---- casts ---------------------------------------------------------------- */
 uint16_t ora_bf16_rne(float f);
 float ora_f32(double v);
@@ -90,11 +104,28 @@ void ora_win_get_x(const ora_win *w, double *X);            /* n*count */
 double ora_win_mass(const ora_win *w, long long e);         /* total mass of element e */
 void ora_win_counters(const ora_win *w, int dst, int src, long long *version, long long *consumed);
 
+/* ---- paper-semantics window ------------------
+ * One plain buffer per in-neighbour: put overwrites, accumulate adds, collect
+ * sums into x then zeroes, update reads without reset.  No protocol state. */
+typedef struct ora_winp ora_winp;
+ora_winp *ora_winp_create(int n, long long count, const double *Wstatic, const double *X0, int zero_init);
+void ora_winp_free(ora_winp *w);
+int ora_winp_accumulate(ora_winp *w, int i, double self_weight, const double *s, const int *dst_mask,
+                        int overwrite);
+void ora_winp_collect(ora_winp *w, int i);
+void ora_winp_update(const ora_winp *w, int i, double self_weight, const double *r, double *out);
+void ora_winp_get_x(const ora_winp *w, double *X);
+
 /* ---- least squares (Eq. 12-13) ------------------------------- */
 void ora_lsq_grad(int m, int d, const double *A, const double *b, const double *x, double *g);
 /* CG on sum_i A_i^T A_i x = sum_i A_i^T b_i; returns iterations */
 int ora_lsq_solve(int n, int m, int d, const double *A, const double *b, double tol,
                   int max_iter, double *x);
+/* ATC-DSGD fixed point x_inf: iterate
+ * X <- W(X - lr (A_i^T(A_i x_i - b_i))_i) in fp64 to stationarity; returns
+ * iterations or -1.  X: start in, x_inf out (n x d). */
+int ora_atc_fixed_point(int n, int m, int d, const double *W, const double *A, const double *b, double lr,
+                        double tol, int max_iter, double *X);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,8 @@ _SIGS = {
     "bf_status_string": (C.c_char_p, [_i]),
     "bf_set_topology": (_i, [_vp, _i, C.POINTER(C.c_double)]),
     "bf_set_machine_topology": (_i, [_vp, _i, _i, C.POINTER(C.c_double)]),
+    "bf_set_topology_local": (_i, [_vp, _wp]),
+    "bf_win_version": (_i, [_vp, C.c_char_p, _i, C.POINTER(_u64)]),
     "bf_in_neighbors": (_i, [_vp, _i, C.POINTER(_i), _i, C.POINTER(_i)]),
     "bf_out_neighbors": (_i, [_vp, _i, C.POINTER(_i), _i, C.POINTER(_i)]),
     "bf_topology_matrix": (_i, [_i, _i, _u64, C.POINTER(C.c_double)]),

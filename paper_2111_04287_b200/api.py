@@ -161,6 +161,24 @@ class Context:
             raise ValueError(f"tensor numel {t.numel()} not divisible by agents_per_proc {self.k}")
         return t.numel() // self.k
 
+    def _dev(self, t: torch.Tensor, what: str = "tensor") -> torch.Tensor:
+        # device-pointer arguments of the C ABI: a CUDA tensor on this context's GPU
+        if not t.is_cuda or t.device.index != self.device:
+            raise ValueError(f"{what} must be a CUDA tensor on cuda:{self.device} (got {t.device})")
+        return t
+
+    def _like(self, t: torch.Tensor, ref: torch.Tensor, what: str, device: bool = True) -> torch.Tensor:
+        # companion tensors (g, psi, out, shadow) are read / written with x's layout
+        if t.dtype not in _DT:
+            raise ValueError(f"{what}: unsupported dtype {t.dtype}")
+        if not t.is_contiguous() or t.numel() != ref.numel():
+            raise ValueError(f"{what} must be contiguous with {ref.numel()} elements (the layout of x)")
+        if device:
+            self._dev(t, what)
+        elif t.device.type != ref.device.type:
+            raise ValueError(f"{what} must live where x lives ({ref.device})")
+        return t
+
     def _views(self, self_weight, src_weights, dst_weights):
         if self_weight is None and src_weights is None and dst_weights is None:
             return None
@@ -170,6 +188,13 @@ class Context:
     def set_topology(self, W) -> bool:
         W = np.ascontiguousarray(np.asarray(W, np.float64))
         check(self.lib.bf_set_topology(self.h, W.shape[0], W.ctypes.data_as(C.POINTER(C.c_double))))
+        return True
+
+    def set_topology_local(self, self_weight, src_weights=None, dst_weights=None) -> bool:
+        """Static topology from local views (collective): each process
+        gives its agents' self / src / dst weights, the library assembles the global W."""
+        v = _Views(self.k, self_weight, src_weights, dst_weights)
+        check(self.lib.bf_set_topology_local(self.h, v.ptr()))
         return True
 
     def set_machine_topology(self, WM, local_size: int) -> bool:
@@ -207,8 +232,11 @@ class Context:
     def neighbor_allreduce(self, tensor: torch.Tensor, self_weight=None, src_weights=None, dst_weights=None,
                            out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         """Eq. 5 / Eq. 9 partial averaging."""
-        count = self._rows(tensor)
+        count = self._rows(self._dev(tensor))
         y = torch.empty_like(tensor) if out is None else out
+        if y.dtype != tensor.dtype:
+            raise ValueError("out must have the dtype of the input")
+        self._like(y, tensor, "out")
         v = self._views(self_weight, src_weights, dst_weights)
         check(self.lib.bf_neighbor_allreduce(self.h, C.c_void_p(tensor.data_ptr()), C.c_void_p(y.data_ptr()),
                                              count, _DT[tensor.dtype], v.ptr() if v else None,
@@ -222,6 +250,12 @@ class Context:
         if x.dtype != torch.float32:
             raise ValueError("x must be the fp32 master copy")
         count = self._rows(x)
+        # x and g may be host tensors (end-to-end path, staged inside the call)
+        self._like(g, x, "g", device=x.is_cuda and g.is_cuda)
+        if shadow is not None:
+            if shadow.dtype != torch.bfloat16:
+                raise ValueError("shadow must be bf16")
+            self._like(shadow, x, "shadow")
         v = self._views(self_weight, src_weights, dst_weights)
         check(self.lib.bf_atc_step(self.h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()), _DT[g.dtype],
                                    count, float(lr), _DT[wire],
@@ -236,7 +270,9 @@ class Context:
         fused in one kernel; x and psi (fp32) are updated in place (psi = x^(0) initially)."""
         if x.dtype != torch.float32 or psi.dtype != torch.float32 or psi.shape != x.shape:
             raise ValueError("x and psi must be fp32 tensors of the same shape")
-        count = self._rows(x)
+        count = self._rows(self._dev(x, "x"))
+        self._like(g, x, "g")
+        self._like(psi, x, "psi")
         v = self._views(self_weight, src_weights, dst_weights)
         check(self.lib.bf_exact_diffusion_step(self.h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()),
                                                _DT[g.dtype], C.c_void_p(psi.data_ptr()), count, float(lr),
@@ -248,7 +284,8 @@ class Context:
         """Fused AWC-DSGD step (Eq. 16): x <- W x - lr*g, in place on the fp32 master x."""
         if x.dtype != torch.float32:
             raise ValueError("x must be the fp32 master copy")
-        count = self._rows(x)
+        count = self._rows(self._dev(x, "x"))
+        self._like(g, x, "g")
         v = self._views(self_weight, src_weights, dst_weights)
         check(self.lib.bf_awc_step(self.h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()), _DT[g.dtype],
                                    count, float(lr), v.ptr() if v else None, _stream_ptr(stream, self.device)))
@@ -281,8 +318,11 @@ class Context:
     def hierarchical_neighbor_allreduce(self, tensor: torch.Tensor, self_weight=None, src_machine_weights=None,
                                         out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         """P:660-675 (machine-level neighbour averaging of machine averages)."""
-        count = self._rows(tensor)
+        count = self._rows(self._dev(tensor))
         y = torch.empty_like(tensor) if out is None else out
+        if y.dtype != tensor.dtype:
+            raise ValueError("out must have the dtype of the input")
+        self._like(y, tensor, "out")
         v = self._views(self_weight, src_machine_weights, None)
         check(self.lib.bf_hierarchical_neighbor_allreduce(self.h, C.c_void_p(tensor.data_ptr()),
                                                           C.c_void_p(y.data_ptr()), count, _DT[tensor.dtype],
@@ -302,9 +342,8 @@ class Context:
     def _hier_step(self, fn, x, g, lr, self_weight, src_machine_weights, stream):
         if x.dtype != torch.float32:
             raise ValueError("x must be the fp32 master copy")
-        count = self._rows(x)
-        if g.shape != x.shape or not g.is_contiguous():
-            raise ValueError("g must be contiguous with the shape of x")
+        count = self._rows(self._dev(x, "x"))
+        self._like(g, x, "g")
         v = self._views(self_weight, src_machine_weights, None)
         check(fn(self.h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()), _DT[g.dtype], count, float(lr),
                  v.ptr() if v else None, _stream_ptr(stream, self.device)))
@@ -312,7 +351,7 @@ class Context:
 
     # ---- windows ---------------------------------------------------
     def win_create(self, tensor: torch.Tensor, name: str, zero_init: bool = True, with_p: bool = False) -> bool:
-        count = self._rows(tensor)
+        count = self._rows(self._dev(tensor))
         torch.cuda.synchronize(self.device)
         check(self.lib.bf_win_create(self.h, name.encode(), C.c_void_p(tensor.data_ptr()), count,
                                      _DT[tensor.dtype], 1 if zero_init else 0, 1 if with_p else 0))
@@ -373,6 +412,10 @@ class Context:
 
     def win_update(self, name: str, self_weight=None, src_weights=None, out: Optional[torch.Tensor] = None,
                    agent_mask: int = 0, stream=None):
+        if out is not None:
+            self._dev(out, "out")
+            if not out.is_contiguous():
+                raise ValueError("out must be contiguous")
         v = self._views(self_weight, src_weights, None)
         check(self.lib.bf_win_update(self.h, name.encode(), v.ptr() if v else None,
                                      C.c_void_p(out.data_ptr()) if out is not None else None, agent_mask,
@@ -393,6 +436,11 @@ class Context:
         v, c = C.c_uint64(), C.c_uint64()
         check(self.lib.bf_win_counters(self.h, name.encode(), dst_local, src_rank, C.byref(v), C.byref(c)))
         return v.value, c.value
+
+    def win_version(self, name: str, src_rank: int) -> int:
+        v = C.c_uint64()
+        check(self.lib.bf_win_version(self.h, name.encode(), int(src_rank), C.byref(v)))
+        return v.value
 
     def win_slot_offset(self, name: str, agent: int, src_rank: int) -> int:
         return self.lib.bf_win_slot_offset(self.h, name.encode(), agent, src_rank)

@@ -46,6 +46,15 @@ struct Desc {
     float s[kMaxN];                // s_j: weight for destination j
 };
 
+// Static local view of one agent (bf_set_topology_local): published in
+// the agent's pad so every process can assemble the same global W.
+struct LocalView {
+    double self_w;
+    int nsrc, ndst;                // -1: not given
+    unsigned char src[kMaxS], dst[kMaxS];
+    double r[kMaxS], s[kMaxS];
+};
+
 struct Pad {
     unsigned long long epoch;      // last completed exchange epoch of this process
     unsigned long long round;      // device-resident one-peer schedule round
@@ -55,6 +64,7 @@ struct Pad {
     unsigned long long done_from[kMaxP];   // done_from[q] = last epoch process q finished reading
     unsigned long long bar_from[kMaxP];    // device barrier arrivals
     Desc desc[kMaxK][2];
+    LocalView lview[kMaxK];
 };
 static_assert(sizeof(Pad) <= kPadBytes, "pad too large");
 

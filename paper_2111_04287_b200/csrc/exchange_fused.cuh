@@ -101,8 +101,8 @@ struct FusedCfg {
 template <int K>
 struct LocalMix {
     float c[K][K];                     // c[a][b]: weight of local agent b in agent a's combine
-    float rc[K * kMaxS];               // remote entries, agent-major: weight ...
-    unsigned char rs[K * kMaxS];       // ... and global source agent
+    float rc[K * kMaxN];               // remote entries, agent-major: weight ...
+    unsigned char rs[K * kMaxN];       // ... and global source agent (push-only views: up to n - 1 each)
     int rbeg[K + 1];                   // entries of agent a: [rbeg[a], rbeg[a+1])
     unsigned pub;                      // bit a: agent a's x_half is read by another process
     unsigned procs;                    // bit q: process q hosts a remote source
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                 const int done = min((rb + 1) * kBatch, nmine);
                 BF_STAT(const unsigned long long tf = globaltimer();)
                 fence_acq_rel(true);   // the consumers' slot stores, visible system-wide ...
-                BF_STAT(if (stat) { stat[V] += globaltimer() - tf; stat[5] += 1; })
+                BF_STAT(if (stat) { stat[4] += globaltimer() - tf; stat[5] += 1; })
                 st_relaxed(prog, (e << kProgShift) | static_cast<unsigned long long>(done), true);   // ... first
                 *released = rb + 1;
             }

@@ -107,6 +107,12 @@ struct bf_ctx {
     unsigned long long *stats = nullptr;      // BF_STATS=1: per-CTA diagnostics of the fused kernel
     int hier_mode = 0;                        // BF_HIER: 0 auto, 1 staged (always), 2 fused (also across GPUs)
     bool win_ef = false;                      // BF_WIN_EF=1: new windows start with error feedback on
+    // stream order across calls: every call of a context reads and advances the same
+    // device state (epoch, round, slots, progress words), so a call issued on another
+    // stream than the previous one first waits for the previous stream's work
+    cudaStream_t last_stream = nullptr;
+    bool have_last = false;
+    cudaEvent_t order_ev = nullptr;
 };
 
 bf_status bf_barrier_internal(bf_ctx *c);
@@ -126,6 +132,23 @@ bf_status check_ctx(bf_ctx *c, bool need_connected = true) {
     cudaGetDevice(&dev);
     if (dev != c->device) cudaSetDevice(c->device);
     return BF_OK;
+}
+
+// Serialise this call after the context's previous call when they are issued on
+// different streams (a non-blocking call on a side stream followed by any other
+// call).  Same stream: nothing to do (stream order).  Inside a CUDA
+// graph capture the captured dependencies fix the order, so nothing is recorded.
+void order_stream(bf_ctx *c, cudaStream_t st) {
+    if (c->have_last && st != c->last_stream && c->order_ev) {
+        cudaStreamCaptureStatus a = cudaStreamCaptureStatusNone, b = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &a) == cudaSuccess && cudaStreamIsCapturing(c->last_stream, &b) == cudaSuccess &&
+            a == cudaStreamCaptureStatusNone && b == cudaStreamCaptureStatusNone) {
+            if (cudaEventRecord(c->order_ev, c->last_stream) == cudaSuccess) cudaStreamWaitEvent(st, c->order_ev, 0);
+        }
+        cudaGetLastError();   // a stream the caller destroyed since: nothing left to wait for
+    }
+    c->last_stream = st;
+    c->have_last = true;
 }
 
 bf_status heap_alloc(bf_ctx *c, size_t bytes, unsigned long long *off) {
@@ -156,6 +179,20 @@ Geometry make_geo(bf_ctx *c, size_t count) {
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// A newly allocated (and zeroed) symmetric region becomes visible to the peers
+// only after every process has zeroed its copy: peers read our progress words and
+// flags, and an unzeroed reused region holds stale data that would read as
+// "published".  Zeroing finished on this device, then a barrier (collective: the
+// callers make the same allocation on every process).
+bf_status publish_region(bf_ctx *c) {
+    if (c->nprocs == 1) return BF_OK;
+    CU(cudaDeviceSynchronize());
+    bf_status s = bf_barrier_internal(c);
+    if (s) return s;
+    CU(cudaDeviceSynchronize());
+    return BF_OK;
+}
 
 // Exchange region: double-buffered slots + per-tile ready flags of every local
 // agent.  Grows on demand (collective: every process makes the same call):
@@ -194,7 +231,7 @@ bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
     c->ready_stride = tmax;
     c->exch_begin = begin;
     c->exch_top = c->heap_used;
-    return BF_OK;
+    return publish_region(c);
 }
 
 bool is_finite_w(double v) { return std::isfinite(v); }
@@ -441,6 +478,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->d_err), h, 0);
     c->W.assign(static_cast<size_t>(c->n) * c->n, 1.0 / c->n);   // default: fully connected (R15)
     c->peer_base[proc_rank] = reinterpret_cast<unsigned long long>(c->heap);
+    cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming);
     cudaDeviceSynchronize();
     *out = c;
     return BF_OK;
@@ -498,6 +536,7 @@ bf_status bf_finalize(bf_ctx *c) {
     if (c->stage_g) cudaFree(c->stage_g);
     if (c->stats) cudaFree(c->stats);
     if (c->h_err) cudaFreeHost(const_cast<unsigned int *>(c->h_err));
+    if (c->order_ev) cudaEventDestroy(c->order_ev);
     delete c;
     return BF_OK;
 }
@@ -560,6 +599,92 @@ bf_status bf_set_topology(bf_ctx *c, int n, const double *W) {
     return BF_OK;
 }
 
+// Static topology from local views (P:378-381 self/src/dst; Eq. 9):
+// every process publishes its agents' views in its pad, a barrier, then every
+// process reads all pads and assembles the same global W:
+//   w_ii = self_weight_i;
+//   j in src_i:            w_ij = r_ij * (s_ij if j lists i as destination, else 1)   (R1)
+//   i gives no src list:   w_ij = s_ij for every j that lists i as destination        (push, R16)
+// With the topology check on, a receiver with a src list must list exactly the
+// senders that name it: else BF_ERR_TOPOLOGY on every process.
+bf_status bf_set_topology_local(bf_ctx *c, const bf_weights *weights) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!weights) return fail(BF_ERR_ARG, "null local views");
+    std::vector<LocalView> mine(c->k);
+    for (int a = 0; a < c->k; ++a) {
+        const int gid = c->proc * c->k + a;
+        const bf_weights &w = weights[a];
+        if ((s = validate_view(c, gid, w, true, true, c->n))) return s;
+        LocalView &v = mine[a];
+        memset(&v, 0, sizeof(v));
+        v.self_w = w.self_weight;
+        v.nsrc = w.n_src;
+        v.ndst = w.n_dst;
+        for (int q = 0; q < w.n_src; ++q) {
+            v.src[q] = static_cast<unsigned char>(w.src_ranks[q]);
+            v.r[q] = w.src_weights[q];
+        }
+        for (int q = 0; q < w.n_dst; ++q) {
+            v.dst[q] = static_cast<unsigned char>(w.dst_ranks[q]);
+            v.s[q] = w.dst_weights[q];
+        }
+    }
+    Pad *pad = reinterpret_cast<Pad *>(c->heap);
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(pad->lview, mine.data(), sizeof(LocalView) * c->k, cudaMemcpyHostToDevice));
+    if ((s = publish_region(c))) return s;   // every pad written before anyone reads
+    std::vector<LocalView> all(c->n);
+    for (int q = 0; q < c->nprocs; ++q) {
+        const Pad *pq = reinterpret_cast<const Pad *>(c->peer_base[q]);
+        CU(cudaMemcpy(&all[static_cast<size_t>(q) * c->k], pq->lview, sizeof(LocalView) * c->k,
+                      cudaMemcpyDeviceToHost));
+    }
+    if ((s = publish_region(c))) return s;   // nobody overwrites a pad another process still reads
+    const int n = c->n;
+    std::vector<double> W(static_cast<size_t>(n) * n, 0.0);
+    auto sends = [&](int j, int i, double *sw) {   // does j list i as destination, with which s
+        const LocalView &v = all[j];
+        for (int q = 0; q < std::max(v.ndst, 0); ++q)
+            if (v.dst[q] == i) {
+                *sw = v.s[q];
+                return true;
+            }
+        return false;
+    };
+    for (int i = 0; i < n; ++i) {
+        const LocalView &v = all[i];
+        W[static_cast<size_t>(i) * n + i] = v.self_w;
+        if (v.nsrc >= 0) {
+            for (int q = 0; q < v.nsrc; ++q) {
+                double sw = 1.0;
+                const int j = v.src[q];
+                const bool pushed = sends(j, i, &sw);
+                if (c->topo_check && all[j].ndst >= 0 && !pushed)
+                    return fail(BF_ERR_TOPOLOGY, "agent %d lists %d as source, but %d does not send to %d (P:382)", i,
+                                j, j, i);
+                W[static_cast<size_t>(i) * n + j] = v.r[q] * (pushed ? sw : 1.0);
+            }
+            if (c->topo_check)
+                for (int j = 0; j < n; ++j) {
+                    double sw;
+                    if (j == i || !sends(j, i, &sw)) continue;
+                    bool listed = false;
+                    for (int q = 0; q < v.nsrc; ++q) listed |= v.src[q] == j;
+                    if (!listed)
+                        return fail(BF_ERR_TOPOLOGY, "agent %d sends to %d, which does not list it as source (P:382)",
+                                    j, i);
+                }
+        } else {
+            for (int j = 0; j < n; ++j) {
+                double sw;
+                if (j != i && sends(j, i, &sw)) W[static_cast<size_t>(i) * n + j] = sw;
+            }
+        }
+    }
+    return bf_set_topology(c, n, W.data());
+}
+
 bf_status bf_set_machine_topology(bf_ctx *c, int local_size, int n_machines, const double *WM) {
     bf_status s = check_ctx(c, false);
     if (s) return s;
@@ -606,7 +731,8 @@ bf_status bf_set_dynamic_schedule(bf_ctx *c, int kind, uint64_t round0) {
     c->sched_L = kind == 2 ? c->machine_L : 1;
     if (kind) {
         Pad *pad = reinterpret_cast<Pad *>(c->heap);
-        CU(launch_set_u64(&pad->round, round0, nullptr));
+        order_stream(c, nullptr);
+    CU(launch_set_u64(&pad->round, round0, nullptr));
         c->launches++;
         CU(cudaDeviceSynchronize());
     }
@@ -649,7 +775,10 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     if ((count + kTile - 1) / kTile > static_cast<size_t>(c->ready_stride))
         return fail(BF_ERR_NOMEM, "too many tiles for the reserved exchange region");
     p.geo = make_geo(c, count);
-    p.geo.vec_ok = (count % 4 == 0) && aligned16(x) && aligned16(y) && (!g || aligned16(g)) &&
+    // rows of agent a start at a * count elements: 16-byte vectors need count to be a
+    // multiple of the vector width (4 fp32, 8 bf16 elements per 16 bytes)
+    const size_t vwidth = (x_kind == 1 || y_kind == 1) ? 8 : 4;
+    p.geo.vec_ok = (count % vwidth == 0) && aligned16(x) && aligned16(y) && (!g || aligned16(g)) &&
                    (!shadow || aligned16(shadow));
     p.x_kind = x_kind;
     p.wire_kind = wire_kind;
@@ -694,6 +823,7 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
         p.psi = psi;
     }
     p.cflag_off = c->cflag_off;
+    order_stream(c, st);
     CU(launch_exchange(p, x_kind, awc_g ? x_kind : g_kind, wire_kind, y_kind, g != nullptr, 0, st));
     c->launches++;
     return BF_OK;
@@ -724,6 +854,7 @@ bf_status bf_atc_step(bf_ctx *c, float *x, const void *g, bf_dtype g_dtype, size
     float *xd = x;
     const void *gd = g;
     const bool x_host = is_host_ptr(x), g_host = is_host_ptr(g);
+    if (x_host || g_host) order_stream(c, st);
     if (x_host) {   // end-to-end path: stage the host tensors through device memory
         s = ensure_stage(&c->stage_x, &c->stage_x_bytes, rows * 4);
         if (s) return s;
@@ -904,6 +1035,7 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
         c->bc_agent_stride = 2 * bytes;
         c->bc_parity_stride = bytes;
         c->hier_ready = true;
+        if ((s = publish_region(c))) return s;
     }
     p.geo = make_geo(c, count);
     p.geo.vec_ok = (count % 4 == 0) && aligned16(x) && aligned16(y) && (!hmode || aligned16(g));
@@ -930,6 +1062,7 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
     p.fc_off = c->fc_off;
     p.bc_agent_stride = c->bc_agent_stride;
     p.bc_parity_stride = c->bc_parity_stride;
+    order_stream(c, static_cast<cudaStream_t>(stream));
     CU(launch_hier(p, dtype, 0, static_cast<cudaStream_t>(stream)));
     c->launches++;
     return BF_OK;
@@ -1118,6 +1251,7 @@ static bf_status win_push(bf_ctx *c, const char *name, const bf_weights *weights
         }
         p.nout[a] = static_cast<unsigned char>(v.n_dst > 0 ? v.n_dst : 0);
     }
+    order_stream(c, static_cast<cudaStream_t>(stream));
     CU(launch_win_push(p, 0, static_cast<cudaStream_t>(stream)));
     c->launches += 2;
     return BF_OK;
@@ -1172,6 +1306,7 @@ static bf_status win_pull(bf_ctx *c, const char *name, const bf_weights *weights
             }
         }
     }
+    order_stream(c, static_cast<cudaStream_t>(stream));
     CU(launch_win_collect(p, update, 0, static_cast<cudaStream_t>(stream)));
     c->launches += 2;
     return BF_OK;
@@ -1219,6 +1354,7 @@ bf_status bf_win_get(bf_ctx *c, const char *name, const bf_weights *weights, uin
             }
         }
     }
+    order_stream(c, static_cast<cudaStream_t>(stream));
     CU(launch_win_get(p, static_cast<unsigned long long>(xp - c->heap), static_cast<cudaStream_t>(stream)));
     c->launches += 2;
     return BF_OK;
@@ -1261,6 +1397,21 @@ bf_status bf_win_counters(bf_ctx *c, const char *name, int dst_local, int src_ra
     return BF_OK;
 }
 
+bf_status bf_win_version(bf_ctx *c, const char *name, int src_rank, uint64_t *version) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    Window *w = find_win(c, name);
+    if (!w) return fail(BF_ERR_WINDOW, "unknown window '%s'", name ? name : "(null)");
+    if (!version) return fail(BF_ERR_ARG, "null version");
+    for (int a = 0; a < c->k; ++a) {   // the first local agent that has src_rank as an in-neighbour
+        const auto &ins = w->side[c->proc * c->k + a].in;
+        if (std::find(ins.begin(), ins.end(), src_rank) == ins.end()) continue;
+        uint64_t consumed;
+        return bf_win_counters(c, name, a, src_rank, version, &consumed);
+    }
+    return fail(BF_ERR_WINDOW, "rank %d is not an in-neighbour of a local agent", src_rank);
+}
+
 long long bf_win_slot_offset(bf_ctx *c, const char *name, int agent, int src_rank) {
     if (!c) return -1;
     Window *w = find_win(c, name);
@@ -1277,6 +1428,7 @@ bf_status bf_barrier(bf_ctx *c, void *stream) {
     if (s) return s;
     if (c->nprocs == 1) return BF_OK;
     Geometry g = make_geo(c, 0);
+    order_stream(c, static_cast<cudaStream_t>(stream));
     CU(launch_barrier(g, ++c->bar_epoch, static_cast<cudaStream_t>(stream)));
     c->launches++;
     return BF_OK;

@@ -30,3 +30,18 @@ def test_multiprocess_parity(nproc, k, hier):
     out = res.stdout + res.stderr
     assert res.returncode == 0, out[-4000:]
     assert out.count("ALL OK") == nproc, out[-4000:]
+
+
+@pytest.mark.parametrize("nproc,k", [(2, 1), (2, 2), (4, 1), (4, 2)])
+def test_multiprocess_production_shape(nproc, k):
+    # 25.6M fp32 per agent (the 8-GPU target's per-GPU shape at k = 1), every fused
+    # op over consecutive rounds, windows with more items than CTAs (mp_worker_big.py)
+    if _ngpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    env = dict(os.environ, BF_TEST_K=str(k), BF_TIMEOUT_MS="10000")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(ROOT, "tests", "mp_worker_big.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert out.count("ALL OK") == nproc, out[-4000:]

@@ -562,3 +562,236 @@ def test_gradient_tracking_invariants_and_convergence():
         assert np.allclose(Y.sum(axis=0), G.sum(axis=0), rtol=0, atol=1e-9)
     assert np.abs(X - xs[None, :]).max() < 1e-8      # exact convergence on a directed graph
     assert np.abs(V - 1).max() > 1e-2                 # and the push-sum weights really matter
+
+
+# ------------------------------------------- hand examples with a nonzero step ---
+def test_awc_hand_example_nonzero_lr():
+    # Eq. 16: the gradient term with gamma != 0, checked by hand
+    g = golden("awc_hier_hand_examples.json")["awc"]
+    W = np.full((2, 2), 0.5)
+    Y = ora.awc(W, np.array(g["x"])[:, None], np.array(g["g"])[:, None], g["lr"])
+    assert np.array_equal(Y[:, 0], np.array(g["expected"]))
+
+
+def test_hier_atc_awc_hand_examples_nonzero_lr():
+    # caption P:869 H-ATC / H-AWC on 2 machines x 2 agents, hand-computed values
+    g = golden("awc_hier_hand_examples.json")["hier"]
+    X = np.array(g["x"])[:, None]
+    G = np.array(g["g"])[:, None]
+    I2, U2 = np.eye(2), np.full((2, 2), 0.5)
+    assert np.array_equal(ora.hier_atc(I2, 2, X, G, g["lr"])[:, 0], g["atc_identity"])
+    assert np.array_equal(ora.hier_atc(U2, 2, X, G, g["lr"])[:, 0], g["atc_uniform"])
+    assert np.array_equal(ora.hier_awc(I2, 2, X, G, g["lr"])[:, 0], g["awc_identity"])
+    assert np.array_equal(ora.hier_awc(U2, 2, X, G, g["lr"])[:, 0], g["awc_uniform"])
+
+
+# --------------------------------------------------------- win_update pins ---
+@pytest.mark.parametrize("model", ["event", "paper"])
+def test_win_update_spec_example_and_idempotent(model):
+    # S:454 ring(3) example: local 0, in-neighbours put 3 and 9,
+    # uniform 1/3 -> 4; a second call with no traffic in between returns the same
+    g = golden("spec_win_update_example.json")
+    n = g["n"]
+    W = ora.ring(n)
+    X0 = np.array([[g["local"]], [g["puts"]["1"]], [g["puts"]["2"]]])
+    Win = ora.Window if model == "event" else ora.WindowPaper
+    win = Win(W, X0, zero_init=True)
+    win.put(1, 1.0, {0: 1.0})
+    win.put(2, 1.0, {0: 1.0})
+    u = 1.0 / (len(ora.in_neighbors(W, 0)) + 1)
+    out1 = win.update(0, u, {1: u, 2: u})
+    out2 = win.update(0, u, {1: u, 2: u})
+    assert abs(out1[0] - g["expected"]) < 1e-15
+    assert np.array_equal(out1, out2)
+    assert win.x()[0, 0] == g["local"]            # update does not touch x (no collect)
+    # zero-initialised buffers before any traffic contribute nothing
+    X1 = np.full((n, 1), g["zero_init_local"])
+    win = Win(W, X1, zero_init=True)
+    assert abs(win.update(0, u, {1: u, 2: u})[0] - g["zero_init_expected"]) < 1e-15
+    # not zero-initialised: buffers hold the local tensor, uniform average returns x
+    win = Win(W, X1, zero_init=False)
+    assert abs(win.update(0, u, {1: u, 2: u})[0] - g["zero_init_local"]) < 1e-14
+
+
+def test_win_update_weights_select_sources():
+    # P:420 win_update(name, self_weight, src_weights): explicit weights, one source at 0
+    W = ora.ring(3)
+    X0 = np.array([[1.0], [2.0], [5.0]])
+    for Win in (ora.Window, ora.WindowPaper):
+        win = Win(W, X0, zero_init=True)
+        win.put(1, 1.0, {0: 1.0})
+        win.put(2, 1.0, {0: 1.0})
+        assert win.update(0, 0.25, {1: 0.75, 2: 0.0})[0] == 0.25 * 1.0 + 0.75 * 2.0
+
+
+# ------------------------ paper-semantics window vs the double-buffered model ---
+def _fig2_W():
+    gold = golden("fig2_neighbor_sets.json")
+    return gold["n"], _edges_to_W(gold["n"], gold["edges_1indexed"], one_indexed=True)
+
+
+def test_paper_window_accumulate_collect_by_hand():
+    # P:402-403 accumulate adds into the neighbour's buffer; P:585 collect sums, then zeroes
+    W2 = np.array([[1.0, 1.0], [1.0, 1.0]])
+    win = ora.WindowPaper(W2, np.array([[1.0], [2.0]]), zero_init=True)
+    win.accumulate(1, 0.5, {0: 0.5})      # buffer_0[1] = 1, x_1 = 1
+    win.accumulate(1, 1.0, {0: 2.0})      # buffer_0[1] = 1 + 2 = 3
+    assert win.update(0, 0.0, {1: 1.0})[0] == 3.0
+    win.collect(0)
+    assert win.x()[:, 0].tolist() == [4.0, 1.0]
+    win.collect(0)                        # buffers were zeroed: nothing more arrives
+    assert win.x()[:, 0].tolist() == [4.0, 1.0]
+    win.put(1, 1.0, {0: 7.0})             # put overwrites
+    win.put(1, 1.0, {0: 1.0})
+    assert win.update(0, 0.0, {1: 1.0})[0] == 1.0
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_event_model_equals_paper_window_without_backlog(seed):
+    # Whenever no payload has to wait in a sender's outbox (the destination half is
+    # free at every accumulate), the double-buffered protocol model gives exactly the
+    # paper's window: x after every event equal (push-sum, Listing 3 weights)
+    n, Wst = _fig2_W()
+    cnt = 3
+    X = np.concatenate([synthetic.agents_x0(n, cnt - 1).astype(np.float64), np.ones((n, 1))], axis=1)
+    ev, pw = ora.Window(Wst, X, zero_init=True), ora.WindowPaper(Wst, X, zero_init=True)
+    rng = np.random.default_rng(seed)
+    n_acc = 0
+    for _ in range(3000):
+        i = int(rng.integers(n))
+        outs = ora.out_neighbors(Wst, i)
+        free = all(ev.counters(j, i)[1] >= ev.counters(j, i)[0] - 1 for j in outs)
+        if rng.random() < 0.5 and free:
+            w = 1.0 / (len(outs) + 1)
+            ev.accumulate(i, w, {j: w for j in outs})
+            pw.accumulate(i, w, {j: w for j in outs})
+            n_acc += 1
+        else:
+            ev.collect(i)
+            pw.collect(i)
+        assert np.allclose(ev.x(), pw.x(), rtol=0, atol=1e-13)
+    assert n_acc > 500
+
+
+def test_event_model_equals_paper_window_put_update():
+    # put + win_update: the latest payload of each slot is the
+    # paper's buffer value, whenever the half was free at the put
+    n, Wst = _fig2_W()
+    X = synthetic.agents_x0(n, 4).astype(np.float64)
+    ev, pw = ora.Window(Wst, X, zero_init=False), ora.WindowPaper(Wst, X, zero_init=False)
+    rng = np.random.default_rng(9)
+    for step in range(400):
+        i = int(rng.integers(n))
+        if rng.random() < 0.5:
+            outs = ora.out_neighbors(Wst, i)
+            s = {j: float(rng.uniform(-1, 1)) for j in outs if rng.random() < 0.7}
+            if all(ev.counters(j, i)[1] >= ev.counters(j, i)[0] - 1 for j in s):
+                sw = float(rng.uniform(0.5, 1.5))
+                ev.put(i, sw, s)
+                pw.put(i, sw, s)
+        else:
+            ins = ora.in_neighbors(Wst, i)
+            r = {j: float(rng.uniform(-1, 1)) for j in ins}
+            sw = float(rng.uniform(-1, 1))
+            assert np.allclose(ev.update(i, sw, r), pw.update(i, sw, r), rtol=0, atol=1e-13)
+        assert np.allclose(ev.x(), pw.x(), rtol=0, atol=1e-13)
+
+
+def test_event_model_with_backlog_conserves_the_paper_mass():
+    # with backlog a payload reaches its destination later than in the paper's window
+    # (it waits in the outbox), so the trajectories differ -- asynchronous results are
+    # interleaving-dependent (R19) -- but after a drain (every payload delivered and
+    # collected) both models hold the same total mass sum_i x_i = sum_i x_i^0
+    n, Wst = _fig2_W()
+    X = np.concatenate([synthetic.agents_x0(n, 2).astype(np.float64), np.ones((n, 1))], axis=1)
+    ev, pw = ora.Window(Wst, X, zero_init=True), ora.WindowPaper(Wst, X, zero_init=True)
+    rng = np.random.default_rng(3)
+    for _ in range(2000):
+        i = int(rng.integers(n))
+        outs = ora.out_neighbors(Wst, i)
+        if rng.random() < 0.7:   # producers run ahead of the consumers: outboxes fill
+            w = 1.0 / (len(outs) + 1)
+            ev.accumulate(i, w, {j: w for j in outs})
+            pw.accumulate(i, w, {j: w for j in outs})
+        else:
+            ev.collect(i)
+            pw.collect(i)
+    # drain: zero-weight accumulates flush the outboxes (self 1, s 0 adds nothing new)
+    for _ in range(4):
+        for i in range(n):
+            outs = ora.out_neighbors(Wst, i)
+            ev.accumulate(i, 1.0, {j: 0.0 for j in outs})
+            pw.accumulate(i, 1.0, {j: 0.0 for j in outs})
+        for i in range(n):
+            ev.collect(i)
+            pw.collect(i)
+    assert np.allclose(ev.x().sum(axis=0), X.sum(axis=0), rtol=0, atol=1e-12)
+    assert np.allclose(pw.x().sum(axis=0), X.sum(axis=0), rtol=0, atol=1e-12)
+    assert np.abs(ev.x() - pw.x()).max() > 1e-6      # the interleavings really differed
+
+
+# -------------------------------------------------- ATC fixed point x_inf ---
+def _atc_fixed_point_linear_solve(W, A, b, lr):
+    # the fixed point written as one linear system (a library solve, independent of
+    # the oracle's iteration): vec X = (W kron I)(vec X - lr (H vec X - c))
+    n, m, d = A.shape
+    H = np.zeros((n * d, n * d))
+    c = np.zeros(n * d)
+    for i in range(n):
+        H[i * d:(i + 1) * d, i * d:(i + 1) * d] = A[i].T @ A[i]
+        c[i * d:(i + 1) * d] = A[i].T @ b[i]
+    Wk = np.kron(W, np.eye(d))
+    M = np.eye(n * d) - Wk @ (np.eye(n * d) - lr * H)
+    return np.linalg.solve(M, lr * Wk @ c).reshape(n, d)
+
+
+@pytest.mark.parametrize("topo", ["ring", "exp2", "one_peer0"])
+def test_atc_fixed_point_matches_linear_solve(topo):
+    # x_inf, the unique fixed point of X = W(X - gamma(HX - c))
+    n = 4
+    A, b, xs = _lsq_problem(n, m=12, d=5, seed=11)
+    W = {"ring": ora.ring(n), "exp2": ora.exp2(n), "one_peer0": ora.one_peer_exp2(n, 0)}[topo]
+    lr = 0.3
+    X, it = ora.atc_fixed_point(W, A, b, lr)
+    ref = _atc_fixed_point_linear_solve(W, A, b, lr)
+    assert np.abs(X - ref).max() < 1e-12 * np.abs(ref).max(), (np.abs(X - ref).max(), it)
+    # uniqueness: any start reaches the same point (linear contraction)
+    X2, _ = ora.atc_fixed_point(W, A, b, lr, X0=np.random.default_rng(1).standard_normal((n, 5)) * 10)
+    assert np.abs(X2 - X).max() < 1e-12 * np.abs(ref).max()
+
+
+def test_atc_fixed_point_special_cases():
+    n = 4
+    A, b, xs = _lsq_problem(n, m=12, d=5, seed=11)
+    # full averaging (W = J/n): every row is the global minimiser x* (the mean gradient vanishes)
+    X, _ = ora.atc_fixed_point(ora.full(n), A, b, 0.3)
+    assert np.abs(X - xs[None, :]).max() < 1e-12
+    # one agent: plain gradient descent's fixed point is its own least-squares solution
+    x1 = np.linalg.lstsq(A[0], b[0], rcond=None)[0]
+    X1, _ = ora.atc_fixed_point(np.eye(1), A[:1], b[:1], 0.3)
+    assert np.abs(X1[0] - x1).max() < 1e-12
+    # ring with distinct data: ATC stops at an O(gamma) bias from x* (the bias
+    # Exact-Diffusion corrects, appendix); halving gamma roughly halves it
+    e1 = np.abs(ora.atc_fixed_point(ora.ring(n), A, b, 0.2)[0] - xs).max()
+    e2 = np.abs(ora.atc_fixed_point(ora.ring(n), A, b, 0.1)[0] - xs).max()
+    assert e1 > 1e-4 and 1.6 < e1 / e2 < 2.4, (e1, e2)
+
+
+# ------------------------------------------------ gradient-tracking halves ---
+def test_gradient_tracking_halves_by_hand_and_vector_v():
+    # lines 1002-1006 on 2 agents, W = [[1/2,1/2],[1/2,1/2]], hand values
+    W = np.full((2, 2), 0.5)
+    U = np.array([[2.0], [4.0]]); V = np.array([[1.0], [3.0]]); Y = np.array([[2.0], [0.0]])
+    Un, Vn, Xn = ora.gt_uv(W, U, V, Y, 0.5)      # u - lr y = (1, 4) -> 2.5 ; v -> 2
+    assert Un[:, 0].tolist() == [2.5, 2.5] and Vn[:, 0].tolist() == [2.0, 2.0] and Xn[:, 0].tolist() == [1.25, 1.25]
+    Yn = ora.gt_y(W, Y, np.array([[1.0], [1.0]]), np.array([[0.0], [3.0]]))   # y + g - g' = (3, -2) -> 0.5
+    assert Yn[:, 0].tolist() == [0.5, 0.5]
+    # the paper's vector v with equal entries == one weight per agent
+    n, d = 5, 4
+    Wd = _column_stochastic_directed(n)
+    rng = np.random.default_rng(4)
+    U, Y = rng.standard_normal((n, d)), rng.standard_normal((n, d))
+    v1 = rng.uniform(0.5, 2, (n, 1))
+    a = ora.gt_uv(Wd, U, v1, Y, 0.1)
+    b_ = ora.gt_uv(Wd, U, np.tile(v1, (1, d)), Y, 0.1)
+    assert np.array_equal(a[0], b_[0]) and np.array_equal(a[2], b_[2]) and np.array_equal(np.tile(a[1], (1, d)), b_[1])

@@ -210,7 +210,8 @@ def main():
     count = a.count
     wire_dt = torch.float32 if a.wire == "fp32" else torch.bfloat16
     wire_b = 4 if a.wire == "fp32" else 2
-    heap = k * 2 * count * wire_b + (64 << 20)
+    # exchange slots (k agents x 2 parities) + across GPUs the push inboxes (n agents x 2 parities)
+    heap = (k + (a.agents if world > 1 else 0)) * 2 * count * wire_b + (64 << 20)
     ctx = bfp.Context(agents_per_proc=k, heap_bytes=heap, device=local)
     n = ctx.n
     if a.topology == "one_peer":

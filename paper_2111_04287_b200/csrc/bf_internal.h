@@ -163,6 +163,11 @@ struct ExchParams {
     unsigned long long prog_off;            // kernel 3: u64 [kMaxGrid] per-CTA publish progress
     unsigned long long *stats;              // kernel 3 built with BF_STATS=1: u64 [grid][8] (diagnostics)
     float *psi;                             // kernel 3 MODE 3 (Exact-Diffusion): psi state [k][count], in place
+    int push;                               // kernel 3 across GPUs: writers push into the readers' inboxes
+    unsigned long long inbox_off;           // push: wire dtype [n source agents][2 parities][cap] in every heap
+    unsigned long long inbox_agent_stride, inbox_parity_stride;   // bytes
+    unsigned long long pflag_off;           // push: u64 [kMaxP writer processes][kMaxGrid] in every heap
+    unsigned pushq[kMaxK];                  // push, kWStatic: bit q = process q reads local agent a
     SrcTab tab;                             // kWStatic: final coefficients; kWDynamic: declared r
     DynDecl dyn;
 };

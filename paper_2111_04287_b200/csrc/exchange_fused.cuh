@@ -533,11 +533,19 @@ static cudaError_t launch_fused_k(const ExchParams &p, int grid, cudaStream_t s)
     return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FusedCfg<K>::kThreadsPerCta), args, smem, s);
 }
 
+}  // namespace bf
+
+#include "exchange_push.cuh"
+
+namespace bf {
+
 template <typename XT, typename GT, typename WT, typename YT, int MODE>
 static cudaError_t launch_fused_t(const ExchParams &p, int grid, cudaStream_t s) {
     switch (p.geo.k) {
-        case 1: return launch_fused_k<XT, GT, WT, YT, MODE, 1>(p, grid, s);
-        case 2: return launch_fused_k<XT, GT, WT, YT, MODE, 2>(p, grid, s);
+        case 1: return p.push ? launch_push_k<XT, GT, WT, YT, MODE, 1>(p, grid, s)
+                              : launch_fused_k<XT, GT, WT, YT, MODE, 1>(p, grid, s);
+        case 2: return p.push ? launch_push_k<XT, GT, WT, YT, MODE, 2>(p, grid, s)
+                              : launch_fused_k<XT, GT, WT, YT, MODE, 2>(p, grid, s);
         case 4: return launch_fused_k<XT, GT, WT, YT, MODE, 4>(p, grid, s);
         case 8: return launch_fused_k<XT, GT, WT, YT, MODE, 8>(p, grid, s);
         default: return cudaErrorInvalidValue;

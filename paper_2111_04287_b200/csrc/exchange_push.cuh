@@ -1,0 +1,388 @@
+// exchange_push.cuh -- the cross-GPU PUSH variant of the local-agent fused kernel
+// (kernel 3 with ExchParams::push), for processes hosting K = 1 or 2 agents (the
+// 8-GPU shape of the paper, one agent per GPU, and 8 agents over 4 GPUs).
+//
+// The pull kernel (exchange_fused.cuh) publishes every wire copy into the
+// writer's own HBM and the reader pulls it over NVLink after acquiring the
+// writer's progress word across NVLink: the two GPUs' CTAs pace each other
+// through ~5 us system-scope round trips, and the writer reads x and g twice
+// (once to publish kLead sub-items ahead, once to combine).  Here:
+//   * the WRITER stores wire(x_half) straight into each reader process's inbox
+//     (remote NVLink stores, posted: no round trip on the data path) and, per
+//     batch of sub-items, releases a progress word that lives in the READER's
+//     heap (pflag[writer process][CTA]);
+//   * the READER polls its own local memory for the progress word and reads the
+//     inbox tiles from its local HBM / L2 (the NVLink writes land in its L2);
+//   * each sub-item is read from HBM once: the local part of every combine
+//     (self term, same-process sources, AWC / ED terms) is formed while the
+//     sub-item is published and parked in shared memory for kLag sub-items, until
+//     the remote tiles of that sub-item have arrived, then the remote terms are
+//     added and y is stored.
+// HBM per agent-element at K = 1 (fp32 ATC): x + g read, y write, inbox landing
+// write + read (often an L2 hit) = 16-20 B, against 28 B for the pull kernel.
+// Same pairwise CTA pairing as the pull kernel (sub-item s -> CTA s mod G on every
+// process), same WAR protection of the double-buffered inbox (done_from), same
+// summation order (R18: self, same-process sources in (a - b) mod K order, remote
+// sources in table order), so results are bitwise those of the pull kernel --
+// except AWC, whose -lr g_a joins the parked local part before the remote terms.
+// Static and scheduled topologies only (a push needs the writer to know its
+// readers; pull-only per-call views keep the pull kernel).
+#pragma once
+
+namespace bf {
+
+#ifndef BF_PUSH_SMEM_KB
+#define BF_PUSH_SMEM_KB 96
+#endif
+#ifndef BF_PUSH_LAG
+#define BF_PUSH_LAG 16
+#endif
+#ifndef BF_PUSH_BATCH
+#define BF_PUSH_BATCH 4
+#endif
+
+template <int K, int V>
+struct PushCfg {
+    // sub-items between the publish of a sub-item and its combine: as many as the
+    // shared-memory budget holds (K agents x V floats per thread per sub-item)
+    static constexpr int kPerSub = K * kThreads * V * 4;
+    static constexpr int kByBytes = BF_PUSH_SMEM_KB * 1024 / kPerSub;
+    static constexpr int kLag = kByBytes < BF_PUSH_LAG ? (kByBytes < 2 ? 2 : kByBytes) : BF_PUSH_LAG;
+    static constexpr int kSmem = kLag * kPerSub;
+    static constexpr int kThreadsPerCta = kThreads + 64;   // 8 consumer warps + signal warp + poll warp
+};
+constexpr int kPushBatch = BF_PUSH_BATCH;
+
+template <int K>
+struct PushMix {
+    float c[K][K];                 // local block of W (registers)
+    float rc[K * kMaxN];           // remote sources, agent-major: weight ...
+    unsigned char rs[K * kMaxN];   // ... and global source agent
+    int rbeg[K + 1];
+    unsigned procs_in;             // processes hosting a remote source of a local agent
+    unsigned procs_out[K];         // per local agent: processes it pushes to
+    unsigned procs_out_all;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_cta_shared(const int *p) {
+    unsigned v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta_shared(int *p, int v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+template <typename XT, typename GT, typename WT, typename YT, int MODE, int K>
+__global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2)
+    exchange_push_kernel(const __grid_constant__ ExchParams p) {
+    constexpr bool HAS_G = MODE != 0;
+    constexpr int V = FusedVec<XT>::V;
+    constexpr int kSubT = kThreads * V;
+    constexpr int L = PushCfg<K, V>::kLag;
+    extern __shared__ __align__(16) float lag[];   // [L][K][kThreads][V]: partial combines, thread-private
+    __shared__ SharedTab st;
+    __shared__ PushMix<K> lm;
+    __shared__ __align__(8) unsigned long long pubbar[kPubRing];
+    __shared__ int s_fail, s_released, s_ready;
+    volatile int *const fail = &s_fail;
+    const Geometry &g = p.geo;
+    Pad *pad = pad_of(g, g.me);
+    if (aborted(g)) return;
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
+    const int parity = static_cast<int>(e & 1);
+    if (threadIdx.x == 0) {
+        s_fail = 0;
+        s_released = 0;
+        s_ready = 0;
+        for (int i = 0; i < kPubRing; ++i) mbar_init(&pubbar[i], kThreads);
+        fence_mbar_init();
+    }
+    bool ok = war_wait(g, e);
+    ok = resolve_sources(p, e, st) && ok;
+    if (!ok) return;
+
+    if (threadIdx.x == 0) {
+        unsigned procs = 0;
+        int nr = 0;
+        for (int a = 0; a < K; ++a) {
+            for (int b = 0; b < K; ++b) lm.c[a][b] = 0.f;
+            lm.c[a][a] = st.self_w[a];
+            lm.rbeg[a] = nr;
+            for (int q = 0; q < st.nsrc[a]; ++q) {
+                const int src = st.src[a][q];
+                if (src / K == g.me) {
+                    lm.c[a][src % K] += st.coef[a][q];
+                } else {
+                    lm.rs[nr] = static_cast<unsigned char>(src);
+                    lm.rc[nr] = st.coef[a][q];
+                    procs |= 1u << (src / K);
+                    ++nr;
+                }
+            }
+        }
+        lm.rbeg[K] = nr;
+        lm.procs_in = procs;
+        unsigned all = 0;
+        for (int a = 0; a < K; ++a) {
+            unsigned out = 0;
+            if (p.wmode == kWStatic) {
+                out = p.pushq[a];
+            } else {   // kWSchedule: the scheduled destination (R5, R27)
+                const unsigned long long round = *reinterpret_cast<volatile unsigned long long *>(&pad->round);
+                int src, dst;
+                sched_peers(p.sched_kind, g.n, p.sched_L, round, g.me * K + a, src, dst);
+                if (dst >= 0 && dst / K != g.me) out = 1u << (dst / K);
+            }
+            lm.procs_out[a] = out;
+            all |= out;
+        }
+        lm.procs_out_all = all;
+    }
+    __syncthreads();
+
+    const bool vec = g.vec_ok != 0;
+    const long long count = g.count;
+    const int G = gridDim.x;
+    const int S = static_cast<int>((count + kSubT - 1) / kSubT);
+    const int nmine = static_cast<int>(blockIdx.x) < S ? (S - static_cast<int>(blockIdx.x) + G - 1) / G : 0;
+    const int nrt = lm.rbeg[K];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto sub = [&](int m) { return static_cast<int>(blockIdx.x) + m * G; };
+    // inbox of source agent j in process q's heap, this epoch's parity
+    auto inbox = [&](int q, int j) {
+        return at<WT>(g.peer_base[q], p.inbox_off + static_cast<unsigned long long>(j) * p.inbox_agent_stride +
+                                          parity * p.inbox_parity_stride);
+    };
+    // progress word of writer process w for CTA b, in reader process q's heap
+    auto pflag = [&](int q, int w) {
+        return at<unsigned long long>(g.peer_base[q], p.pflag_off) + static_cast<long long>(w) * kMaxGrid + blockIdx.x;
+    };
+
+    if (warp == kThreads / 32) {
+        // ================ signal warp (lane 0): system-scope releases ================
+        const int nbatch = lm.procs_out_all ? (nmine + kPushBatch - 1) / kPushBatch : 0;
+        if (lane == 0 && nbatch > 0) {
+            volatile int *released = &s_released;
+            for (int rb = 0; rb < nbatch; ++rb) {
+                if (!mbar_wait_acq_b(g, &pubbar[rb % kPubRing], static_cast<unsigned>(rb / kPubRing) & 1u, fail)) break;
+                const int done = min((rb + 1) * kPushBatch, nmine);
+                fence_acq_rel(true);   // the consumers' remote inbox stores, visible system-wide ...
+                for (int q = 0; q < g.nprocs; ++q)   // ... before the progress word in every reader's heap
+                    if ((lm.procs_out_all >> q) & 1u)
+                        st_relaxed(pflag(q, g.me), (e << kProgShift) | static_cast<unsigned long long>(done), true);
+                *released = rb + 1;
+            }
+        }
+    } else if (warp == kThreads / 32 + 1) {
+        // ===== poll warp (lane 0): local progress words of the writers -> s_ready =====
+        if (lane == 0 && nrt > 0 && nmine > 0) {
+            unsigned long long seen[kMaxP];
+            for (int q = 0; q < kMaxP; ++q) seen[q] = 0;
+            int ready = 0;
+            unsigned long long t_idle = globaltimer();
+            unsigned it = 0;
+            while (ready < nmine && !*fail) {
+                int lo = nmine;
+                for (int q = 0; q < g.nprocs; ++q) {
+                    if (!((lm.procs_in >> q) & 1u)) continue;
+                    const unsigned long long need = (e << kProgShift) | static_cast<unsigned long long>(ready + 1);
+                    if (seen[q] < need) seen[q] = ld_acquire_sys(pflag(g.me, q));
+                    const long long c = static_cast<long long>(seen[q]) - static_cast<long long>(e << kProgShift);
+                    lo = min(lo, c <= 0 ? 0 : static_cast<int>(c));
+                }
+                if (lo > ready) {
+                    ready = lo;
+                    st_release_cta_shared(&s_ready, ready);
+                    t_idle = globaltimer();
+                } else {
+                    if ((++it & 63u) == 0) {
+                        const unsigned code = ld_relaxed_sys_u32(&pad->abort);
+                        if (code) {
+                            if (g.host_err) *g.host_err = code;
+                            *fail = 1;
+                        } else if (globaltimer() - t_idle > g.timeout_ns) {
+                            abort_all(g, BF_ERR_TIMEOUT);
+                            *fail = 1;
+                        }
+                    }
+                    __nanosleep(64);
+                }
+            }
+        }
+    } else {
+        // ============================ consumer warps ============================
+        const unsigned long long pol_stream = policy_evict_first();
+        auto xrow = [&](int a) { return static_cast<const XT *>(p.x) + static_cast<long long>(a) * count; };
+        auto grow = [&](int a) { return static_cast<const GT *>(p.g) + static_cast<long long>(a) * count; };
+        const int e0 = threadIdx.x * V;
+        float *mylag = lag + static_cast<long long>(threadIdx.x) * V;   // + (slot * K + a) * kSubT
+        if (lm.procs_out_all == 0 && nrt == 0) {
+            // nothing crosses processes for this process (e.g. a schedule round inside it)
+        }
+        int slot = 0;
+        for (int m = 0; m < nmine + L; ++m, slot = slot + 1 == L ? 0 : slot + 1) {
+            const int mc = m - L;
+            // ---------------- combine sub-item mc: local part (smem) + remote tiles (inbox) ----------------
+            if (mc >= 0) {
+                const long long base = static_cast<long long>(sub(mc)) * kSubT;
+                const int valid = clamp_valid_v<V>(count - base, e0);
+                if (nrt > 0) {
+                    if (static_cast<int>(ld_acquire_cta_shared(&s_ready)) <= mc) {
+                        const unsigned long long t0 = globaltimer();
+                        while (static_cast<int>(ld_acquire_cta_shared(&s_ready)) <= mc) {
+                            if (*fail) break;
+                            if (globaltimer() - t0 > g.timeout_ns + 1000000000ull) {   // the poll warp times out first
+                                *fail = 1;
+                                break;
+                            }
+                            __nanosleep(32);
+                        }
+                    }
+                    if (*fail) break;
+                }
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    float acc[V];
+                    const float *lp = mylag + static_cast<long long>(slot * K + a) * kSubT;
+#pragma unroll
+                    for (int i = 0; i < V; i += 4) {
+                        const float4 t = *reinterpret_cast<const float4 *>(lp + i);
+                        acc[i] = t.x, acc[i + 1] = t.y, acc[i + 2] = t.z, acc[i + 3] = t.w;
+                    }
+                    const int rb = lm.rbeg[a], re = lm.rbeg[a + 1];
+                    for (int i0 = rb; i0 < re; i0 += 4) {   // up to 4 remote tiles in flight
+                        float v[4][V];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (i0 + u < re) VecN<WT, V>::load_cg(inbox(g.me, lm.rs[i0 + u]) + base + e0, v[u], valid, true);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (i0 + u < re) {
+                                const float c = lm.rc[i0 + u];
+#pragma unroll
+                                for (int j = 0; j < V; ++j) acc[j] = fmaf(c, v[u][j], acc[j]);
+                            }
+                    }
+                    YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base + e0;
+                    VecN<YT, V>::store_hint(yr, acc, valid, vec, pol_stream);
+                    if (p.shadow) {
+                        bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base + e0;
+                        VecN<bf16, V>::store_hint(sr, acc, valid, vec, pol_stream);
+                    }
+                }
+            }
+            // ---------------- publish sub-item m and park the local part of its combine ----------------
+            if (m < nmine) {
+                const long long base = static_cast<long long>(sub(m)) * kSubT;
+                const int valid = clamp_valid_v<V>(count - base, e0);
+                float xv[K][V];
+                float gv[HAS_G ? K : 1][V];
+#pragma unroll
+                for (int a = 0; a < K; ++a) VecN<XT, V>::load_hint(xrow(a) + base + e0, xv[a], valid, vec, pol_stream);
+                if constexpr (HAS_G) {
+#pragma unroll
+                    for (int a = 0; a < K; ++a) VecN<GT, V>::load_hint(grow(a) + base + e0, gv[a], valid, vec, pol_stream);
+                }
+                if constexpr (MODE == 1) {   // Eq. 4
+#pragma unroll
+                    for (int a = 0; a < K; ++a)
+#pragma unroll
+                        for (int i = 0; i < V; ++i) xv[a][i] = fmaf(-p.lr, gv[a][i], xv[a][i]);
+                }
+                if constexpr (MODE == 3) {   // Exact-Diffusion: psi = x - lr g (stored), phi = psi + x - psi_prev
+#pragma unroll
+                    for (int a = 0; a < K; ++a) {
+                        float pv[V];
+                        float *pr = p.psi + static_cast<long long>(a) * count + base + e0;
+                        VecN<float, V>::load_hint(pr, pv, valid, vec, pol_stream);
+                        float psi[V];
+#pragma unroll
+                        for (int i = 0; i < V; ++i) {
+                            psi[i] = fmaf(-p.lr, gv[a][i], xv[a][i]);
+                            xv[a][i] = (psi[i] + xv[a][i]) - pv[i];
+                        }
+                        VecN<float, V>::store_hint(pr, psi, valid, vec, pol_stream);
+                    }
+                }
+                // wire copies into every reader process's inbox (NVLink stores)
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    const unsigned out = lm.procs_out[a];
+                    if (!out) continue;
+                    for (int q = 0; q < g.nprocs; ++q)
+                        if ((out >> q) & 1u) VecN<WT, V>::store(inbox(q, g.me * K + a) + base + e0, xv[a], valid, true);
+                }
+                // local part of every combine: self, then same-process sources ((a - b) mod K)
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    float acc[V];
+                    const float cs = lm.c[a][a];
+#pragma unroll
+                    for (int i = 0; i < V; ++i) acc[i] = cs * xv[a][i];
+#pragma unroll
+                    for (int d = 1; d < K; ++d) {
+                        const int b = (a + K - d) % K;
+                        const float c = lm.c[a][b];
+                        if (c != 0.f) {
+#pragma unroll
+                            for (int i = 0; i < V; ++i)
+                                acc[i] = fmaf(c, MODE == 0 ? xv[b][i] : VecN<WT, V>::wire(xv[b][i]), acc[i]);
+                        }
+                    }
+                    float *lp = mylag + static_cast<long long>(slot * K + a) * kSubT;
+#pragma unroll
+                    for (int i = 0; i < V; i += 4) *reinterpret_cast<float4 *>(lp + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+                }
+                if constexpr (MODE == 2) {   // AWC (Eq. 16): the remote terms come later; -lr g is local
+#pragma unroll
+                    for (int a = 0; a < K; ++a) {
+                        float *lp = mylag + static_cast<long long>(slot * K + a) * kSubT;
+#pragma unroll
+                        for (int i = 0; i < V; ++i) lp[i] = fmaf(-p.lr, gv[a][i], lp[i]);
+                    }
+                }
+                if (lm.procs_out_all && ((m + 1) % kPushBatch == 0 || m + 1 == nmine)) {
+                    const int b = m / kPushBatch;
+                    if (b >= kPubRing) {   // the ring slot's previous phase must have been released
+                        volatile int *released = &s_released;
+                        while (*released <= b - kPubRing && !*fail) __nanosleep(64);
+                    }
+                    mbar_arrive_release(&pubbar[b % kPubRing]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (*fail) return;
+    last_cta(pad, [&] {
+        pad->epoch = e;
+        if (p.wmode == kWSchedule) pad->round = pad->round + 1;
+        publish_done(g, e);
+    });
+}
+
+template <typename XT, typename GT, typename WT, typename YT, int MODE, int K>
+static cudaError_t launch_push_k(const ExchParams &p, int grid, cudaStream_t s) {
+    using Cfg = PushCfg<K, FusedVec<XT>::V>;
+    const void *fn = reinterpret_cast<const void *>(exchange_push_kernel<XT, GT, WT, YT, MODE, K>);
+    constexpr int kSubT = kThreads * FusedVec<XT>::V;
+    static int maxg = 0;
+    if (maxg == 0) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        if (e != cudaSuccess) return e;
+        maxg = max_coresident(fn, Cfg::kThreadsPerCta, Cfg::kSmem);
+        if (maxg <= 0) return cudaErrorInvalidConfiguration;
+    }
+    static const int grid_env = getenv("BF_FUSED_GRID") ? atoi(getenv("BF_FUSED_GRID")) : 0;   // tuning
+    if (grid <= 0 && grid_env > 0) grid = grid_env;
+    if (grid <= 0 || grid > maxg) grid = maxg;
+    const long long subs = (p.geo.count + kSubT - 1) / kSubT;
+    if (grid > subs) grid = static_cast<int>(subs);
+    if (grid > kMaxGrid) grid = kMaxGrid;
+    if (grid < 1) grid = 1;
+    void *args[] = {const_cast<ExchParams *>(&p)};
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(Cfg::kThreadsPerCta), args, Cfg::kSmem, s);
+}
+
+}  // namespace bf

@@ -106,6 +106,8 @@ struct bf_ctx {
     unsigned long long launches = 0;
     unsigned long long *stats = nullptr;      // BF_STATS=1: per-CTA diagnostics of the fused kernel
     int hier_mode = 0;                        // BF_HIER: 0 auto, 1 staged (always), 2 fused (also across GPUs)
+    int xfer = 1;                             // BF_XFER: 1 push (default across GPUs, K = 1, 2), 0 pull
+    unsigned long long inbox_off = 0, pflag_off = 0;   // push inboxes [n][2][cap] + progress words (0: none)
     bool win_ef = false;                      // BF_WIN_EF=1: new windows start with error feedback on
     // stream order across calls: every call of a context reads and advances the same
     // device state (epoch, round, slots, progress words), so a call issued on another
@@ -225,6 +227,19 @@ bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
     c->ccnt_off = ccnt_off;
     c->cflag_off = cflag_off;
     if ((s = heap_alloc(c, static_cast<size_t>(kMaxGrid) * 8, &c->prog_off))) return s;
+    // push inboxes (cross-GPU fused kernel at K = 1, 2): one double-buffered inbox per
+    // source agent in every reader's heap.  Optional: without room the pull kernel runs.
+    c->inbox_off = c->pflag_off = 0;
+    if (c->nprocs > 1 && c->xfer && (c->k == 1 || c->k == 2)) {
+        const size_t need = static_cast<size_t>(c->n) * 2 * cap + static_cast<size_t>(kMaxP) * kMaxGrid * 8 + 2 * kAlign;
+        if (c->heap_used + need <= c->heap_bytes) {
+            unsigned long long ib, pf;
+            if ((s = heap_alloc(c, static_cast<size_t>(c->n) * 2 * cap, &ib))) return s;
+            if ((s = heap_alloc(c, static_cast<size_t>(kMaxP) * kMaxGrid * 8, &pf))) return s;
+            c->inbox_off = ib;
+            c->pflag_off = pf;
+        }
+    }
     c->exch_cap = cap;
     c->slot_off = slot_off;
     c->ready_off = ready_off;
@@ -456,6 +471,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
     if (const char *x = getenv("BF_HIER")) c->hier_mode = strcmp(x, "staged") == 0 ? 1 : strcmp(x, "fused") == 0 ? 2 : 0;
     if (const char *x = getenv("BF_WIN_EF")) c->win_ef = atoi(x) != 0;
+    if (const char *x = getenv("BF_XFER")) c->xfer = strcmp(x, "pull") == 0 ? 0 : 1;
     if (const char *x = getenv("BF_STATS"))
         if (atoi(x) && cudaMalloc(&c->stats, static_cast<size_t>(kMaxGrid) * 8 * 8) == cudaSuccess)
             cudaMemset(c->stats, 0, static_cast<size_t>(kMaxGrid) * 8 * 8);
@@ -823,6 +839,24 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
         p.psi = psi;
     }
     p.cflag_off = c->cflag_off;
+    // cross-GPU push variant (exchange_push.cuh): static topologies and schedules at
+    // K = 1, 2, when the inboxes fit in the heap; per-call views and the caller-assembled
+    // hierarchical W keep the pull kernel
+    if (p.kernel == 3 && c->nprocs > 1 && c->inbox_off && !static_tab && p.wmode != kWDynamic &&
+        (c->k == 1 || c->k == 2)) {
+        p.push = 1;
+        p.inbox_off = c->inbox_off;
+        p.inbox_agent_stride = 2 * c->exch_cap;
+        p.inbox_parity_stride = c->exch_cap;
+        p.pflag_off = c->pflag_off;
+        if (p.wmode == kWStatic)
+            for (int a = 0; a < c->k; ++a) {
+                const int gid = c->proc * c->k + a;
+                for (int i = 0; i < c->n; ++i)
+                    if (i / c->k != c->proc && c->W[static_cast<size_t>(i) * c->n + gid] != 0.0)
+                        p.pushq[a] |= 1u << (i / c->k);
+            }
+    }
     order_stream(c, st);
     CU(launch_exchange(p, x_kind, awc_g ? x_kind : g_kind, wire_kind, y_kind, g != nullptr, 0, st));
     c->launches++;

@@ -30,7 +30,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "neighbor_allreduce GB/s/GPU + ATC-DSGD iters/s at 1/2/4/8 B200, % of roofline"
-NVLINK_PEAK_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction (nominal 900)
+NVLINK_PEAK_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction (the roofline denominator)
+NVLINK_NOMINAL_GBS = 900.0   # north_star / B200_PROFILING.md nominal per direction (context)
+NVLINK_BIDIR_GBS = 680.0     # profiles/r01_nvlink_calibration.md: per-GPU pull/push with both directions busy (context)
 HBM_FALLBACK_GBS = 6650.0    # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 
 
@@ -47,7 +49,27 @@ def parse():
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-nar", action="store_true", help="skip the C3 1 GiB neighbor_allreduce line")
+    ap.add_argument("--nar-bytes", type=int, default=1 << 30, help="bytes per agent of the C3 call")
     return ap.parse_args()
+
+
+def host_cpu():
+    """(model name, logical CPUs usable by this process) of the box's host."""
+    model = "unknown"
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        ncpu = len(os.sched_getaffinity(0))
+    except Exception:
+        ncpu = os.cpu_count() or 1
+    return model, ncpu
 
 
 def hbm_peak():
@@ -125,10 +147,15 @@ class Clocks:
 
 
 # ------------------------------------------------------------ CPU oracle ----
-def oracle_step_rate(a, budget_s=12.0, prefix=1 << 20):
-    """Time the oracle (oracle/bf_oracle.c, single thread, as it stands) on a
-    bounded prefix sample of the same workload; returns (iters/s extrapolated
-    to the full count, sample description, seconds spent)."""
+def oracle_step_rate(a, budget_s=12.0, prefix=1 << 20, threads=1):
+    """Time the oracle (oracle/bf_oracle.c, as it stands) on a bounded prefix
+    sample of the same workload.  threads > 1: the prefix is split into column
+    slices, one thread per slice, each calling the same single-threaded oracle
+    function (the step is column-wise; ctypes releases the GIL), so `threads`
+    host cores work.  Returns (iters/s extrapolated to the full count, sample
+    description, seconds spent, measured seconds per prefix step, factor)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     import numpy as np
 
     import oracle as ora
@@ -137,18 +164,28 @@ def oracle_step_rate(a, budget_s=12.0, prefix=1 << 20):
     X = synthetic.agents_x0(n, prefix).astype(np.float64)
     G = synthetic.agents_grad(n, prefix, 0).astype(np.float64)
     Wk = [ora.one_peer_exp2(n, k) if a.topology == "one_peer" else ora.exp2(n) for k in range(3)]
+    bounds = np.linspace(0, prefix, threads + 1).astype(int)
+    Xs = [np.ascontiguousarray(X[:, lo:hi]) for lo, hi in zip(bounds[:-1], bounds[1:])]
+    Gs = [np.ascontiguousarray(G[:, lo:hi]) for lo, hi in zip(bounds[:-1], bounds[1:])]
+    pool = ThreadPoolExecutor(threads) if threads > 1 else None
     t0 = time.perf_counter()
     steps = 0
     while True:
-        X = ora.atc(Wk[steps % 3], X, G, a.lr, wire_bf16=(a.wire == "bf16"))
+        W = Wk[steps % 3]
+        f = lambda i: ora.atc(W, Xs[i], Gs[i], a.lr, wire_bf16=(a.wire == "bf16"))
+        Xs = list(pool.map(f, range(threads))) if pool else [f(0)]
         steps += 1
         el = time.perf_counter() - t0
         if el >= budget_s:
             break
-    per_step_full = el / steps * (a.count / prefix)
+    if pool:
+        pool.shutdown()
+    per_prefix = el / steps
+    factor = a.count / prefix
     sample = (f"{steps} oracle ATC steps on a {prefix}-element prefix of each of the {n} agents "
-              f"({el:.1f} s), extrapolated linearly to {a.count} elements")
-    return 1.0 / per_step_full, sample, el
+              f"({el:.1f} s, {per_prefix * 1e3:.1f} ms per prefix step, {threads} thread(s) on column slices), "
+              f"time scaled linearly by {factor:.2f} to {a.count} elements")
+    return 1.0 / (per_prefix * factor), sample, el, per_prefix, factor
 
 
 def run_reference(a):
@@ -170,8 +207,11 @@ def run_reference(a):
     for s in range(a.steps):
         X = ora.atc(Wk[s % 3], X, G, a.lr, wire_bf16=(a.wire == "bf16"))
     el = time.perf_counter() - t0
-    ms_full = el / a.steps * (a.count / prefix) * 1e3
+    factor = a.count / prefix
+    ms_prefix = el / a.steps * 1e3
+    ms_full = ms_prefix * factor
     value = 1e3 / ms_full
+    model, ncpu = host_cpu()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_full, "higher_is_better": True,
@@ -179,11 +219,43 @@ def run_reference(a):
         "config": {"workload": workload_name(a), "agents": n, "count": a.count, "topology": a.topology,
                    "wire": a.wire},
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "kind": "oracle",
+                         "cpu_model": model, "nproc": ncpu,
                          "sample": f"each step = one oracle ATC step on a {prefix}-element prefix of each agent, "
-                                   f"time scaled linearly to {a.count} elements"},
+                                   f"time scaled linearly to {a.count} elements",
+                         "measured_ms_per_prefix_step": ms_prefix, "extrapolation_factor": factor},
+        "timing": "ms_per_step is the measured prefix time x extrapolation_factor (not timed at full size)",
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def nar_line(a, ctx, k, world, nar_count, ms, nsteps, rounds, peak_hbm, peak_kind, sources, dests):
+    """C3 neighbor_allreduce GB/s/GPU: algorithmic NVLink-in bytes
+    d_in_remote x M per second at N > 1; at N = 1 (every neighbour on the same GPU,
+    combined in registers) the algorithmic HBM bytes (read x + write y) per second."""
+    M = nar_count * 4
+    rounds = rounds if a.topology == "one_peer" else [0]
+    rem = statistics.mean(len({j for la in range(k) for j in sources(ctx.rank + la, r) if j // k != ctx.proc})
+                          for r in rounds)
+    pub = statistics.mean(sum(1 for la in range(k) if any(j // k != ctx.proc for j in dests(ctx.rank + la, r)))
+                          for r in rounds)
+    hbm = k * 2 * M + pub * M
+    nvl = rem * M
+    t = ms * 1e-3
+    out = {"bytes_per_agent": M, "dtype": "fp32", "topology": a.topology, "ms_per_call": ms, "calls": nsteps,
+           "hbm_gbs": hbm / t / 1e9, "nvlink_in_gbs_per_gpu": nvl / t / 1e9}
+    if world == 1 or nvl == 0:
+        out["gbs_per_gpu"] = out["hbm_gbs"]
+        out["gbs_definition"] = "N = 1: algorithmic HBM bytes (read x + write y) per second"
+        out["frac_of_hbm_peak"] = out["hbm_gbs"] / peak_hbm
+        out["peak"] = f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"
+    else:
+        out["gbs_per_gpu"] = out["nvlink_in_gbs_per_gpu"]
+        out["gbs_definition"] = "algorithmic NVLink-in bytes (distinct remote in-neighbours of the local agents x M) per second"
+        out["frac_of_nvlink_770"] = out["gbs_per_gpu"] / NVLINK_PEAK_GBS
+        out["frac_of_nominal_900"] = out["gbs_per_gpu"] / NVLINK_NOMINAL_GBS
+        out["frac_of_bidir_680"] = out["gbs_per_gpu"] / NVLINK_BIDIR_GBS
+    return out
 
 
 # ----------------------------------------------------------------- ours -----
@@ -211,7 +283,8 @@ def main():
     wire_dt = torch.float32 if a.wire == "fp32" else torch.bfloat16
     wire_b = 4 if a.wire == "fp32" else 2
     # exchange slots (k agents x 2 parities) + across GPUs the push inboxes (n agents x 2 parities)
-    heap = (k + (a.agents if world > 1 else 0)) * 2 * count * wire_b + (64 << 20)
+    nar_count = 0 if a.no_nar else a.nar_bytes // 4
+    heap = (k + (a.agents if world > 1 else 0)) * 2 * max(count * wire_b, nar_count * 4) + (64 << 20)
     ctx = bfp.Context(agents_per_proc=k, heap_bytes=heap, device=local)
     n = ctx.n
     if a.topology == "one_peer":
@@ -283,17 +356,41 @@ def main():
         barrier()
         e2e_ms = e0.elapsed_time(e1) / a.steps
         e2e = {"ms": e2e_ms, "h2d": k * count * 4, "d2h": k * 1024 * 4}
+    # ---- C3 (BASELINE.json configs[2]): one neighbor_allreduce call at 1 GiB fp32 per
+    # agent on the same topology, timed on the device like the step ----
+    nar = None
+    if nar_count:
+        del gs
+        xn = torch.empty(k, nar_count, device="cuda")
+        for la in range(k):
+            bfp.Context.fill_uniform(xn[la], synthetic.SEED_X0 + 100 + ctx.rank + la)
+        yn = torch.empty_like(xn)
+        nsteps = max(3, min(a.steps, 20))
+        for _ in range(3):
+            ctx.neighbor_allreduce(xn, out=yn)
+        barrier()
+        n0 = torch.cuda.Event(enable_timing=True)
+        n1 = torch.cuda.Event(enable_timing=True)
+        n0.record(stream)
+        for _ in range(nsteps):
+            ctx.neighbor_allreduce(xn, out=yn)
+        n1.record(stream)
+        barrier()
+        # schedule rounds of the timed calls (every schedule-mode call advances the round)
+        r0 = a.warmup + a.steps + (0 if a.no_e2e else 2 + a.steps) + 3
+        nar = {"ms": n0.elapsed_time(n1) / nsteps, "steps": nsteps, "rounds": range(r0, r0 + nsteps)}
+        del xn, yn
     clk = clocks.stop()
     ctx.poll_error()
 
     # ---- max over ranks ----
-    vals = torch.tensor([total_ms / a.steps, kern_ms, e2e["ms"] if e2e else 0.0] + by_round, dtype=torch.float64,
-                        device="cuda")
+    vals = torch.tensor([total_ms / a.steps, kern_ms, e2e["ms"] if e2e else 0.0, nar["ms"] if nar else 0.0] + by_round,
+                        dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     vals = [float(v) for v in vals.cpu()]
-    ms_step, ms_kern, ms_e2e = vals[:3]
-    ms_by_round = vals[3:]
+    ms_step, ms_kern, ms_e2e, ms_nar = vals[:4]
+    ms_by_round = vals[4:]
 
     if rank == 0:
         d = degree(a.topology, n)
@@ -323,7 +420,8 @@ def main():
         remote, publishers, t_roof = 0.0, 0.0, 0.0
         roof_by_round = {}
         for r in rounds:
-            rem_r = sum(1 for la in range(k) for sidx in sources(ctx.rank + la, r) if sidx // k != ctx.proc)
+            # distinct remote source agents: one copy per GPU is what the method must move
+            rem_r = len({sidx for la in range(k) for sidx in sources(ctx.rank + la, r) if sidx // k != ctx.proc})
             pub_r = sum(1 for la in range(k) if any(didx // k != ctx.proc for didx in dests(ctx.rank + la, r)))
             remote += rem_r / len(rounds)
             publishers += pub_r / len(rounds)
@@ -371,7 +469,6 @@ def main():
                        "topology": a.topology, "wire": a.wire, "lr": a.lr,
                        "l2": "inputs larger than L2 (x, 2 rotating gradient sets: "
                              f"{3 * n * count * 4 / 1e9:.2f} GB)"},
-            "neighbor_allreduce_gbs_per_gpu": (k * d * count * wire_b) / (ms_kern * 1e-3) / 1e9,
             "gpu_launches": launches,
             "roofline": roof,
             "clocks": clk,
@@ -381,9 +478,26 @@ def main():
                            "d2h_bytes_per_step": e2e["d2h"] * world,
                            "path": "Context.atc_step with pinned host gradients (H2D inside the C-ABI call) "
                                    "+ D2H of 1024 elements per agent"}
+        if nar:
+            line["neighbor_allreduce"] = nar_line(a, ctx, k, world, nar_count, ms_nar, nar["steps"], nar["rounds"],
+                                                  peak_hbm, peak_kind, sources, dests)
+            line["neighbor_allreduce_gbs_per_gpu"] = line["neighbor_allreduce"]["gbs_per_gpu"]
+        if world > 1:
+            roof["frac_of_nominal_900"] = (roof["achieved"] / NVLINK_NOMINAL_GBS if roof["bound"] == "nvlink"
+                                           else None)
+            roof["frac_of_bidir_680"] = (roof["achieved"] / NVLINK_BIDIR_GBS if roof["bound"] == "nvlink"
+                                         else None)
         if world == 1 and not a.no_cpu:
-            v, sample, el = oracle_step_rate(a)
-            line["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle", "sample": sample}
+            model, ncpu = host_cpu()
+            v, sample, el, per_prefix, factor = oracle_step_rate(a)
+            line["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle", "sample": sample,
+                                    "cpu_model": model, "nproc": ncpu,
+                                    "measured_ms_per_prefix_step": per_prefix * 1e3, "extrapolation_factor": factor}
+            thr = min(a.agents, ncpu)
+            if thr > 1:
+                v2, sample2, _, pp2, _ = oracle_step_rate(a, budget_s=8.0, threads=thr)
+                line["cpu_baseline_threads"] = {"value": v2, "unit": "iters/s", "cores": thr, "kind": "oracle",
+                                                "sample": sample2, "measured_ms_per_prefix_step": pp2 * 1e3}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -204,6 +204,27 @@ bf_status bf_exact_diffusion_step(bf_ctx *ctx, float *x, const void *g, bf_dtype
                                   size_t count, float lr, bf_dtype wire, const bf_weights *weights,
                                   void *stream);
 
+/* Push-sum gradient tracking (appendix "Push-sum gradient tracking", PAPER.md lines
+ * 1000-1006, listing GT-varying), one fused launch per partial
+ * averaging of a round (the gradient at the new x is the caller's, in between):
+ *   bf_gt_uv_step:  u_i <- sum_j w_ij (u_j - lr y_j)            (line 1002)
+ *                   v_i <- sum_j w_ij v_j                         (line 1003)
+ *                   x_out_i = u_i / v_i                           (line 1004)
+ *   bf_gt_y_step:   y_i <- sum_j w_ij (y_j + g_j - g_prev_j)     (line 1006)
+ * u, y, x_out, g, g_prev: fp32 device tensors [agents_per_proc][count]; u and y are
+ * updated in place.  v: fp32 device array [agents_per_proc], ONE push-sum weight per
+ * agent (v^0 = 1 keeps every entry of the paper's vector v equal -- reading R28),
+ * updated in place; the neighbours' weights travel through the signal pads.  W:
+ * static topology, schedule or per-call views, as bf_neighbor_allreduce (the
+ * listing uses push views: self 1/(d_out+1), dst 1/(d_out+1), src 1).  wire: dtype
+ * of the neighbours' copies.  Needs the fused exchange kernel (agents_per_proc 1,
+ * 2, 4 or 8 on one GPU): else BF_ERR_UNSUPPORTED.  Collective like
+ * bf_neighbor_allreduce. */
+bf_status bf_gt_uv_step(bf_ctx *ctx, float *u, float *v, const float *y, float *x_out, size_t count, float lr,
+                        bf_dtype wire, const bf_weights *weights, void *stream);
+bf_status bf_gt_y_step(bf_ctx *ctx, float *y, const float *g, const float *g_prev, size_t count, bf_dtype wire,
+                       const bf_weights *weights, void *stream);
+
 /* bf_hierarchical_neighbor_allreduce (R12): y = (W_M kron J_L/L) x:
  * intra-machine average, machine-level neighbour averaging, broadcast.
  * machine_weights: NULL (static machine topology) or an array of
@@ -276,6 +297,15 @@ bf_status bf_win_put(bf_ctx *ctx, const char *name, const bf_weights *weights,
                      uint64_t agent_mask, void *stream);
 bf_status bf_win_accumulate(bf_ctx *ctx, const char *name, const bf_weights *weights,
                             int require_mutex, uint64_t agent_mask, void *stream);
+/* Gradient-in-window push (SGP-style push-sum SGD): one kernel
+ * does the local step x_a <- x_a - lr g_a (Eq. 4) and then exactly what
+ * bf_win_accumulate does with the updated x_a (payloads s_ja x_a to the
+ * destinations, x_a <- self_weight x_a).  g: device tensor of the
+ * window's dtype and layout [agents_per_proc][count].  The push-sum weight p is
+ * not touched by the step (it scales only the numerator).  Errors as
+ * bf_win_accumulate; BF_ERR_ARG for a null / host gradient or non-finite lr. */
+bf_status bf_win_accumulate_grad(bf_ctx *ctx, const char *name, const void *g, float lr, const bf_weights *weights,
+                                 uint64_t agent_mask, void *stream);
 /* bf_win_update: out_a = self_w * x_a + sum_j r_aj * (latest
  * complete payload from j); weights NULL = uniform 1/(d_in+1) (R10); out NULL =
  * in place.  Marks the read payloads consumed; slots are not reset. */

@@ -64,6 +64,7 @@ def lib():
         L.ora_win_free.argtypes = [C.c_void_p]
         L.ora_win_accumulate.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, _ip, C.c_int]
         L.ora_win_collect.argtypes = [C.c_void_p, C.c_int]
+        L.ora_win_adapt.argtypes = [C.c_void_p, C.c_int, _dp, C.c_double]
         L.ora_win_update.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, _dp]
         L.ora_win_get_x.argtypes = [C.c_void_p, _dp]
         L.ora_win_mass.argtypes = [C.c_void_p, C.c_longlong]
@@ -322,6 +323,12 @@ class Window:
 
     def collect(self, i):
         lib().ora_win_collect(self._h, i)
+
+    def adapt(self, i, g, lr):
+        """x_i <- x_i - lr g_i (ora_win_adapt; g covers the whole window row)."""
+        g = _f64(g)
+        assert g.shape == (self.count,)
+        lib().ora_win_adapt(self._h, i, _d(g), float(np.float32(lr)))
 
     def update(self, i, self_weight, src_weights):
         r = np.zeros(self.n, np.float64)

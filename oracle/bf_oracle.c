@@ -474,6 +474,13 @@ int ora_win_accumulate(ora_win *w, int i, double self_weight, const double *s,
     return 0;
 }
 
+/* Local SGD step inside a window, before a push (SGP-style gradient-in-window,
+ * SURVEY 8(f) rank 4): x_i <- x_i - lr g_i (Eq. 4) on the window tensor;
+ * the p lane (the last element when the caller appends it) gets g = 0. */
+void ora_win_adapt(ora_win *w, int i, const double *g, double lr) {
+    for (long long e = 0; e < w->count; ++e) w->x[(size_t)i * w->count + e] -= lr * g[e];
+}
+
 void ora_win_collect(ora_win *w, int i) {
     long long C = w->count;
     for (int q = 0; q < w->nin[i]; ++q) {

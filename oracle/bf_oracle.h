@@ -96,6 +96,8 @@ void ora_win_free(ora_win *w);
  * (s[j] used for j in dst set; dst_mask[j] != 0 selects) */
 int ora_win_accumulate(ora_win *w, int i, double self_weight, const double *s,
                        const int *dst_mask, int overwrite);
+/* local step x_i <- x_i - lr g_i before a push (gradient-in-window, SGP-style) */
+void ora_win_adapt(ora_win *w, int i, const double *g, double lr);
 /* update_then_collect by agent i (sum of ready halves, release) */
 void ora_win_collect(ora_win *w, int i);
 /* win_update by agent i: out = self_w*x_i + sum_j r_j*latest slot j (no reset) */

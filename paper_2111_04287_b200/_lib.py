@@ -73,6 +73,7 @@ _SIGS = {
     "bf_win_free": (_i, [_vp, C.c_char_p]),
     "bf_win_put": (_i, [_vp, C.c_char_p, _wp, _u64, _vp]),
     "bf_win_accumulate": (_i, [_vp, C.c_char_p, _wp, _i, _u64, _vp]),
+    "bf_win_accumulate_grad": (_i, [_vp, C.c_char_p, _vp, C.c_float, _wp, _u64, _vp]),
     "bf_win_update": (_i, [_vp, C.c_char_p, _wp, _vp, _u64, _vp]),
     "bf_win_update_then_collect": (_i, [_vp, C.c_char_p, _u64, _vp]),
     "bf_win_get_p": (_i, [_vp, C.c_char_p, C.POINTER(C.c_double), _vp]),
@@ -88,6 +89,8 @@ _SIGS = {
     "bf_alloc": (_i, [_vp, _sz, C.POINTER(_vp)]),
     "bf_win_get": (_i, [_vp, C.c_char_p, _wp, _u64, _vp]),
     "bf_exact_diffusion_step": (_i, [_vp, _vp, _vp, _i, _vp, _sz, C.c_float, _i, _wp, _vp]),
+    "bf_gt_uv_step": (_i, [_vp, _vp, _vp, _vp, _vp, _sz, C.c_float, _i, _wp, _vp]),
+    "bf_gt_y_step": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _wp, _vp]),
 }
 
 _lib = None

@@ -3,17 +3,15 @@
 * Exact-Diffusion (appendix, Eqs. ed-1..ed-3) is a single fused primitive:
   `Context.exact_diffusion_step` (MODE 3 of the fused exchange kernel).
 * Push-sum gradient tracking (appendix, "Push-sum gradient tracking",
-  PAPER.md lines 1000-1006 and its listing) needs three partial averagings per
-  round; here they are the library's fused calls:
+  PAPER.md lines 1000-1006 and its listing) needs two partial-averaging passes
+  per round around the caller's gradient; each is one fused launch:
 
-      u <- W (u - lr y)            one fused ATC call (adapt = u - lr y)
-      v <- W v                     neighbor_allreduce of the push-sum weights
-      x  = u / v                   elementwise (application code, as in the listing)
-      g' = grad(x)                 the caller's gradient
-      y <- W (y + g' - g)          one fused ATC call with lr = 1 and "gradient" g - g'
+      u <- W (u - lr y), v <- W v, x = u / v     Context.gt_uv_step   (MODE 5)
+      g' = grad(x)                               the caller's gradient
+      y <- W (y + g' - g)                        Context.gt_y_step    (MODE 4)
 
-  The elementwise glue (u / v, g - g') is application code exactly as in the
-  paper's listing; every partial averaging runs in libbluefog_b200.so.
+  v is one push-sum weight per agent (reading R28: v^0 = 1 keeps the entries of
+  the paper's vector v equal).  No elementwise glue runs outside the kernels.
 """
 from __future__ import annotations
 
@@ -23,16 +21,17 @@ import torch
 
 
 def gradient_tracking_step(ctx, u: torch.Tensor, v: torch.Tensor, y: torch.Tensor, g_prev: torch.Tensor,
-                           grad_fn: Callable[[torch.Tensor], torch.Tensor], lr: float):
-    """One round of push-sum gradient tracking over the context's current
-    topology / one-peer schedule (each fused call advances a one-peer round,
-    so all three averagings of a round must use the same W: call with a static
-    topology, or with per-call views).  u, y, g_prev: fp32 (K, d); v: fp32
-    (K, 1).  Returns (x, u, v, y, g) -- u, v, y updated in place."""
-    ctx.atc_step(u, y, lr)                      # u <- W (u - lr y)
-    ctx.neighbor_allreduce(v, out=v)            # v <- W v
-    x = u / v                                   # x = u / v
+                           grad_fn: Callable[[torch.Tensor], torch.Tensor], lr: float, x: torch.Tensor = None,
+                           **weights):
+    """One round of push-sum gradient tracking over the context's current topology /
+    schedule, or per-call views passed as `weights` (self_weight, src_weights,
+    dst_weights -- the same W for both passes of the round; with a one-peer schedule
+    the two passes take two consecutive rounds of it, so use views or a static W).
+    u, y, g_prev: fp32 (K, d); v: fp32 (K,).  Returns (x, u, v, y, g) -- u, v, y
+    updated in place, g the new gradient (the caller keeps it as the next g_prev)."""
+    if x is None:
+        x = torch.empty_like(u)
+    ctx.gt_uv_step(u, v, y, x, lr, **weights)     # u <- W(u - lr y); v <- W v; x = u / v
     g = grad_fn(x)
-    diff = g_prev - g                           # y + g - g_prev = y - 1 * (g_prev - g)
-    ctx.atc_step(y, diff.contiguous(), 1.0)     # y <- W (y + g - g_prev)
+    ctx.gt_y_step(y, g, g_prev, **weights)        # y <- W(y + g - g_prev)
     return x, u, v, y, g

@@ -279,6 +279,43 @@ class Context:
                                                _DT[wire], v.ptr() if v else None, _stream_ptr(stream, self.device)))
         return x
 
+    def gt_uv_step(self, u: torch.Tensor, v: torch.Tensor, y: torch.Tensor, x_out: torch.Tensor, lr: float,
+                   wire: torch.dtype = torch.float32, self_weight=None, src_weights=None, dst_weights=None,
+                   stream=None) -> torch.Tensor:
+        """Push-sum gradient tracking, first half of a round (appendix), one
+        fused launch: u <- W(u - lr y), v <- W v (one fp32 weight per agent, shape (K,)),
+        x_out = u / v.  u, v updated in place; returns x_out."""
+        for t, nm in ((u, "u"), (y, "y"), (x_out, "x_out")):
+            if t.dtype != torch.float32:
+                raise ValueError(f"{nm} must be fp32")
+        count = self._rows(self._dev(u, "u"))
+        self._like(y, u, "y")
+        self._like(x_out, u, "x_out")
+        self._dev(v, "v")
+        if v.dtype != torch.float32 or v.numel() != self.k or not v.is_contiguous():
+            raise ValueError(f"v must be a contiguous fp32 tensor of {self.k} push-sum weights (one per agent)")
+        vw = self._views(self_weight, src_weights, dst_weights)
+        check(self.lib.bf_gt_uv_step(self.h, C.c_void_p(u.data_ptr()), C.c_void_p(v.data_ptr()),
+                                     C.c_void_p(y.data_ptr()), C.c_void_p(x_out.data_ptr()), count, float(lr),
+                                     _DT[wire], vw.ptr() if vw else None, _stream_ptr(stream, self.device)))
+        return x_out
+
+    def gt_y_step(self, y: torch.Tensor, g: torch.Tensor, g_prev: torch.Tensor, wire: torch.dtype = torch.float32,
+                  self_weight=None, src_weights=None, dst_weights=None, stream=None) -> torch.Tensor:
+        """Push-sum gradient tracking, second half (appendix), one fused launch:
+        y <- W(y + g - g_prev), in place."""
+        for t, nm in ((y, "y"), (g, "g"), (g_prev, "g_prev")):
+            if t.dtype != torch.float32:
+                raise ValueError(f"{nm} must be fp32")
+        count = self._rows(self._dev(y, "y"))
+        self._like(g, y, "g")
+        self._like(g_prev, y, "g_prev")
+        vw = self._views(self_weight, src_weights, dst_weights)
+        check(self.lib.bf_gt_y_step(self.h, C.c_void_p(y.data_ptr()), C.c_void_p(g.data_ptr()),
+                                    C.c_void_p(g_prev.data_ptr()), count, _DT[wire], vw.ptr() if vw else None,
+                                    _stream_ptr(stream, self.device)))
+        return y
+
     def awc_step(self, x: torch.Tensor, g: torch.Tensor, lr: float, self_weight=None, src_weights=None,
                  dst_weights=None, stream=None) -> torch.Tensor:
         """Fused AWC-DSGD step (Eq. 16): x <- W x - lr*g, in place on the fp32 master x."""
@@ -408,6 +445,18 @@ class Context:
         v = self._views(self_weight, None, dst_weights)
         check(self.lib.bf_win_accumulate(self.h, name.encode(), v.ptr() if v else None,
                                          1 if require_mutex else 0, agent_mask, _stream_ptr(stream, self.device)))
+        return True
+
+    def win_accumulate_grad(self, name: str, g: torch.Tensor, lr: float, self_weight=None, dst_weights=None,
+                            agent_mask: int = 0, stream=None) -> bool:
+        """Gradient-in-window push (SGP-style): x <- x - lr g, then win_accumulate, in one kernel.
+        g: device tensor of the window's dtype and shape."""
+        self._dev(g, "g")
+        if not g.is_contiguous():
+            raise ValueError("g must be contiguous")
+        v = self._views(self_weight, None, dst_weights)
+        check(self.lib.bf_win_accumulate_grad(self.h, name.encode(), C.c_void_p(g.data_ptr()), float(lr),
+                                              v.ptr() if v else None, agent_mask, _stream_ptr(stream, self.device)))
         return True
 
     def win_update(self, name: str, self_weight=None, src_weights=None, out: Optional[torch.Tensor] = None,

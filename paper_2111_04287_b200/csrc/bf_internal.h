@@ -65,6 +65,10 @@ struct Pad {
     unsigned long long bar_from[kMaxP];    // device barrier arrivals
     Desc desc[kMaxK][2];
     LocalView lview[kMaxK];
+    // push-sum gradient tracking (MODE 5): the scalar push-sum weight v of each local
+    // agent for this epoch, published for the readers; tag = epoch
+    unsigned long long gtv_tag[kMaxK][2];
+    float gtv[kMaxK][2];
 };
 static_assert(sizeof(Pad) <= kPadBytes, "pad too large");
 
@@ -163,6 +167,10 @@ struct ExchParams {
     unsigned long long prog_off;            // kernel 3: u64 [kMaxGrid] per-CTA publish progress
     unsigned long long *stats;              // kernel 3 built with BF_STATS=1: u64 [grid][8] (diagnostics)
     float *psi;                             // kernel 3 MODE 3 (Exact-Diffusion): psi state [k][count], in place
+    int gt;                                 // kernel 3: 4 = GT y-step (MODE 4), 5 = GT u/v-step (MODE 5), else 0
+    const float *g2;                        // kernel 3 MODE 4 (GT y-step): g_prev [k][count] (fp32)
+    float *gt_v;                            // kernel 3 MODE 5 (GT u/v-step): scalar weight v [k], updated in place
+    float *x_out;                           // kernel 3 MODE 5: x = u / v [k][count]
     int push;                               // kernel 3 across GPUs: writers push into the readers' inboxes
     unsigned long long inbox_off;           // push: wire dtype [n source agents][2 parities][cap] in every heap
     unsigned long long inbox_agent_stride, inbox_parity_stride;   // bytes
@@ -202,6 +210,8 @@ struct WinParams {
     int dtype;                              // 0 fp32, 1 bf16 (slot dtype = x dtype)
     int overwrite;                          // put
     int ef;                                 // error feedback of the bf16 wire rounding into the outbox
+    const void *g;                          // gradient-in-window push (window dtype, [k][count]) or null
+    float lr;
     int with_p;
     unsigned long long agent_mask;
     int maxdin, maxdout;

@@ -28,6 +28,7 @@ cudaError_t launch_fused_nar(const ExchParams &p, int x_kind, int grid, cudaStre
 cudaError_t launch_fused_atc(const ExchParams &p, int g_kind, int wire_kind, int grid, cudaStream_t s);
 cudaError_t launch_fused_awc(const ExchParams &p, int g_kind, int wire_kind, int grid, cudaStream_t s);
 cudaError_t launch_fused_ed(const ExchParams &p, int g_kind, int wire_kind, int grid, cudaStream_t s);
+cudaError_t launch_fused_gt(const ExchParams &p, int wire_kind, int grid, cudaStream_t s);
 
 // Shared-memory ring of the TMA-prefetched x / g tiles (2 stages).
 template <typename XT, typename GT, bool HAS_G>
@@ -510,6 +511,10 @@ bool fused_supported(int k, int nprocs) { return k == 1 || k == 2 || k == 4 || (
 
 static cudaError_t launch_fused(const ExchParams &p, int x_kind, int g_kind, int wire_kind, int y_kind, int has_g,
                                 int grid, cudaStream_t s) {
+    if (p.gt) {   // push-sum gradient tracking: fp32 tensors
+        if (x_kind != 0 || y_kind != 0 || g_kind != 0) return cudaErrorInvalidValue;
+        return launch_fused_gt(p, wire_kind, grid, s);
+    }
     if (p.awc) {   // AWC: fp32 master x, wire = the x value in the wire dtype
         if (x_kind != 0 || y_kind != 0) return cudaErrorInvalidValue;
         return launch_fused_awc(p, p.g_bf16 ? 1 : 0, wire_kind, grid, s);

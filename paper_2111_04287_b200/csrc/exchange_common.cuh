@@ -160,6 +160,44 @@ static __device__ void write_descriptors(const ExchParams &p, unsigned long long
     }
 }
 
+// Push-sum gradient tracking, u/v-step (MODE 5): the scalar weights v_j of the
+// sources, combined with the step's coefficients -- v_a <- w_aa v_a + sum_j w_aj v_j
+// (appendix line 1003 with v^0 = 1, so every entry of the paper's vector v is
+// the same scalar).  Block 0 publishes the local agents' v in the pad for this
+// epoch; every CTA reads same-process weights from p.gt_v and other processes'
+// from their pads (bounded spin on the epoch tag).  Returns false on a fault.
+static __device__ bool gt_weights(const ExchParams &p, unsigned long long e, const SharedTab &st, float *vnew) {
+    const Geometry &g = p.geo;
+    const int k = g.k, parity = static_cast<int>(e & 1);
+    if (blockIdx.x == 0 && threadIdx.x < k) {
+        Pad *pad = pad_of(g, g.me);
+        pad->gtv[threadIdx.x][parity] = p.gt_v[threadIdx.x];
+        st_release(&pad->gtv_tag[threadIdx.x][parity], e, g.nprocs > 1);
+    }
+    bool ok = true;
+    if (threadIdx.x < k) {
+        const int a = threadIdx.x;
+        float acc = st.self_w[a] * p.gt_v[a];
+        for (int q = 0; q < st.nsrc[a]; ++q) {
+            const int j = st.src[a][q];
+            float vj;
+            if (j / k == g.me) {
+                vj = p.gt_v[j % k];
+            } else {
+                Pad *pj = pad_of(g, j / k);
+                if (!spin_ge(g, &pj->gtv_tag[j % k][parity], e)) {
+                    ok = false;
+                    break;
+                }
+                vj = *reinterpret_cast<volatile float *>(&pj->gtv[j % k][parity]);
+            }
+            acc = fmaf(st.coef[a][q], vj, acc);
+        }
+        vnew[a] = acc;
+    }
+    return __syncthreads_and(ok);
+}
+
 // Walks the items w = first, first + stride, ... as (tile t, local agent a)
 // with w = t*k + a, without integer division in the loop.
 struct ItemIt {

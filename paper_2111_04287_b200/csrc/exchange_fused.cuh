@@ -44,6 +44,11 @@ namespace bf {
 //   MODE 2: AWC  (Eq. 16):           y_a = sum_b w_ab x_b - lr g_a
 //   MODE 3: Exact-Diffusion (appendix ed-1..ed-3): psi = x - lr g (stored over
 //           psi_prev), phi = psi + x - psi_prev, y_a = sum_b w_ab phi_b
+//   MODE 4: push-sum gradient tracking, y-step (appendix):
+//           y_a = sum_b w_ab (y_b + g_b - g2_b)    (x = y, g = g^(k+1), g2 = g^(k))
+//   MODE 5: push-sum gradient tracking, u/v-step (lines 1002-1004):
+//           u_a = sum_b w_ab (u_b - lr y_b)  (x = u, g = y),  v_a = sum_b w_ab v_b
+//           (scalar weights, gt_weights), x_out_a = u_a / v_a
 // Summation order (R18): self, local sources in (a - b) mod K order, then the
 // remote sources in table order; a neighbour's term always uses the value as it
 // travels on the wire (bf16 RNE for a bf16 wire), the self term the fp32 value.
@@ -148,6 +153,10 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     if (p.wmode == kWDynamic) write_descriptors(p, e);
     ok = resolve_sources(p, e, st) && ok;
     if (!ok) return;   // fault latched; nothing in flight yet
+    __shared__ float s_vnew[K];
+    if constexpr (MODE == 5) {
+        if (!gt_weights(p, e, st, s_vnew)) return;
+    }
 
     // ---- split every agent's sources into the local block and the remote list ----
     if (threadIdx.x == 0) {
@@ -324,11 +333,19 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                     if (!((pub >> a) & 1u)) continue;
                     float v[V];
                     VecN<XT, V>::load_hint(xrow(a) + base + e0, v, valid, vec, pol_keep);
-                    if constexpr (MODE == 1) {
+                    if constexpr (MODE == 1 || MODE == 5) {
                         float gv[V];
                         VecN<GT, V>::load_hint(grow(a) + base + e0, gv, valid, vec, pol_keep);
 #pragma unroll
                         for (int i = 0; i < V; ++i) v[i] = fmaf(-p.lr, gv[i], v[i]);
+                    }
+                    if constexpr (MODE == 4) {   // GT y-step: y + g - g_prev
+                        float gv[V], hv[V];
+                        VecN<GT, V>::load_hint(grow(a) + base + e0, gv, valid, vec, pol_keep);
+                        VecN<float, V>::load_hint(p.g2 + static_cast<long long>(a) * count + base + e0, hv, valid, vec,
+                                                  pol_keep);
+#pragma unroll
+                        for (int i = 0; i < V; ++i) v[i] = (v[i] + gv[i]) - hv[i];
                     }
                     if constexpr (MODE == 3) {   // Exact-Diffusion: phi = (x - lr g) + x - psi_prev
                         float gv[V], pv[V];
@@ -353,7 +370,10 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                 // every local load of the group is issued (raw) before the first use
                 typename VecN<XT, V>::Raw xr[U][K];
                 typename VecN<GT, V>::Raw gr[U][HAS_G ? K : 1];
-                typename VecN<float, MODE == 3 ? V : 4>::Raw pr[U][MODE == 3 ? K : 1];   // Exact-Diffusion psi^(k-1)
+                // third stream: Exact-Diffusion psi^(k-1) (MODE 3), gradient tracking g^(k) (MODE 4)
+                constexpr bool THIRD = MODE == 3 || MODE == 4;
+                const float *third = MODE == 3 ? p.psi : p.g2;
+                typename VecN<float, THIRD ? V : 4>::Raw pr[U][THIRD ? K : 1];
                 // one branch per group: the common case is a straight line of vector loads
                 bool fast = vec;
 #pragma unroll
@@ -369,10 +389,10 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
 #pragma unroll
                             for (int a = 0; a < K; ++a) VecN<GT, V>::load_raw_fast(grow(a) + base, gr[u][a], pol_stream);
                         }
-                        if constexpr (MODE == 3) {
+                        if constexpr (THIRD) {
 #pragma unroll
                             for (int a = 0; a < K; ++a)
-                                VecN<float, V>::load_raw_fast(p.psi + static_cast<long long>(a) * count + base, pr[u][a],
+                                VecN<float, V>::load_raw_fast(third + static_cast<long long>(a) * count + base, pr[u][a],
                                                               pol_stream);
                         }
                     }
@@ -390,10 +410,10 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                             for (int a = 0; a < K; ++a)
                                 VecN<GT, V>::load_raw(grow(a) + base + e0, gr[u][a], valid, pol_stream);
                         }
-                        if constexpr (MODE == 3) {
+                        if constexpr (THIRD) {
 #pragma unroll
                             for (int a = 0; a < K; ++a)
-                                VecN<float, V>::load_raw(p.psi + static_cast<long long>(a) * count + base + e0, pr[u][a],
+                                VecN<float, V>::load_raw(third + static_cast<long long>(a) * count + base + e0, pr[u][a],
                                                          valid, pol_stream);
                         }
                     }
@@ -404,6 +424,12 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                     for (int a = 0; a < K; ++a) {
                         VecN<XT, V>::unpack(xr[u][a], xv[u][a]);
                         if constexpr (HAS_G) VecN<GT, V>::unpack(gr[u][a], gv[u][a]);
+                        if constexpr (MODE == 4) {   // GT y-step: y + g - g_prev
+                            float hv[V];
+                            VecN<float, V>::unpack(pr[u][a], hv);
+#pragma unroll
+                            for (int i = 0; i < V; ++i) xv[u][a][i] = (xv[u][a][i] + gv[u][a][i]) - hv[i];
+                        }
                         if constexpr (MODE == 3) {   // psi_prev kept in gv's place after use below
                             float pv[V];
                             VecN<float, V>::unpack(pr[u][a], pv);
@@ -420,7 +446,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
             for (int u = 0; u < nu; ++u) {
                 const long long base = static_cast<long long>(sub(mc + u)) * kSubT;
                 const int valid = clamp_valid_v<V>(count - base, e0);
-                if constexpr (MODE == 1) {
+                if constexpr (MODE == 1 || MODE == 5) {
 #pragma unroll
                     for (int a = 0; a < K; ++a)
 #pragma unroll
@@ -474,6 +500,13 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                         bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base + e0;
                         VecN<bf16, V>::store_hint(sr, acc, valid, vec, pol_stream);
                     }
+                    if constexpr (MODE == 5) {   // x = u / v (appendix)
+                        const float vn = s_vnew[a];
+#pragma unroll
+                        for (int i = 0; i < V; ++i) acc[i] = acc[i] / vn;
+                        VecN<float, V>::store_hint(p.x_out + static_cast<long long>(a) * count + base + e0, acc, valid,
+                                                   vec, pol_stream);
+                    }
                 }
                 consumed += nrt;
             }
@@ -484,6 +517,8 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     BF_STAT(if (stat && threadIdx.x == 0) stat[0] = globaltimer() - t_k0;)
     if (*fail) return;   // nothing is in flight any more; the fault is latched
     last_cta(pad, [&] {
+        if constexpr (MODE == 5)
+            for (int a = 0; a < K; ++a) p.gt_v[a] = s_vnew[a];
         pad->epoch = e;
         if (p.wmode == kWSchedule) pad->round = pad->round + 1;
         publish_done(g, e);

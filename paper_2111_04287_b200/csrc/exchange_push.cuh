@@ -40,6 +40,16 @@ namespace bf {
 #ifndef BF_PUSH_BATCH
 #define BF_PUSH_BATCH 4
 #endif
+// signal warps: a system-scope release fence waits for every store the SM issued
+// before it -- BF_STATS measured ~14 us per fence at K = 1 with NVLink stores in
+// flight, so one warp fencing batch after batch paces the whole exchange (fence
+// time ~ 90% of the kernel).  NSIG warps fence different batches concurrently
+// (batch rb -> warp rb mod NSIG): the latency stays, the throughput of releases
+// scales; progress words are raised with a remote atomic max, so a later batch's
+// release overtaking an earlier one never moves a word backwards.
+#ifndef BF_PUSH_NSIG
+#define BF_PUSH_NSIG 4
+#endif
 
 template <int K, int V>
 struct PushCfg {
@@ -49,9 +59,15 @@ struct PushCfg {
     static constexpr int kByBytes = BF_PUSH_SMEM_KB * 1024 / kPerSub;
     static constexpr int kLag = kByBytes < BF_PUSH_LAG ? (kByBytes < 2 ? 2 : kByBytes) : BF_PUSH_LAG;
     static constexpr int kSmem = kLag * kPerSub;
-    static constexpr int kThreadsPerCta = kThreads + 64;   // 8 consumer warps + signal warp + poll warp
+    static constexpr int kThreadsPerCta = kThreads + 32 * (1 + BF_PUSH_NSIG);   // consumers + poll + signal warps
 };
 constexpr int kPushBatch = BF_PUSH_BATCH;
+constexpr int kPushSig = BF_PUSH_NSIG;
+static_assert(kPubRing % kPushSig == 0, "a publish-barrier slot must always map to the same signal warp");
+
+__device__ __forceinline__ void red_max_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 template <int K>
 struct PushMix {
@@ -84,23 +100,33 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2
     __shared__ SharedTab st;
     __shared__ PushMix<K> lm;
     __shared__ __align__(8) unsigned long long pubbar[kPubRing];
-    __shared__ int s_fail, s_released, s_ready;
+    __shared__ int s_fail, s_ready;
+    __shared__ int s_rel[kPubRing];   // last batch whose publish barrier phase a signal warp has consumed
     volatile int *const fail = &s_fail;
     const Geometry &g = p.geo;
     Pad *pad = pad_of(g, g.me);
     if (aborted(g)) return;
+    // BF_STATS (diagnostic build): 0 kernel ns, 1 consumer ns waiting for remote tiles,
+    // 2 ns until the first remote batch was seen, 3 ns until the consumer loop ended,
+    // 4 release-fence ns, 5 fences, 6 progress polls, 7 prologue ns
+    BF_STAT(const unsigned long long t_k0 = globaltimer();)
+    BF_STAT(unsigned long long *const stat = p.stats ? p.stats + blockIdx.x * 8 : nullptr;)
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&pad->epoch) + 1;
     const int parity = static_cast<int>(e & 1);
     if (threadIdx.x == 0) {
         s_fail = 0;
-        s_released = 0;
         s_ready = 0;
+        for (int i = 0; i < kPubRing; ++i) s_rel[i] = i - kPubRing;
         for (int i = 0; i < kPubRing; ++i) mbar_init(&pubbar[i], kThreads);
         fence_mbar_init();
     }
     bool ok = war_wait(g, e);
     ok = resolve_sources(p, e, st) && ok;
     if (!ok) return;
+    __shared__ float s_vnew[K];
+    if constexpr (MODE == 5) {
+        if (!gt_weights(p, e, st, s_vnew)) return;
+    }
 
     if (threadIdx.x == 0) {
         unsigned procs = 0;
@@ -140,6 +166,7 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2
         lm.procs_out_all = all;
     }
     __syncthreads();
+    BF_STAT(if (stat && threadIdx.x == 0) stat[7] = globaltimer() - t_k0;)
 
     const bool vec = g.vec_ok != 0;
     const long long count = g.count;
@@ -159,22 +186,25 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2
         return at<unsigned long long>(g.peer_base[q], p.pflag_off) + static_cast<long long>(w) * kMaxGrid + blockIdx.x;
     };
 
-    if (warp == kThreads / 32) {
-        // ================ signal warp (lane 0): system-scope releases ================
+    if (warp >= kThreads / 32 + 1) {
+        // ============ signal warps (lane 0): system-scope releases, batch rb -> warp rb mod NSIG ============
+        const int sw = warp - (kThreads / 32 + 1);
         const int nbatch = lm.procs_out_all ? (nmine + kPushBatch - 1) / kPushBatch : 0;
-        if (lane == 0 && nbatch > 0) {
-            volatile int *released = &s_released;
-            for (int rb = 0; rb < nbatch; ++rb) {
+        if (lane == 0) {
+            volatile int *rel = s_rel;
+            for (int rb = sw; rb < nbatch; rb += kPushSig) {
                 if (!mbar_wait_acq_b(g, &pubbar[rb % kPubRing], static_cast<unsigned>(rb / kPubRing) & 1u, fail)) break;
+                rel[rb % kPubRing] = rb;   // the barrier slot may take its next phase
                 const int done = min((rb + 1) * kPushBatch, nmine);
+                BF_STAT(const unsigned long long tf = globaltimer();)
                 fence_acq_rel(true);   // the consumers' remote inbox stores, visible system-wide ...
+                BF_STAT(if (stat) { atomicAdd(stat + 4, globaltimer() - tf); atomicAdd(stat + 5, 1ull); })
                 for (int q = 0; q < g.nprocs; ++q)   // ... before the progress word in every reader's heap
                     if ((lm.procs_out_all >> q) & 1u)
-                        st_relaxed(pflag(q, g.me), (e << kProgShift) | static_cast<unsigned long long>(done), true);
-                *released = rb + 1;
+                        red_max_sys(pflag(q, g.me), (e << kProgShift) | static_cast<unsigned long long>(done));
             }
         }
-    } else if (warp == kThreads / 32 + 1) {
+    } else if (warp == kThreads / 32) {
         // ===== poll warp (lane 0): local progress words of the writers -> s_ready =====
         if (lane == 0 && nrt > 0 && nmine > 0) {
             unsigned long long seen[kMaxP];
@@ -187,11 +217,15 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2
                 for (int q = 0; q < g.nprocs; ++q) {
                     if (!((lm.procs_in >> q) & 1u)) continue;
                     const unsigned long long need = (e << kProgShift) | static_cast<unsigned long long>(ready + 1);
-                    if (seen[q] < need) seen[q] = ld_acquire_sys(pflag(g.me, q));
+                    if (seen[q] < need) {
+                        seen[q] = ld_acquire_sys(pflag(g.me, q));
+                        BF_STAT(if (stat) stat[6] += 1;)
+                    }
                     const long long c = static_cast<long long>(seen[q]) - static_cast<long long>(e << kProgShift);
                     lo = min(lo, c <= 0 ? 0 : static_cast<int>(c));
                 }
                 if (lo > ready) {
+                    BF_STAT(if (stat && ready == 0) stat[2] = globaltimer() - t_k0;)
                     ready = lo;
                     st_release_cta_shared(&s_ready, ready);
                     t_idle = globaltimer();
@@ -238,6 +272,7 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2
                             }
                             __nanosleep(32);
                         }
+                        BF_STAT(if (stat && threadIdx.x == 0) stat[1] += globaltimer() - t0;)
                     }
                     if (*fail) break;
                 }
@@ -270,6 +305,13 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2
                         bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base + e0;
                         VecN<bf16, V>::store_hint(sr, acc, valid, vec, pol_stream);
                     }
+                    if constexpr (MODE == 5) {   // x = u / v (appendix)
+                        const float vn = s_vnew[a];
+#pragma unroll
+                        for (int i = 0; i < V; ++i) acc[i] = acc[i] / vn;
+                        VecN<float, V>::store_hint(p.x_out + static_cast<long long>(a) * count + base + e0, acc, valid,
+                                                   vec, pol_stream);
+                    }
                 }
             }
             // ---------------- publish sub-item m and park the local part of its combine ----------------
@@ -284,11 +326,21 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2
 #pragma unroll
                     for (int a = 0; a < K; ++a) VecN<GT, V>::load_hint(grow(a) + base + e0, gv[a], valid, vec, pol_stream);
                 }
-                if constexpr (MODE == 1) {   // Eq. 4
+                if constexpr (MODE == 1 || MODE == 5) {   // Eq. 4 (GT: u - lr y)
 #pragma unroll
                     for (int a = 0; a < K; ++a)
 #pragma unroll
                         for (int i = 0; i < V; ++i) xv[a][i] = fmaf(-p.lr, gv[a][i], xv[a][i]);
+                }
+                if constexpr (MODE == 4) {   // GT y-step: y + g - g_prev
+#pragma unroll
+                    for (int a = 0; a < K; ++a) {
+                        float hv[V];
+                        VecN<float, V>::load_hint(p.g2 + static_cast<long long>(a) * count + base + e0, hv, valid, vec,
+                                                  pol_stream);
+#pragma unroll
+                        for (int i = 0; i < V; ++i) xv[a][i] = (xv[a][i] + gv[a][i]) - hv[i];
+                    }
                 }
                 if constexpr (MODE == 3) {   // Exact-Diffusion: psi = x - lr g (stored), phi = psi + x - psi_prev
 #pragma unroll
@@ -344,18 +396,22 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2
                 }
                 if (lm.procs_out_all && ((m + 1) % kPushBatch == 0 || m + 1 == nmine)) {
                     const int b = m / kPushBatch;
-                    if (b >= kPubRing) {   // the ring slot's previous phase must have been released
-                        volatile int *released = &s_released;
-                        while (*released <= b - kPubRing && !*fail) __nanosleep(64);
+                    if (b >= kPubRing) {   // the slot's previous phase must have been consumed by its signal warp
+                        volatile int *rel = s_rel;
+                        while (rel[b % kPubRing] < b - kPubRing && !*fail) __nanosleep(64);
                     }
                     mbar_arrive_release(&pubbar[b % kPubRing]);
                 }
             }
         }
     }
+    BF_STAT(if (stat && threadIdx.x == 0) stat[3] = globaltimer() - t_k0;)
     __syncthreads();
+    BF_STAT(if (stat && threadIdx.x == 0) stat[0] = globaltimer() - t_k0;)
     if (*fail) return;
     last_cta(pad, [&] {
+        if constexpr (MODE == 5)
+            for (int a = 0; a < K; ++a) p.gt_v[a] = s_vnew[a];
         pad->epoch = e;
         if (p.wmode == kWSchedule) pad->round = pad->round + 1;
         publish_done(g, e);

@@ -768,11 +768,18 @@ bf_status bf_reserve(bf_ctx *c, size_t bytes_per_agent) {
 }
 
 // ---- hot path ---------------------------------------------------------------
+struct GtArgs {                     // push-sum gradient tracking steps (MODE 4 / 5)
+    int mode = 0;
+    const float *g2 = nullptr;
+    float *v = nullptr;
+    float *x_out = nullptr;
+};
+
 static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *y, void *shadow, size_t count,
                                  int x_kind, int g_kind, int wire_kind, int y_kind, float lr,
                                  const bf_weights *weights, cudaStream_t st, const void *awc_g = nullptr,
                                  const SrcTab *static_tab = nullptr, float *psi = nullptr,
-                                 unsigned static_pub = 0) {
+                                 unsigned static_pub = 0, const GtArgs *gt = nullptr) {
     if (count == 0) return BF_OK;
     if (count > (1ull << 40)) return fail(BF_ERR_ARG, "count too large");
     ExchParams p;
@@ -839,6 +846,17 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
         p.psi = psi;
     }
     p.cflag_off = c->cflag_off;
+    if (gt) {   // gradient tracking: only the fused kernel implements MODE 4 / 5
+        if (p.kernel != 3)
+            return fail(BF_ERR_UNSUPPORTED, "gradient tracking needs the fused exchange kernel (agents_per_proc 1, 2, "
+                                            "4 or 8 on one GPU)");
+        p.gt = gt->mode;
+        p.g2 = gt->g2;
+        p.gt_v = gt->v;
+        p.x_out = gt->x_out;
+        if (gt->g2 && !aligned16(gt->g2)) p.geo.vec_ok = 0;
+        if (gt->x_out && !aligned16(gt->x_out)) p.geo.vec_ok = 0;
+    }
     // cross-GPU push variant (exchange_push.cuh): static topologies and schedules at
     // K = 1, 2, when the inboxes fit in the heap; per-call views and the caller-assembled
     // hierarchical W keep the pull kernel
@@ -934,6 +952,42 @@ bf_status bf_exact_diffusion_step(bf_ctx *c, float *x, const void *g, bf_dtype g
         return fail(BF_ERR_ARG, "bf_exact_diffusion_step takes device tensors");
     return exchange_common(c, x, g, x, nullptr, count, 0, g_dtype, wire, 0, lr, weights,
                            static_cast<cudaStream_t>(stream), nullptr, nullptr, psi);
+}
+
+// Push-sum gradient tracking (appendix), one fused launch
+// per partial averaging.
+bf_status bf_gt_uv_step(bf_ctx *c, float *u, float *v, const float *y, float *x_out, size_t count, float lr,
+                        bf_dtype wire, const bf_weights *weights, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (count == 0) return BF_OK;
+    if (!u || !v || !y || !x_out) return fail(BF_ERR_ARG, "null tensor");
+    if (wire != BF_FLOAT32 && wire != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
+    if (!std::isfinite(lr)) return fail(BF_ERR_ARG, "non-finite lr");
+    if (is_host_ptr(u) || is_host_ptr(v) || is_host_ptr(y) || is_host_ptr(x_out))
+        return fail(BF_ERR_ARG, "bf_gt_uv_step takes device tensors");
+    GtArgs gt;
+    gt.mode = 5;
+    gt.v = v;
+    gt.x_out = x_out;
+    return exchange_common(c, u, y, u, nullptr, count, 0, 0, wire, 0, lr, weights, static_cast<cudaStream_t>(stream),
+                           nullptr, nullptr, nullptr, 0, &gt);
+}
+
+bf_status bf_gt_y_step(bf_ctx *c, float *y, const float *g, const float *g_prev, size_t count, bf_dtype wire,
+                       const bf_weights *weights, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (count == 0) return BF_OK;
+    if (!y || !g || !g_prev) return fail(BF_ERR_ARG, "null tensor");
+    if (wire != BF_FLOAT32 && wire != BF_BFLOAT16) return fail(BF_ERR_UNSUPPORTED, "dtype");
+    if (is_host_ptr(y) || is_host_ptr(g) || is_host_ptr(g_prev))
+        return fail(BF_ERR_ARG, "bf_gt_y_step takes device tensors");
+    GtArgs gt;
+    gt.mode = 4;
+    gt.g2 = g_prev;
+    return exchange_common(c, y, g, y, nullptr, count, 0, 0, wire, 0, 0.f, weights, static_cast<cudaStream_t>(stream),
+                           nullptr, nullptr, nullptr, 0, &gt);
 }
 
 // hmode 0: y = (W_M (x) J_L/L) x; 1 (H-ATC): x <- (W_M (x) J_L/L)(x - lr g);
@@ -1237,7 +1291,7 @@ static bf_status win_setup(bf_ctx *c, Window *w, uint64_t agent_mask, WinParams 
 }
 
 static bf_status win_push(bf_ctx *c, const char *name, const bf_weights *weights, uint64_t agent_mask,
-                          int overwrite, void *stream) {
+                          int overwrite, void *stream, const void *grad = nullptr, float lr = 0.f) {
     bf_status s = check_ctx(c);
     if (s) return s;
     Window *w = find_win(c, name);
@@ -1246,6 +1300,9 @@ static bf_status win_push(bf_ctx *c, const char *name, const bf_weights *weights
     win_setup(c, w, agent_mask, p);
     p.overwrite = overwrite;
     p.ef = (w->dtype == BF_BFLOAT16 && !overwrite && w->ef) ? 1 : 0;
+    p.g = grad;
+    p.lr = lr;
+    if (grad && !aligned16(grad)) p.geo.vec_ok = 0;
     for (int a = 0; a < c->k; ++a) {
         const int gid = c->proc * c->k + a;
         const auto &outs = w->side[gid].out;
@@ -1299,6 +1356,16 @@ bf_status bf_win_accumulate(bf_ctx *c, const char *name, const bf_weights *weigh
                             uint64_t agent_mask, void *stream) {
     (void)require_mutex;   // the versioned SPSC slot protocol is the mutex
     return win_push(c, name, weights, agent_mask, 0, stream);
+}
+
+bf_status bf_win_accumulate_grad(bf_ctx *c, const char *name, const void *g, float lr, const bf_weights *weights,
+                                 uint64_t agent_mask, void *stream) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!g) return fail(BF_ERR_ARG, "null gradient");
+    if (!std::isfinite(lr)) return fail(BF_ERR_ARG, "non-finite lr");
+    if (is_host_ptr(g)) return fail(BF_ERR_ARG, "bf_win_accumulate_grad takes a device gradient");
+    return win_push(c, name, weights, agent_mask, 0, stream, g, lr);
 }
 
 static bf_status win_pull(bf_ctx *c, const char *name, const bf_weights *weights, void *out, uint64_t agent_mask,

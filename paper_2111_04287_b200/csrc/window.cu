@@ -43,15 +43,43 @@ __global__ void win_push_decide(const __grid_constant__ WinParams p) {
     }
 }
 
-// Elements per thread-vector (16-byte accesses of the window dtype) and vectors
-// per thread per tile; element of vector j of this thread: (j*kThreads + tid)*V.
+// Elements per thread-vector (16-byte accesses of the window dtype), vectors per
+// thread per item, and elements per item (the window kernels' own tile):
+// element of vector j of this thread: (j*kThreads + tid)*V.  NV = 8 keeps 8
+// independent 16-byte loads of every stream in flight per thread (the r01 tile of
+// 4096 elements gave 2 per bf16 thread: ncu showed 48-55% of DRAM peak, latency-bound).
+// (BF_WIN_BYTES / 16 fp32 vectors, half as many 8 x bf16 vectors, per stream; the fp32 outbox streams of a backlogged
+// destination are walked vector by vector -- the rare path.)
+#ifndef BF_WIN_BYTES
+#define BF_WIN_BYTES 128   // bytes of each stream in flight per thread
+#endif
 template <typename T>
 struct WinVec {
     static constexpr int V = sizeof(T) >= 4 ? 4 : 8;
-    static constexpr int NV = kTile / (kThreads * V);
+    static constexpr int NV = BF_WIN_BYTES / 16 / (sizeof(T) >= 4 ? 1 : 2);   // 32 fp32 values per stream
+    static constexpr int TILE = NV * kThreads * V;
 };
 template <int V>
 __device__ __forceinline__ int win_elem(int j) { return (j * kThreads + threadIdx.x) * V; }
+template <typename T>
+__host__ __device__ __forceinline__ long long win_items(int k, long long count) {
+    return static_cast<long long>(k) * ((count + WinVec<T>::TILE - 1) / WinVec<T>::TILE);
+}
+
+// all NV raw vectors of one stream of an item, issued before any use
+template <typename T, int V, int NV>
+__device__ __forceinline__ void win_load_raw(const T *base, typename VecN<T, V>::Raw (&r)[NV], long long rem,
+                                             bool vec) {
+    if (vec && rem >= static_cast<long long>(NV) * kThreads * V) {
+        const unsigned long long pol = policy_evict_normal();
+#pragma unroll
+        for (int j = 0; j < NV; ++j) VecN<T, V>::load_raw_fast(base + win_elem<V>(j), r[j], pol);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            VecN<T, V>::load_raw(base + win_elem<V>(j), r[j], clamp_valid_v<V>(rem, win_elem<V>(j)), 0ull);
+    }
+}
 
 // min CTAs per SM for the streaming window kernels (0 = no bound; tuning variants: -DBF_WIN_COLLECT_MINB=6)
 #ifndef BF_WIN_PUSH_MINB
@@ -81,9 +109,11 @@ __device__ __forceinline__ int win_elem(int j) { return (j * kThreads + threadId
 #else
 #define BF_COLLECT_LB __launch_bounds__(kThreads)
 #endif
-template <typename T>
+// SGD = true: the gradient-in-window variant (SGP-style, bf_win_accumulate_grad):
+// x_half = x - lr g (Eq. 4) replaces x before the payloads and the self scaling.
+template <typename T, bool SGD>
 __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) {
-    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV;
+    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV, TILE = WinVec<T>::TILE;
     const Geometry &g = p.geo;
     const unsigned long long me = g.peer_base[g.me];
     Pad *pad = pad_of(g, g.me);
@@ -93,25 +123,27 @@ __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) 
     const unsigned long long *dec = at<unsigned long long>(me, p.dec_off);
     const unsigned long long *dlv = at<unsigned long long>(me, p.delivered_off);
     const unsigned int *obv = at<unsigned int>(me, p.obvalid_off);
-    const long long items = static_cast<long long>(k) * g.T;
+    const long long items = win_items<T>(k, count);
     for (long long w = blockIdx.x; w < items; w += gridDim.x) {
         const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
         if (!active(p, a)) continue;
-        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        const long long base = static_cast<long long>(t) * TILE, rem = count - base;
         T *xr = static_cast<T *>(p.x) + static_cast<long long>(a) * count + base;
-        // x and the first destination's outbox are loaded before the first use
-        float xv[NV][V], ob0[NV][V];
-        const bool ob0_used = p.nout[a] > 0 && obv[a * p.maxdout + p.out_q[a][0]] != 0 && !p.overwrite;
-        const float *ob0p = at<float>(me, p.outbox_off) +
-                            static_cast<long long>(a * p.maxdout + (p.nout[a] > 0 ? p.out_q[a][0] : 0)) * p.cpad + base;
+        typename VecN<T, V>::Raw xraw[NV];
+        win_load_raw<T, V, NV>(xr, xraw, rem, vec);
+        typename VecN<T, V>::Raw graw[SGD ? NV : 1];
+        if constexpr (SGD)
+            win_load_raw<T, V, NV>(static_cast<const T *>(p.g) + static_cast<long long>(a) * count + base, graw, rem, vec);
+        // x (or x - lr g) of vector j as fp32
+        auto xval = [&](int j, float *xv) {
+            VecN<T, V>::unpack(xraw[j], xv);
+            if constexpr (SGD) {
+                float gv[V];
+                VecN<T, V>::unpack(graw[j], gv);
 #pragma unroll
-        for (int j = 0; j < NV; ++j)
-            WIN_LD(T, V, xr + win_elem<V>(j), xv[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
-        if (ob0_used) {
-#pragma unroll
-            for (int j = 0; j < NV; ++j)
-                VecN<float, V>::load(ob0p + win_elem<V>(j), ob0[j], clamp_valid_v<V>(rem, win_elem<V>(j)), true);
-        }
+                for (int i = 0; i < V; ++i) xv[i] = fmaf(-p.lr, gv[i], xv[i]);
+            }
+        };
         for (int q = 0; q < p.nout[a]; ++q) {
             const int qo = p.out_q[a][q], dst = p.out_dst[a][q], qin = p.out_qin[a][q];
             const float s = p.out_s[a][q];
@@ -119,53 +151,62 @@ __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) 
             const bool deliver = dec[ci] != 0;
             const bool use_ob = obv[ci] != 0 && !p.overwrite;
             float *ob = at<float>(me, p.outbox_off) + static_cast<long long>(ci) * p.cpad + base;
-            float pay[NV][V];
-#pragma unroll
-            for (int j = 0; j < NV; ++j) {
-                const int vl = clamp_valid_v<V>(rem, win_elem<V>(j));
-                if (use_ob) {
-                    if (q == 0) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i) pay[j][i] = ob0[j][i];
-                    } else {
-                        VecN<float, V>::load(ob + win_elem<V>(j), pay[j], vl, true);
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < V; ++i) pay[j][i] = use_ob ? fmaf(s, xv[j][i], pay[j][i]) : s * xv[j][i];
-            }
-            if (deliver) {
-                const int half = static_cast<int>(dlv[ci] & 1ull);
-                T *slot = at<T>(g.peer_base[dst / k],
-                                p.slot_off + ((static_cast<unsigned long long>(dst % k) * p.maxdin + qin) * 2 + half) *
-                                                 p.cpad * esize(p)) + base;
+            T *slot = at<T>(g.peer_base[dst / k],
+                            p.slot_off + ((static_cast<unsigned long long>(dst % k) * p.maxdin + qin) * 2 +
+                                          (dlv[ci] & 1ull)) * p.cpad * esize(p)) + base;
+            // payload = (outbox +) s * x  (push-side scaling, Eq. 10)
+            if (use_ob) {   // a backlogged payload to this destination: add onto its outbox
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     const int vl = clamp_valid_v<V>(rem, win_elem<V>(j));
-                    WIN_ST(T, V, slot + win_elem<V>(j), pay[j], vl, vec);
-                    if (p.ef) {   // keep the wire rounding residual (bf16) in the outbox (R24)
-                        float r[V];
+                    float ov[V], xv[V];
+                    VecN<float, V>::load(ob + win_elem<V>(j), ov, vl, true);
+                    xval(j, xv);
 #pragma unroll
-                        for (int i = 0; i < V; ++i) {
-                            const float wire = sizeof(T) == 2 ? bf2f(f2bf(pay[j][i])) : pay[j][i];
-                            r[i] = pay[j][i] - wire;
+                    for (int i = 0; i < V; ++i) ov[i] = fmaf(s, xv[i], ov[i]);
+                    if (deliver) {
+                        WIN_ST(T, V, slot + win_elem<V>(j), ov, vl, vec);
+                        if (p.ef) {   // keep the wire rounding residual (bf16) in the outbox (R24)
+                            float r[V];
+#pragma unroll
+                            for (int i = 0; i < V; ++i) r[i] = ov[i] - (sizeof(T) == 2 ? bf2f(f2bf(ov[i])) : ov[i]);
+                            VecN<float, V>::store(ob + win_elem<V>(j), r, vl, true);
                         }
-                        VecN<float, V>::store(ob + win_elem<V>(j), r, vl, true);
+                    } else {
+                        VecN<float, V>::store(ob + win_elem<V>(j), ov, vl, true);
                     }
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < NV; ++j)
-                    VecN<float, V>::store(ob + win_elem<V>(j), pay[j], clamp_valid_v<V>(rem, win_elem<V>(j)), true);
+                for (int j = 0; j < NV; ++j) {
+                    const int vl = clamp_valid_v<V>(rem, win_elem<V>(j));
+                    float pay[V];
+                    xval(j, pay);
+#pragma unroll
+                    for (int i = 0; i < V; ++i) pay[i] = s * pay[i];
+                    if (deliver) {
+                        WIN_ST(T, V, slot + win_elem<V>(j), pay, vl, vec);
+                        if (p.ef) {
+                            float r[V];
+#pragma unroll
+                            for (int i = 0; i < V; ++i) r[i] = pay[i] - (sizeof(T) == 2 ? bf2f(f2bf(pay[i])) : pay[i]);
+                            VecN<float, V>::store(ob + win_elem<V>(j), r, vl, true);
+                        }
+                    } else {
+                        VecN<float, V>::store(ob + win_elem<V>(j), pay, vl, true);
+                    }
+                }
             }
         }
         const float sw = p.self_w[a];
-        if (sw != 1.0f) {
+        if (sw != 1.0f || SGD) {   // x <- self_weight * x (R8)
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
+                float xv[V];
+                xval(j, xv);
 #pragma unroll
-                for (int i = 0; i < V; ++i) xv[j][i] *= sw;
-                WIN_ST(T, V, xr + win_elem<V>(j), xv[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+                for (int i = 0; i < V; ++i) xv[i] *= sw;
+                WIN_ST(T, V, xr + win_elem<V>(j), xv, clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
             }
         }
     }
@@ -244,62 +285,72 @@ __global__ void BF_COLLECT_LB win_collect_kernel(const __grid_constant__ WinPara
     for (int idx = threadIdx.x; idx < k * p.maxdin; idx += blockDim.x)
         (void)ld_acquire_sys(at<unsigned long long>(me, p.version_off) + idx);
     __syncthreads();
-    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV;
-    const long long items = static_cast<long long>(k) * g.T;
+    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV, TILE = WinVec<T>::TILE;
+    const long long items = win_items<T>(k, count);
     for (long long w = blockIdx.x; w < items; w += gridDim.x) {
         const int t = static_cast<int>(w / k), b = static_cast<int>(w % k);
         if (!active(p, b)) continue;
-        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        const long long base = static_cast<long long>(t) * TILE, rem = count - base;
         const T *xr = static_cast<const T *>(p.x) + static_cast<long long>(b) * count + base;
         T *outr = static_cast<T *>(p.out) + static_cast<long long>(b) * count + base;
         const float sw = update ? p.self_w[b] : 1.0f;
         // the first payload of the first in-neighbour is loaded together with x
         // (the common one-payload case has every load in flight before the first use)
         const T *pre_h = nullptr;
+        float pre_r = 1.0f;
         if (p.nin[b] > 0) {
             const int ci = b * p.maxdin;
             const unsigned long long c0 = snap[ci * 2], v0 = snap[ci * 2 + 1];
             const unsigned long long m0 = update ? v0 - 1 : c0;
-            if (update || c0 < v0)
+            if (update || c0 < v0) {
                 pre_h = at<const T>(me, p.slot_off + (static_cast<unsigned long long>(ci) * 2 + (m0 & 1)) * p.cpad *
                                                          esize(p)) + base;
+                pre_r = update ? p.in_r[b][0] : 1.0f;
+            }
         }
-        float acc[NV][V], pre[NV][V];
+        float acc[NV][V];
+        {
+            typename VecN<T, V>::Raw xraw[NV], praw[NV];
+            win_load_raw<T, V, NV>(xr, xraw, rem, vec);
+            if (pre_h) win_load_raw<T, V, NV>(pre_h, praw, rem, vec);
 #pragma unroll
-        for (int j = 0; j < NV; ++j)
-            WIN_LD(T, V, xr + win_elem<V>(j), acc[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
-        if (pre_h) {
+            for (int j = 0; j < NV; ++j) {
+                VecN<T, V>::unpack(xraw[j], acc[j]);
 #pragma unroll
-            for (int j = 0; j < NV; ++j)
-                VecN<T, V>::load_cg(pre_h + win_elem<V>(j), pre[j], clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+                for (int i = 0; i < V; ++i) acc[j][i] *= sw;
+            }
+            if (pre_h) {
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    float v4[V];
+                    VecN<T, V>::unpack(praw[j], v4);
+#pragma unroll
+                    for (int i = 0; i < V; ++i) acc[j][i] = fmaf(pre_r, v4[i], acc[j][i]);
+                }
+            }
         }
-#pragma unroll
-        for (int j = 0; j < NV; ++j)
-#pragma unroll
-            for (int i = 0; i < V; ++i) acc[j][i] *= sw;
         for (int q = 0; q < p.nin[b]; ++q) {
             const int ci = b * p.maxdin + q;
             const unsigned long long c = snap[ci * 2], v = snap[ci * 2 + 1];
             const float r = update ? p.in_r[b][q] : 1.0f;
             // update: the latest complete payload v-1 (v == 0: the initial copy in half 1);
-            // collect: every delivered payload c..v-1.
+            // collect: every delivered payload c..v-1, in order.
             const unsigned long long m_first = update ? v - 1 : c;
             const unsigned long long m_end = update ? v : v;
             for (unsigned long long m = m_first; update ? (m == m_first) : (m < m_end);
                  m = update ? m_first + 1 : m + 1) {
                 const T *h = at<const T>(me, p.slot_off + (static_cast<unsigned long long>(ci) * 2 + (m & 1)) *
                                                               p.cpad * esize(p)) + base;
+                if (h != pre_h) {   // (pre_h was added first: it is the first of this order)
+                    typename VecN<T, V>::Raw hraw[NV];
+                    win_load_raw<T, V, NV>(h, hraw, rem, vec);
 #pragma unroll
-                for (int j = 0; j < NV; ++j) {
-                    float v4[V];
-                    if (h == pre_h) {   // already loaded with x
+                    for (int j = 0; j < NV; ++j) {
+                        float v4[V];
+                        VecN<T, V>::unpack(hraw[j], v4);
 #pragma unroll
-                        for (int i = 0; i < V; ++i) v4[i] = pre[j][i];
-                    } else {
-                        VecN<T, V>::load_cg(h + win_elem<V>(j), v4, clamp_valid_v<V>(rem, win_elem<V>(j)), vec);
+                        for (int i = 0; i < V; ++i) acc[j][i] = fmaf(r, v4[i], acc[j][i]);
                     }
-#pragma unroll
-                    for (int i = 0; i < V; ++i) acc[j][i] = fmaf(r, v4[i], acc[j][i]);
                 }
                 if (update) break;
             }
@@ -346,18 +397,18 @@ __global__ void BF_COLLECT_LB win_collect_kernel(const __grid_constant__ WinPara
 template <typename T>
 __global__ void __launch_bounds__(kThreads) win_get_kernel(const __grid_constant__ WinParams p,
                                                            unsigned long long x_off) {
-    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV;
+    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV, TILE = WinVec<T>::TILE;
     const Geometry &g = p.geo;
     const unsigned long long me = g.peer_base[g.me];
     const long long count = g.count;
     const bool vec = g.vec_ok != 0;
     const int k = g.k;
     const unsigned long long *ver = at<unsigned long long>(me, p.version_off);
-    const long long items = static_cast<long long>(k) * g.T;
+    const long long items = win_items<T>(k, count);
     for (long long w = blockIdx.x; w < items; w += gridDim.x) {
         const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
         if (!active(p, a)) continue;
-        const long long base = static_cast<long long>(t) * kTile, rem = count - base;
+        const long long base = static_cast<long long>(t) * TILE, rem = count - base;
         for (int q = 0; q < p.nin[a]; ++q) {
             const float r = p.in_r[a][q];
             if (r == 0.f) continue;
@@ -406,8 +457,17 @@ static int stream_grid(long long items) {
 // most one per item
 template <typename F>
 static int occ_grid(F fn, long long items) {
-    static int maxg = 0;
-    if (maxg == 0) maxg = max_coresident(reinterpret_cast<const void *>(fn), kThreads, 0);
+    // co-resident CTAs, cached per kernel (instantiations of one signature share F)
+    static const void *fns[16] = {};
+    static int occ[16] = {};
+    const void *f = reinterpret_cast<const void *>(fn);
+    int slot = 0;
+    while (slot < 15 && fns[slot] && fns[slot] != f) ++slot;
+    if (fns[slot] != f) {
+        fns[slot] = f;
+        occ[slot] = max_coresident(f, kThreads, 0);
+    }
+    const int maxg = occ[slot];
     long long g = maxg > 0 ? maxg : stream_grid(items);
     if (items < g) g = items;
     return g < 1 ? 1 : static_cast<int>(g);
@@ -415,22 +475,32 @@ static int occ_grid(F fn, long long items) {
 
 cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s) {
     win_push_decide<<<1, 256, 0, s>>>(p);
+    const long long items = p.dtype == 0 ? win_items<float>(p.geo.k, p.geo.count) : win_items<bf16>(p.geo.k, p.geo.count);
+    if (p.g) {
+        if (grid <= 0)
+            grid = p.dtype == 0 ? occ_grid(win_push_kernel<float, true>, items) : occ_grid(win_push_kernel<bf16, true>, items);
+        if (p.dtype == 0)
+            win_push_kernel<float, true><<<grid, kThreads, 0, s>>>(p);
+        else
+            win_push_kernel<bf16, true><<<grid, kThreads, 0, s>>>(p);
+        return cudaGetLastError();
+    }
     if (grid <= 0)
-        grid = p.dtype == 0 ? occ_grid(win_push_kernel<float>, static_cast<long long>(p.geo.k) * p.geo.T)
-                            : occ_grid(win_push_kernel<bf16>, static_cast<long long>(p.geo.k) * p.geo.T);
+        grid = p.dtype == 0 ? occ_grid(win_push_kernel<float, false>, items) : occ_grid(win_push_kernel<bf16, false>, items);
     if (p.dtype == 0)
-        win_push_kernel<float><<<grid, kThreads, 0, s>>>(p);
+        win_push_kernel<float, false><<<grid, kThreads, 0, s>>>(p);
     else
-        win_push_kernel<bf16><<<grid, kThreads, 0, s>>>(p);
+        win_push_kernel<bf16, false><<<grid, kThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_win_get(const WinParams &p, unsigned long long x_off, cudaStream_t s) {
-    const long long items = static_cast<long long>(p.geo.k) * p.geo.T;
     if (p.dtype == 0)
-        win_get_kernel<float><<<occ_grid(win_get_kernel<float>, items), kThreads, 0, s>>>(p, x_off);
+        win_get_kernel<float><<<occ_grid(win_get_kernel<float>, win_items<float>(p.geo.k, p.geo.count)), kThreads, 0,
+                                s>>>(p, x_off);
     else
-        win_get_kernel<bf16><<<occ_grid(win_get_kernel<bf16>, items), kThreads, 0, s>>>(p, x_off);
+        win_get_kernel<bf16><<<occ_grid(win_get_kernel<bf16>, win_items<bf16>(p.geo.k, p.geo.count)), kThreads, 0,
+                               s>>>(p, x_off);
     win_get_finish<<<1, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
@@ -438,8 +508,8 @@ cudaError_t launch_win_get(const WinParams &p, unsigned long long x_off, cudaStr
 cudaError_t launch_win_collect(const WinParams &p, int update, int grid, cudaStream_t s) {
     win_collect_decide<<<1, 256, 0, s>>>(p);
     if (grid <= 0)
-        grid = p.dtype == 0 ? occ_grid(win_collect_kernel<float>, static_cast<long long>(p.geo.k) * p.geo.T)
-                            : occ_grid(win_collect_kernel<bf16>, static_cast<long long>(p.geo.k) * p.geo.T);
+        grid = p.dtype == 0 ? occ_grid(win_collect_kernel<float>, win_items<float>(p.geo.k, p.geo.count))
+                            : occ_grid(win_collect_kernel<bf16>, win_items<bf16>(p.geo.k, p.geo.count));
     if (p.dtype == 0)
         win_collect_kernel<float><<<grid, kThreads, 0, s>>>(p, update);
     else

@@ -27,7 +27,7 @@ def main():
     agents = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     count = 25_600_000
     k = agents // world
-    ctx = bfp.Context(agents_per_proc=k, heap_bytes=k * 2 * count * 4 + (64 << 20), device=local)
+    ctx = bfp.Context(agents_per_proc=k, heap_bytes=(k + agents) * 2 * count * 4 + (64 << 20), device=local)
     n = ctx.n
     if topo == "one_peer":
         ctx.set_dynamic_schedule("one_peer_exp2", 0)
@@ -44,6 +44,8 @@ def main():
     ctx.exchange_stats(reset=True)
     tau = max(1, (n - 1).bit_length()) if topo == "one_peer" else 1
     names = ["kernel", "cons_wait", "comm_wait_peer", "comm_wait_slot", "fence", "fences", "polls", "prologue"]
+    if os.environ.get("BF_XFER", "push") != "pull" and k <= 2 and world > 1:   # exchange_push.cuh slots
+        names = ["kernel", "cons_wait", "first_ready", "loop_end", "fence", "fences", "polls", "prologue"]
     rows = {r: [] for r in range(tau)}
     for s in range(6 * tau):
         if world > 1:

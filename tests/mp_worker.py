@@ -130,6 +130,35 @@ def main():
     check("exact diffusion", np_(x), ref, We, X, 1e-6,
           np.abs(We) @ (np.abs(X) + 0.1 * np.abs(Ge.astype(np.float64)) + np.abs(Pe.astype(np.float64))))
 
+    # ---- push-sum gradient tracking (appendix): MODE 5 / MODE 4 ----
+    Adj = np.eye(n, dtype=bool)
+    rg = np.random.default_rng(31)
+    for i in range(n):
+        Adj[(i + 1) % n, i] = True
+        for j in rg.choice(n, min(2, n), replace=False):
+            Adj[j, i] = True
+    Wg = Adj / Adj.sum(axis=0, keepdims=True)          # directed, column stochastic
+    ctx.set_topology(Wg)
+    cnt = 30011
+    u, U = inputs(cnt, seed_off=3)
+    y, Y = inputs(cnt, seed_off=4)
+    Vf = np.linspace(0.5, 1.5, n)
+    v = torch.from_numpy(Vf[rows].astype(np.float32)).cuda()
+    xo = torch.empty_like(u)
+    ctx.gt_uv_step(u, v, y, xo, 0.05)
+    torch.cuda.synchronize()
+    Ur, Vr, Xr = ora.gt_uv(Wg, U, Vf.astype(np.float32).astype(np.float64)[:, None], Y, 0.05)
+    check("gt u", np_(u), Ur, Wg, np.abs(U) + 0.05 * np.abs(Y), 1e-6)
+    if np.abs(v.cpu().numpy() - Vr[rows, 0]).max() > 1e-6 * np.abs(Vr).max():
+        failures.append("gt v")
+    if np.abs(np_(xo) - Xr[rows]).max() > 1e-5 * np.abs(Xr).max():
+        failures.append("gt x = u / v")
+    gn, Gn = inputs(cnt, seed_off=5)
+    gp, Gp = inputs(cnt, seed_off=6)
+    ctx.gt_y_step(y, gn, gp)
+    torch.cuda.synchronize()
+    check("gt y", np_(y), ora.gt_y(Wg, Y, Gn, Gp), Wg, np.abs(Y) + np.abs(Gn) + np.abs(Gp), 1e-6)
+
     # ---- hierarchical -------------------------------------------------------------
     for L in sorted({1, 2, n}):
         if n % L or n // L < 1:

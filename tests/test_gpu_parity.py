@@ -761,21 +761,24 @@ def test_exact_diffusion_reaches_exact_minimiser_on_gpu():
     ctx.close()
 
 
-# ------------------------- push-sum gradient tracking from the fused primitives ---
-def test_gradient_tracking_matches_oracle_and_converges():
-    # appendix "Push-sum gradient tracking": 3 partial averagings per round, each a
-    # fused library call (algorithms.gradient_tracking_step), directed column-stochastic W
+# ------------------------- push-sum gradient tracking: two fused launches per round ---
+@pytest.mark.parametrize("n", [1, 2, 5, 8])
+def test_gradient_tracking_matches_oracle_and_converges(n):
+    """appendix "Push-sum gradient tracking" (lines 1000-1006): gt_uv_step (MODE 5:
+    u <- W(u - lr y), v <- W v, x = u / v) and gt_y_step (MODE 4: y <- W(y + g - g_prev)),
+    a directed column-stochastic W; each launch checked against ora.gt_uv / ora.gt_y
+    on the GPU's state (tolerance rule with b = sum_j |w_ij| (|u_j| + lr|y_j|), resp.
+    (|y_j| + |g_j| + |g_prev_j|)); then convergence to the least-squares minimiser."""
     from paper_2111_04287_b200.algorithms import gradient_tracking_step
-    n, m, d, lr = 5, 10, 4, 0.05
+    m, d, lr = 10, 4099, 0.05
     rng = np.random.default_rng(8)
-    A = rng.standard_normal((n, m, d)) / np.sqrt(m)
+    A = rng.standard_normal((n, m, d)) / np.sqrt(m) / 8
     b = rng.standard_normal((n, m))
-    xs = np.linalg.lstsq(A.reshape(n * m, d), b.reshape(n * m), rcond=None)[0]
     Adj = np.eye(n, dtype=bool)
     r2 = np.random.default_rng(2)
     for i in range(n):
         Adj[(i + 1) % n, i] = True
-        for j in r2.choice(n, 2, replace=False):
+        for j in r2.choice(n, min(2, n), replace=False):
             Adj[j, i] = True
     W = Adj / Adj.sum(axis=0, keepdims=True)
     ctx = _ctx(n)
@@ -787,24 +790,48 @@ def test_gradient_tracking_matches_oracle_and_converges():
         X64 = X.double()
         return torch.bmm(At.transpose(1, 2), (torch.bmm(At, X64.unsqueeze(2)).squeeze(2) - bt).unsqueeze(2)) \
             .squeeze(2).float().contiguous()
-    grad_np = lambda X: np.einsum("imd,im->id", A, np.einsum("imd,id->im", A, X) - b)
-    u = torch.zeros(n, d, device="cuda")
-    v = torch.ones(n, 1, device="cuda")
-    g = grad_gpu(u / v)
+    u = _gpu(synthetic.agents_x0(n, d) * 0.1)
+    v = torch.ones(n, device="cuda")
+    g = grad_gpu(u)
     y = g.clone()
-    # step-by-step parity: the GPU state is fed to the oracle every round
-    for _ in range(5):
-        U, V, Y, Gp = _np(u), _np(v), _np(y), _np(g)
-        x, u, v, y, g = gradient_tracking_step(ctx, u, v, y, g, grad_gpu, lr)
+    x = torch.empty_like(u)
+    for step in range(4):
+        U, V, Y = _np(u), _np(v)[:, None], _np(y)
+        ctx.gt_uv_step(u, v, y, x, lr)
         torch.cuda.synchronize()
-        Xr, Ur, Vr, Yr, Gr = ora.gradient_tracking_step(W, U, V, Y, Gp, grad_np, lr)
-        assert np.allclose(_np(v), Vr, rtol=1e-6, atol=0)
-        assert np.allclose(_np(u), Ur, rtol=1e-5, atol=1e-6)
-        assert np.allclose(_np(y), Yr, rtol=1e-4, atol=1e-6)
+        Ur, Vr, Xr = ora.gt_uv(W, U, V, Y, lr)
+        bu = np.abs(W) @ (np.abs(U) + np.float32(lr) * np.abs(Y))
+        assert np.all(np.abs(_np(u) - Ur) <= 1e-6 * bu + 1e-30), f"u step {step}"
+        assert np.allclose(_np(v), Vr[:, 0], rtol=1e-6, atol=0)
+        # x = u / v: the forward error of u scaled by 1/v, plus one fp32 rounding
+        assert np.all(np.abs(_np(x) - Xr) <= (1e-6 * bu + 2.0 ** -24 * np.abs(Xr)) / np.abs(Vr) * 1.001 + 1e-30)
+        gn = grad_gpu(x)
+        Y0, Gn, Gp = _np(y), _np(gn), _np(g)
+        ctx.gt_y_step(y, gn, g)
+        torch.cuda.synchronize()
+        by = np.abs(W) @ (np.abs(Y0) + np.abs(Gn) + np.abs(Gp))
+        assert np.all(np.abs(_np(y) - ora.gt_y(W, Y0, Gn, Gp)) <= 1e-6 * by + 1e-30), f"y step {step}"
+        g = gn
+    # convergence (small problem, d = 4): the listing's loop through the library's two launches
+    ctx.close()
+    d2 = 4
+    A2 = rng.standard_normal((n, m, d2)) / np.sqrt(m)
+    b2 = rng.standard_normal((n, m))
+    xs = np.linalg.lstsq(A2.reshape(n * m, d2), b2.reshape(n * m), rcond=None)[0]
+    ctx = _ctx(n)
+    ctx.set_topology(W)
+    A2t, b2t = torch.from_numpy(A2).cuda(), torch.from_numpy(b2).cuda()
+    g2 = lambda X: torch.bmm(A2t.transpose(1, 2), (torch.bmm(A2t, X.double().unsqueeze(2)).squeeze(2) - b2t)
+                             .unsqueeze(2)).squeeze(2).float().contiguous()
+    u = torch.zeros(n, d2, device="cuda")
+    v = torch.ones(n, device="cuda")
+    gp = g2(u)
+    y = gp.clone()
     for _ in range(3000):
-        x, u, v, y, g = gradient_tracking_step(ctx, u, v, y, g, grad_gpu, lr)
+        x, u, v, y, gp = gradient_tracking_step(ctx, u, v, y, gp, g2, 0.05)
     torch.cuda.synchronize()
-    assert np.abs(_np(x) - xs[None, :]).max() < 1e-4 * np.abs(xs).max()
+    assert abs(float(v.sum()) - n) < 1e-4                      # column-stochastic: sum v = n
+    assert np.abs(_np(x) - xs[None, :]).max() < 1e-4 * max(1.0, np.abs(xs).max())
     ctx.close()
 
 

@@ -340,3 +340,40 @@ def test_window_sync_pushsum_items_exceed_grid(dtype):
         assert np.allclose(ctx.win_p("big"), p, rtol=0, atol=1e-12)
     ctx.win_free("big")
     ctx.close()
+
+
+# ------------------------------- gradient-in-window push (SGP-style) ---
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_win_accumulate_grad_matches_event_model(dtype):
+    """bf_win_accumulate_grad: x <- x - lr g (Eq. 4) fused into the push of
+    win_accumulate, against ora.Window.adapt + accumulate, with random
+    per-agent interleaving of pushes and collects."""
+    n, count, lr = 8, 20011, 0.1
+    Wst = ora.exp2(n)
+    ctx = _ctx(n)
+    ctx.set_topology(Wst)
+    x = _gpu(synthetic.agents_x0(n, count), dtype)
+    X0 = _np(x)
+    ctx.win_create(x, "sgp", zero_init=True, with_p=True)
+    win = ora.Window(Wst, np.concatenate([X0, np.ones((n, 1))], axis=1), zero_init=True)
+    rng = np.random.default_rng(17)
+    for step in range(40):
+        i = int(rng.integers(n))
+        if rng.random() < 0.6:
+            g = _gpu(synthetic.agents_grad(n, count, step), dtype)
+            G = _np(g)
+            ctx.win_accumulate_grad("sgp", g, lr, agent_mask=1 << i)
+            win.adapt(i, np.concatenate([G[i], [0.0]]), lr)
+            outs = ora.out_neighbors(Wst, i)
+            w = 1.0 / (len(outs) + 1)
+            win.accumulate(i, w, {j: w for j in outs})
+        else:
+            ctx.win_update_then_collect("sgp", agent_mask=1 << i)
+            win.collect(i)
+    torch.cuda.synchronize()
+    ref = win.x()
+    tol = 3e-5 if dtype == torch.float32 else 2e-2
+    assert np.abs(_np(x) - ref[:, :-1]).max() < tol
+    assert np.allclose(ctx.win_p("sgp"), ref[:, -1], rtol=0, atol=1e-12)
+    ctx.win_free("sgp")
+    ctx.close()

@@ -795,3 +795,15 @@ def test_gradient_tracking_halves_by_hand_and_vector_v():
     a = ora.gt_uv(Wd, U, v1, Y, 0.1)
     b_ = ora.gt_uv(Wd, U, np.tile(v1, (1, d)), Y, 0.1)
     assert np.array_equal(a[0], b_[0]) and np.array_equal(a[2], b_[2]) and np.array_equal(np.tile(a[1], (1, d)), b_[1])
+
+
+def test_win_adapt_then_accumulate_by_hand():
+    # gradient-in-window (SGP-style): x_1 = 2 - 0.5 * 2 = 1, then accumulate s = 1/2, self 1/2
+    W2 = np.array([[1.0, 1.0], [1.0, 1.0]])
+    win = ora.Window(W2, np.array([[0.0], [2.0]]), zero_init=True)
+    win.adapt(1, np.array([2.0]), 0.5)
+    win.accumulate(1, 0.5, {0: 0.5})
+    win.collect(0)
+    assert win.x()[:, 0].tolist() == [0.5, 0.5]
+    # mass after the step: the step removes lr * g from the total, nothing else does
+    assert win.mass(0) == 1.0

@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c3,c5,h,io,o,e,c2")
+    ap.add_argument("--only", default="c1,c3,c5,h,io,o,e,gt,c2")
     ap.add_argument("--agents", type=int, default=8)
     ap.add_argument("--max-bytes", type=int, default=1 << 30)
     ap.add_argument("--out", default=None)
@@ -88,6 +88,10 @@ def main():
 
     only = set(a.only.split(","))
 
+    def xheap(k, n, bytes_per_agent, extra):
+        # exchange slots (k agents x 2 parities) + across GPUs the push inboxes (n x 2)
+        return (k + (n if world > 1 else 0)) * 2 * bytes_per_agent + extra
+
     # ---------------------------------------------------------------- C1 ----
     if "c1" in only:
         n = 4
@@ -127,7 +131,7 @@ def main():
         n = a.agents
         k = n // world
         maxb = a.max_bytes
-        ctx = bfp.Context(agents_per_proc=k, heap_bytes=k * 2 * maxb + (256 << 20), device=local)
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=xheap(k, n, maxb, 256 << 20), device=local)
         ctx.reserve(maxb)
         W = bfp.topology_matrix("exp2", n)
         for dtype, es in ((torch.float32, 4), (torch.bfloat16, 2)):
@@ -167,7 +171,8 @@ def main():
         n = a.agents
         k = n // world
         count = 25_600_000
-        ctx = bfp.Context(agents_per_proc=k, heap_bytes=8 * k * count * 4 + (1 << 30), device=local)
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=xheap(k, n, count * 4, 6 * k * count * 4 + (1 << 30)),
+                          device=local)
         x = torch.empty(k, count, device="cuda")
         for la in range(k):
             bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + ctx.rank + la)
@@ -211,7 +216,8 @@ def main():
         n = a.agents
         k = n // world
         count = 25_600_000
-        ctx = bfp.Context(agents_per_proc=k, heap_bytes=8 * k * count * 4 + (1 << 30), device=local)
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=xheap(k, n, count * 4, 6 * k * count * 4 + (1 << 30)),
+                          device=local)
         x = torch.empty(k, count, device="cuda")
         g = torch.empty_like(x)
         for la in range(k):
@@ -286,7 +292,7 @@ def main():
         n = a.agents
         k = n // world
         count = 25_600_000
-        ctx = bfp.Context(agents_per_proc=k, heap_bytes=k * 2 * count * 4 + (256 << 20), device=local)
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=xheap(k, n, count * 4, 256 << 20), device=local)
         ctx.set_topology(bfp.topology_matrix("exp2", n))
         x = torch.empty(k, count, device="cuda")
         g = torch.empty(k, count, device="cuda")
@@ -302,6 +308,32 @@ def main():
               "hbm_frac": hbm / peak if world == 1 else None})
         ctx.close()
 
+    # ---------------------------------------------------------------- GT ----
+    # push-sum gradient tracking round (appendix): the two fused
+    # launches (gt_uv_step, gt_y_step) over C4-sized vectors, static exp-2
+    if "gt" in only:
+        n = a.agents
+        k = n // world
+        count = 25_600_000
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=xheap(k, n, count * 4, 256 << 20), device=local)
+        ctx.set_topology(bfp.topology_matrix("exp2", n))
+        u, y, g, gp, xo = (torch.empty(k, count, device="cuda") for _ in range(5))
+        for la in range(k):
+            for i, t in enumerate((u, y, g, gp)):
+                bfp.Context.fill_uniform(t[la], synthetic.SEED_X0 + 10 * i + ctx.rank + la, scale=2.0 ** -7)
+        v = torch.ones(k, device="cuda")
+
+        def gt_round():
+            ctx.gt_uv_step(u, v, y, xo, 1e-3)
+            ctx.gt_y_step(y, g, gp)
+        ms = timed(gt_round, 20)
+        hbm = k * 32 * count        # uv: u, y read + u, x write; y: y, g, g_prev read + y write
+        emit({"config": f"GT push-sum gradient-tracking round (2 fused launches), {n} agents x {count} fp32, "
+                        "static exp-2", "ms_per_round": ms, "rounds_per_s": 1e3 / ms,
+              "hbm_gbs": hbm / (ms * 1e-3) / 1e9 if world == 1 else None,
+              "hbm_frac": hbm / (ms * 1e-3) / 1e9 / peak if world == 1 else None})
+        ctx.close()
+
     # ----------------------------------------------------------------- O ----
     # ATC optimizer over ResNet-50's 161 parameter tensors (tensor fusion into
     # buckets, one fused kernel per bucket), synthetic gradients (§8(f) rank 3)
@@ -312,7 +344,7 @@ def main():
         k = n // world
         shapes = resnet50_param_shapes()
         total = sum(math.prod(sh) for sh in shapes)
-        ctx = bfp.Context(agents_per_proc=k, heap_bytes=k * 2 * total * 4 + (256 << 20), device=local)
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=xheap(k, n, total * 4, 256 << 20), device=local)
         ctx.set_dynamic_schedule("one_peer_exp2", 0)
         for bucket_mb in (4, 25, 128):
             params = [torch.nn.Parameter(torch.zeros(k, *sh, device="cuda")) for sh in shapes]

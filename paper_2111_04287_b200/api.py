@@ -175,8 +175,8 @@ class Context:
             raise ValueError(f"{what} must be contiguous with {ref.numel()} elements (the layout of x)")
         if device:
             self._dev(t, what)
-        elif t.device.type != ref.device.type:
-            raise ValueError(f"{what} must live where x lives ({ref.device})")
+        elif t.is_cuda and t.device.index != self.device:
+            raise ValueError(f"{what} must be on cuda:{self.device} or in host memory (got {t.device})")
         return t
 
     def _views(self, self_weight, src_weights, dst_weights):
@@ -251,7 +251,7 @@ class Context:
             raise ValueError("x must be the fp32 master copy")
         count = self._rows(x)
         # x and g may be host tensors (end-to-end path, staged inside the call)
-        self._like(g, x, "g", device=x.is_cuda and g.is_cuda)
+        self._like(g, x, "g", device=False)
         if shadow is not None:
             if shadow.dtype != torch.bfloat16:
                 raise ValueError("shadow must be bf16")

@@ -32,7 +32,10 @@ __device__ __forceinline__ void publish_done(const Geometry &g, unsigned long lo
     // only other processes wait on done_from (war_wait); one process needs no
     // system-scope release (an idle fence.acq_rel.sys alone costs ~3.5 us)
     if (g.nprocs == 1) return;
-    for (int q = 0; q < g.nprocs; ++q) st_release_sys(&pad_of(g, q)->done_from[g.me], e);
+    // one system-scope fence orders every read of this epoch before all the stores
+    // (a st.release.sys per process would fence once per process)
+    fence_acq_rel(true);
+    for (int q = 0; q < g.nprocs; ++q) st_relaxed(&pad_of(g, q)->done_from[g.me], e, true);
 }
 
 // --------------------------------------------------------------------------

@@ -581,7 +581,8 @@ static cudaError_t launch_fused_t(const ExchParams &p, int grid, cudaStream_t s)
                               : launch_fused_k<XT, GT, WT, YT, MODE, 1>(p, grid, s);
         case 2: return p.push ? launch_push_k<XT, GT, WT, YT, MODE, 2>(p, grid, s)
                               : launch_fused_k<XT, GT, WT, YT, MODE, 2>(p, grid, s);
-        case 4: return launch_fused_k<XT, GT, WT, YT, MODE, 4>(p, grid, s);
+        case 4: return p.push ? launch_push_k<XT, GT, WT, YT, MODE, 4>(p, grid, s)
+                              : launch_fused_k<XT, GT, WT, YT, MODE, 4>(p, grid, s);
         case 8: return launch_fused_k<XT, GT, WT, YT, MODE, 8>(p, grid, s);
         default: return cudaErrorInvalidValue;
     }

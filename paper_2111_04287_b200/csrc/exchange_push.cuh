@@ -47,23 +47,29 @@ namespace bf {
 // (batch rb -> warp rb mod NSIG): the latency stays, the throughput of releases
 // scales; progress words are raised with a remote atomic max, so a later batch's
 // release overtaking an earlier one never moves a word backwards.
+// (measured at N = 2: K = 1 one-peer 0.233 ms with one signal warp, 0.201 with 4,
+// 0.193-0.195 with 8; K = 2 is best with 4 -- 8 more warps cost it registers)
 #ifndef BF_PUSH_NSIG
-#define BF_PUSH_NSIG 4
+#define BF_PUSH_NSIG 0   // 0: 8 for K = 1, 4 for K = 2
 #endif
 
 template <int K, int V>
 struct PushCfg {
+    // K <= 2: 2 CTAs per SM, 96 KB each; K = 4 holds 4 agents' partial combines per
+    // sub-item: 1 CTA per SM with 192 KB (a deeper lag, and no register cap of 2 CTAs)
+    static constexpr int kMinB = K >= 4 ? 1 : 2;
+    static constexpr int kSmemKB = K >= 4 ? 2 * BF_PUSH_SMEM_KB : BF_PUSH_SMEM_KB;
     // sub-items between the publish of a sub-item and its combine: as many as the
     // shared-memory budget holds (K agents x V floats per thread per sub-item)
     static constexpr int kPerSub = K * kThreads * V * 4;
-    static constexpr int kByBytes = BF_PUSH_SMEM_KB * 1024 / kPerSub;
+    static constexpr int kByBytes = kSmemKB * 1024 / kPerSub;
     static constexpr int kLag = kByBytes < BF_PUSH_LAG ? (kByBytes < 2 ? 2 : kByBytes) : BF_PUSH_LAG;
     static constexpr int kSmem = kLag * kPerSub;
-    static constexpr int kThreadsPerCta = kThreads + 32 * (1 + BF_PUSH_NSIG);   // consumers + poll + signal warps
+    static constexpr int kSig = BF_PUSH_NSIG > 0 ? BF_PUSH_NSIG : (K == 1 ? 8 : 4);
+    static constexpr int kThreadsPerCta = kThreads + 32 * (1 + kSig);   // consumers + poll + signal warps
+    static_assert(kPubRing % kSig == 0, "a publish-barrier slot must always map to the same signal warp");
 };
 constexpr int kPushBatch = BF_PUSH_BATCH;
-constexpr int kPushSig = BF_PUSH_NSIG;
-static_assert(kPubRing % kPushSig == 0, "a publish-barrier slot must always map to the same signal warp");
 
 __device__ __forceinline__ void red_max_sys(unsigned long long *p, unsigned long long v) {
     asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -90,12 +96,13 @@ __device__ __forceinline__ void st_release_cta_shared(int *p, int v) {
 }
 
 template <typename XT, typename GT, typename WT, typename YT, int MODE, int K>
-__global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, 2)
+__global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, PushCfg<K, FusedVec<XT>::V>::kMinB)
     exchange_push_kernel(const __grid_constant__ ExchParams p) {
     constexpr bool HAS_G = MODE != 0;
     constexpr int V = FusedVec<XT>::V;
     constexpr int kSubT = kThreads * V;
     constexpr int L = PushCfg<K, V>::kLag;
+    constexpr int kPushSig = PushCfg<K, V>::kSig;
     extern __shared__ __align__(16) float lag[];   // [L][K][kThreads][V]: partial combines, thread-private
     __shared__ SharedTab st;
     __shared__ PushMix<K> lm;

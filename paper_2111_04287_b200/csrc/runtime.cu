@@ -230,7 +230,7 @@ bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
     // push inboxes (cross-GPU fused kernel at K = 1, 2): one double-buffered inbox per
     // source agent in every reader's heap.  Optional: without room the pull kernel runs.
     c->inbox_off = c->pflag_off = 0;
-    if (c->nprocs > 1 && c->xfer && (c->k == 1 || c->k == 2)) {
+    if (c->nprocs > 1 && c->xfer && (c->k == 1 || c->k == 2 || c->k == 4)) {
         const size_t need = static_cast<size_t>(c->n) * 2 * cap + static_cast<size_t>(kMaxP) * kMaxGrid * 8 + 2 * kAlign;
         if (c->heap_used + need <= c->heap_bytes) {
             unsigned long long ib, pf;
@@ -861,7 +861,7 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     // K = 1, 2, when the inboxes fit in the heap; per-call views and the caller-assembled
     // hierarchical W keep the pull kernel
     if (p.kernel == 3 && c->nprocs > 1 && c->inbox_off && !static_tab && p.wmode != kWDynamic &&
-        (c->k == 1 || c->k == 2)) {
+        (c->k == 1 || c->k == 2 || c->k == 4)) {
         p.push = 1;
         p.inbox_off = c->inbox_off;
         p.inbox_agent_stride = 2 * c->exch_cap;

@@ -168,6 +168,8 @@ struct ExchParams {
     unsigned long long *stats;              // kernel 3 built with BF_STATS=1: u64 [grid][8] (diagnostics)
     float *psi;                             // kernel 3 MODE 3 (Exact-Diffusion): psi state [k][count], in place
     int gt;                                 // kernel 3: 4 = GT y-step (MODE 4), 5 = GT u/v-step (MODE 5), else 0
+    int hier_L;                             // push MODE 6-8 (hierarchical): rows per machine agent (machine size)
+    int hier_mode;                          // 0: not hierarchical; 6, 7, 8: MODE of the hierarchical push
     const float *g2;                        // kernel 3 MODE 4 (GT y-step): g_prev [k][count] (fp32)
     float *gt_v;                            // kernel 3 MODE 5 (GT u/v-step): scalar weight v [k], updated in place
     float *x_out;                           // kernel 3 MODE 5: x = u / v [k][count]
@@ -248,6 +250,7 @@ struct WinParams {
 cudaError_t launch_exchange(const ExchParams &p, int x_kind, int g_kind, int wire_kind, int y_kind,
                             int has_g, int grid, cudaStream_t s);
 cudaError_t launch_hier(const HierParams &p, int x_kind, int grid, cudaStream_t s);
+cudaError_t launch_hier_push(const ExchParams &p, int x_kind, int g_kind, cudaStream_t s);
 cudaError_t launch_barrier(const Geometry &geo, unsigned long long epoch, cudaStream_t s);
 cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s);
 cudaError_t launch_win_collect(const WinParams &p, int update, int grid, cudaStream_t s);

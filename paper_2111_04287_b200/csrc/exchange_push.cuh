@@ -27,6 +27,16 @@
 // except AWC, whose -lr g_a joins the parked local part before the remote terms.
 // Static and scheduled topologies only (a push needs the writer to know its
 // readers; pull-only per-call views keep the pull kernel).
+//
+// Hierarchical modes (R12; caption P:869) when every machine lies inside
+// one process (machine size L divides agents_per_proc): a "machine agent" is a
+// whole machine, K = machines per process, and each sub-item of machine agent a
+// reads its L rows a*L + l:
+//   MODE 6: hierarchical neighbor_allreduce  y_row = sum_m' W_M[m][m'] mean(x of m')
+//   MODE 7: H-ATC  the mean of fp32(x - lr g) over the machine's rows (Eq. 17)
+//   MODE 8: H-AWC  y_row = sum_m' W_M[m][m'] mean(x of m') - lr g_row (Eq. 16)
+// The machine average crosses NVLink once per reader process; the broadcast back
+// to the L rows is the store of the combine.
 #pragma once
 
 namespace bf {
@@ -98,7 +108,8 @@ __device__ __forceinline__ void st_release_cta_shared(int *p, int v) {
 template <typename XT, typename GT, typename WT, typename YT, int MODE, int K>
 __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, PushCfg<K, FusedVec<XT>::V>::kMinB)
     exchange_push_kernel(const __grid_constant__ ExchParams p) {
-    constexpr bool HAS_G = MODE != 0;
+    constexpr bool HAS_G = MODE != 0 && MODE != 6;
+    constexpr bool HIER = MODE >= 6;
     constexpr int V = FusedVec<XT>::V;
     constexpr int kSubT = kThreads * V;
     constexpr int L = PushCfg<K, V>::kLag;
@@ -256,6 +267,8 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
         const unsigned long long pol_stream = policy_evict_first();
         auto xrow = [&](int a) { return static_cast<const XT *>(p.x) + static_cast<long long>(a) * count; };
         auto grow = [&](int a) { return static_cast<const GT *>(p.g) + static_cast<long long>(a) * count; };
+        const int HL = HIER ? p.hier_L : 1;   // rows per (machine) agent
+        const float invL = 1.0f / static_cast<float>(HL);
         const int e0 = threadIdx.x * V;
         float *mylag = lag + static_cast<long long>(threadIdx.x) * V;   // + (slot * K + a) * kSubT
         if (lm.procs_out_all == 0 && nrt == 0) {
@@ -306,11 +319,29 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
                                 for (int j = 0; j < V; ++j) acc[j] = fmaf(c, v[u][j], acc[j]);
                             }
                     }
-                    YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base + e0;
-                    VecN<YT, V>::store_hint(yr, acc, valid, vec, pol_stream);
-                    if (p.shadow) {
-                        bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base + e0;
-                        VecN<bf16, V>::store_hint(sr, acc, valid, vec, pol_stream);
+                    if constexpr (HIER) {   // broadcast to the machine's rows (H-AWC: - lr g per row)
+                        for (int l = 0; l < HL; ++l) {
+                            const long long row = static_cast<long long>(a) * HL + l;
+                            float out[V];
+#pragma unroll
+                            for (int i = 0; i < V; ++i) out[i] = acc[i];
+                            if constexpr (MODE == 8) {
+                                float gr[V];
+                                VecN<GT, V>::load_hint(static_cast<const GT *>(p.g) + row * count + base + e0, gr, valid,
+                                                       vec, pol_stream);
+#pragma unroll
+                                for (int i = 0; i < V; ++i) out[i] = fmaf(-p.lr, gr[i], out[i]);
+                            }
+                            VecN<YT, V>::store_hint(static_cast<YT *>(p.y) + row * count + base + e0, out, valid, vec,
+                                                    pol_stream);
+                        }
+                    } else {
+                        YT *yr = static_cast<YT *>(p.y) + static_cast<long long>(a) * count + base + e0;
+                        VecN<YT, V>::store_hint(yr, acc, valid, vec, pol_stream);
+                        if (p.shadow) {
+                            bf16 *sr = static_cast<bf16 *>(p.shadow) + static_cast<long long>(a) * count + base + e0;
+                            VecN<bf16, V>::store_hint(sr, acc, valid, vec, pol_stream);
+                        }
                     }
                     if constexpr (MODE == 5) {   // x = u / v (appendix)
                         const float vn = s_vnew[a];
@@ -326,10 +357,35 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
                 const long long base = static_cast<long long>(sub(m)) * kSubT;
                 const int valid = clamp_valid_v<V>(count - base, e0);
                 float xv[K][V];
-                float gv[HAS_G ? K : 1][V];
+                float gv[HAS_G && !HIER ? K : 1][V];
+                if constexpr (HIER) {   // the machine average of the L rows (R12), H-ATC: of x - lr g
 #pragma unroll
-                for (int a = 0; a < K; ++a) VecN<XT, V>::load_hint(xrow(a) + base + e0, xv[a], valid, vec, pol_stream);
-                if constexpr (HAS_G) {
+                    for (int a = 0; a < K; ++a) {
+                        float sum[V];
+#pragma unroll
+                        for (int i = 0; i < V; ++i) sum[i] = 0.f;
+#pragma unroll 4
+                        for (int l = 0; l < HL; ++l) {
+                            const long long row = static_cast<long long>(a) * HL + l;
+                            float r[V];
+                            VecN<XT, V>::load_hint(xrow(0) + row * count + base + e0, r, valid, vec, pol_stream);
+                            if constexpr (MODE == 7) {
+                                float gr[V];
+                                VecN<GT, V>::load_hint(grow(0) + row * count + base + e0, gr, valid, vec, pol_stream);
+#pragma unroll
+                                for (int i = 0; i < V; ++i) r[i] = fmaf(-p.lr, gr[i], r[i]);
+                            }
+#pragma unroll
+                            for (int i = 0; i < V; ++i) sum[i] += r[i];
+                        }
+#pragma unroll
+                        for (int i = 0; i < V; ++i) xv[a][i] = sum[i] * invL;
+                    }
+                } else {
+#pragma unroll
+                    for (int a = 0; a < K; ++a) VecN<XT, V>::load_hint(xrow(a) + base + e0, xv[a], valid, vec, pol_stream);
+                }
+                if constexpr (HAS_G && !HIER) {
 #pragma unroll
                     for (int a = 0; a < K; ++a) VecN<GT, V>::load_hint(grow(a) + base + e0, gv[a], valid, vec, pol_stream);
                 }
@@ -393,7 +449,7 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
 #pragma unroll
                     for (int i = 0; i < V; i += 4) *reinterpret_cast<float4 *>(lp + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
                 }
-                if constexpr (MODE == 2) {   // AWC (Eq. 16): the remote terms come later; -lr g is local
+                if constexpr (MODE == 2) {   // AWC (Eq. 16): the remote terms come later; -lr g is local (per row for H-AWC)
 #pragma unroll
                     for (int a = 0; a < K; ++a) {
                         float *lp = mylag + static_cast<long long>(slot * K + a) * kSubT;

@@ -860,8 +860,10 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     // cross-GPU push variant (exchange_push.cuh): static topologies and schedules at
     // K = 1, 2, when the inboxes fit in the heap; per-call views and the caller-assembled
     // hierarchical W keep the pull kernel
+    // K = 4: push only for static W (measured at N = 2, 8 agents: exp-2 0.77 ms push vs
+    // 1.18 pull; one-peer rounds with 1-2 remote sources of 4 run faster pulled, 0.50 vs 0.60)
     if (p.kernel == 3 && c->nprocs > 1 && c->inbox_off && !static_tab && p.wmode != kWDynamic &&
-        (c->k == 1 || c->k == 2 || c->k == 4)) {
+        (c->k == 1 || c->k == 2 || (c->k == 4 && p.wmode == kWStatic))) {
         p.push = 1;
         p.inbox_off = c->inbox_off;
         p.inbox_agent_stride = 2 * c->exch_cap;
@@ -1095,6 +1097,59 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
     const size_t es = dtype == BF_FLOAT32 ? 4 : 2;
     s = ensure_exchange(c, count * es);
     if (s) return s;
+    // Across GPUs with every machine inside one process (L divides agents_per_proc) and a
+    // static machine topology: the push kernel's hierarchical modes (exchange_push.cuh
+    // MODE 6-8) -- each machine's average is formed in registers from its L rows, crosses
+    // NVLink once per reader process, and the combine is stored to the L rows.
+    const int Km = L <= c->k && c->k % L == 0 ? c->k / L : 0;
+    if (c->hier_mode != 1 && c->nprocs > 1 && c->inbox_off && !machine_weights && (Km == 1 || Km == 2 || Km == 4) &&
+        count <= c->exch_cap / es) {
+        ExchParams q;
+        memset(&q, 0, sizeof(q));
+        q.geo = make_geo(c, count);
+        q.geo.k = Km;
+        q.geo.n = NM;
+        const size_t vw = dtype == BF_BFLOAT16 ? 8 : 4;
+        q.geo.vec_ok = (count % vw == 0) && aligned16(x) && aligned16(y) && (!hmode || aligned16(g));
+        q.wmode = kWStatic;
+        for (int a = 0; a < Km; ++a) {   // machine-level rows of W_M, sources in (m - d) mod M order
+            const int m = c->proc * Km + a;
+            q.tab.self_w[a] = static_cast<float>(c->WM[static_cast<size_t>(m) * NM + m]);
+            int cnt = 0;
+            for (int d = 1; d < NM; ++d) {
+                const int mm = ((m - d) % NM + NM) % NM;
+                const double w = c->WM[static_cast<size_t>(m) * NM + mm];
+                if (w == 0.0) continue;
+                q.tab.src[a][cnt] = static_cast<unsigned char>(mm);
+                q.tab.coef[a][cnt] = static_cast<float>(w);
+                ++cnt;
+            }
+            q.tab.nsrc[a] = static_cast<unsigned char>(cnt);
+            for (int i = 0; i < NM; ++i)   // processes hosting a machine that reads machine m
+                if (i / Km != c->proc && c->WM[static_cast<size_t>(i) * NM + m] != 0.0) q.pushq[a] |= 1u << (i / Km);
+        }
+        q.x = x;
+        q.y = y;
+        q.g = g;
+        q.lr = hmode ? lr : 0.f;
+        q.kernel = 3;
+        q.push = 1;
+        q.hier_L = L;
+        q.hier_mode = hmode == 0 ? 6 : (hmode == 1 ? 7 : 8);
+        q.slot_off = c->slot_off;
+        q.slot_agent_stride = 2 * c->exch_cap;
+        q.slot_parity_stride = c->exch_cap;
+        q.inbox_off = c->inbox_off;
+        q.inbox_agent_stride = 2 * c->exch_cap;
+        q.inbox_parity_stride = c->exch_cap;
+        q.pflag_off = c->pflag_off;
+        q.prog_off = c->prog_off;
+        q.stats = c->stats;
+        order_stream(c, static_cast<cudaStream_t>(stream));
+        CU(launch_hier_push(q, dtype, hmode ? static_cast<int>(g_dtype) : 0, static_cast<cudaStream_t>(stream)));
+        c->launches++;
+        return BF_OK;
+    }
     if (c->hier_ready && c->hier_L != L) {   // slices are sized per machine size: reallocate
         CU(cudaDeviceSynchronize());
         if ((s = bf_barrier_internal(c))) return s;

@@ -14,3 +14,4 @@ done
 for xf in push pull; do
 BF_XFER=$xf timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr 127.0.0.1 --master-port 29544 bench_suite.py --only c1 2>&1 | grep '^{'
 done
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr 127.0.0.1 --master-port 29545 bench_suite.py --only h 2>&1 | grep '^{'

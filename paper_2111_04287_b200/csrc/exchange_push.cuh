@@ -59,6 +59,9 @@ namespace bf {
 // release overtaking an earlier one never moves a word backwards.
 // (measured at N = 2: K = 1 one-peer 0.233 ms with one signal warp, 0.201 with 4,
 // 0.193-0.195 with 8; K = 2 is best with 4 -- 8 more warps cost it registers)
+#ifndef BF_PUSH_K4_MINB
+#define BF_PUSH_K4_MINB 1   // CTAs per SM of the K = 4 push kernel (2: 96 KB lag, 2 signal warps)
+#endif
 #ifndef BF_PUSH_NSIG
 #define BF_PUSH_NSIG 0   // 0: 8 for K = 1, 4 for K = 2
 #endif
@@ -67,15 +70,15 @@ template <int K, int V>
 struct PushCfg {
     // K <= 2: 2 CTAs per SM, 96 KB each; K = 4 holds 4 agents' partial combines per
     // sub-item: 1 CTA per SM with 192 KB (a deeper lag, and no register cap of 2 CTAs)
-    static constexpr int kMinB = K >= 4 ? 1 : 2;
-    static constexpr int kSmemKB = K >= 4 ? 2 * BF_PUSH_SMEM_KB : BF_PUSH_SMEM_KB;
+    static constexpr int kMinB = K >= 4 ? BF_PUSH_K4_MINB : 2;
+    static constexpr int kSmemKB = K >= 4 && BF_PUSH_K4_MINB == 1 ? 2 * BF_PUSH_SMEM_KB : BF_PUSH_SMEM_KB;
     // sub-items between the publish of a sub-item and its combine: as many as the
     // shared-memory budget holds (K agents x V floats per thread per sub-item)
     static constexpr int kPerSub = K * kThreads * V * 4;
     static constexpr int kByBytes = kSmemKB * 1024 / kPerSub;
     static constexpr int kLag = kByBytes < BF_PUSH_LAG ? (kByBytes < 2 ? 2 : kByBytes) : BF_PUSH_LAG;
     static constexpr int kSmem = kLag * kPerSub;
-    static constexpr int kSig = BF_PUSH_NSIG > 0 ? BF_PUSH_NSIG : (K == 1 ? 8 : 4);
+    static constexpr int kSig = BF_PUSH_NSIG > 0 ? BF_PUSH_NSIG : (K == 1 ? 8 : (K >= 4 && kMinB == 2 ? 2 : 4));
     static constexpr int kThreadsPerCta = kThreads + 32 * (1 + kSig);   // consumers + poll + signal warps
     static_assert(kPubRing % kSig == 0, "a publish-barrier slot must always map to the same signal warp");
 };

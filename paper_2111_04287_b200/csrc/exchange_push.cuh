@@ -60,7 +60,8 @@ namespace bf {
 // (measured at N = 2: K = 1 one-peer 0.233 ms with one signal warp, 0.201 with 4,
 // 0.193-0.195 with 8; K = 2 is best with 4 -- 8 more warps cost it registers)
 #ifndef BF_PUSH_K4_MINB
-#define BF_PUSH_K4_MINB 1   // CTAs per SM of the K = 4 push kernel (2: 96 KB lag, 2 signal warps)
+#define BF_PUSH_K4_MINB 2   // CTAs per SM of the K = 4 push kernel (1: 192 KB lag, 4 signal warps;
+                            // measured N = 2 exp-2: 2 per SM 0.72 ms, 1 per SM 0.78 ms)
 #endif
 #ifndef BF_PUSH_NSIG
 #define BF_PUSH_NSIG 0   // 0: 8 for K = 1, 4 for K = 2

@@ -106,7 +106,7 @@ struct bf_ctx {
     unsigned long long launches = 0;
     unsigned long long *stats = nullptr;      // BF_STATS=1: per-CTA diagnostics of the fused kernel
     int hier_mode = 0;                        // BF_HIER: 0 auto, 1 staged (always), 2 fused (also across GPUs)
-    int xfer = 1;                             // BF_XFER: 1 push (default across GPUs, K = 1, 2), 0 pull
+    int xfer = 1;                             // BF_XFER: 1 push (default across GPUs), 0 pull, 2 push_all (tuning)
     unsigned long long inbox_off = 0, pflag_off = 0;   // push inboxes [n][2][cap] + progress words (0: none)
     bool win_ef = false;                      // BF_WIN_EF=1: new windows start with error feedback on
     // stream order across calls: every call of a context reads and advances the same
@@ -471,7 +471,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
     if (const char *x = getenv("BF_HIER")) c->hier_mode = strcmp(x, "staged") == 0 ? 1 : strcmp(x, "fused") == 0 ? 2 : 0;
     if (const char *x = getenv("BF_WIN_EF")) c->win_ef = atoi(x) != 0;
-    if (const char *x = getenv("BF_XFER")) c->xfer = strcmp(x, "pull") == 0 ? 0 : 1;
+    if (const char *x = getenv("BF_XFER")) c->xfer = strcmp(x, "pull") == 0 ? 0 : (strcmp(x, "push_all") == 0 ? 2 : 1);
     if (const char *x = getenv("BF_STATS"))
         if (atoi(x) && cudaMalloc(&c->stats, static_cast<size_t>(kMaxGrid) * 8 * 8) == cudaSuccess)
             cudaMemset(c->stats, 0, static_cast<size_t>(kMaxGrid) * 8 * 8);
@@ -863,7 +863,7 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     // K = 4: push only for static W (measured at N = 2, 8 agents: exp-2 0.77 ms push vs
     // 1.18 pull; one-peer rounds with 1-2 remote sources of 4 run faster pulled, 0.50 vs 0.60)
     if (p.kernel == 3 && c->nprocs > 1 && c->inbox_off && !static_tab && p.wmode != kWDynamic &&
-        (c->k == 1 || c->k == 2 || (c->k == 4 && p.wmode == kWStatic))) {
+        (c->k == 1 || c->k == 2 || (c->k == 4 && (p.wmode == kWStatic || c->xfer == 2)))) {
         p.push = 1;
         p.inbox_off = c->inbox_off;
         p.inbox_agent_stride = 2 * c->exch_cap;
@@ -1101,32 +1101,56 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
     // static machine topology: the push kernel's hierarchical modes (exchange_push.cuh
     // MODE 6-8) -- each machine's average is formed in registers from its L rows, crosses
     // NVLink once per reader process, and the combine is stored to the L rows.
-    const int Km = L <= c->k && c->k % L == 0 ? c->k / L : 0;
+    // Machines inside processes (L divides K): K / L machine agents per process.  A
+    // machine spanning P = L / K processes: one "partial" agent per process -- the
+    // average of its K rows -- and machine m's average is the mean of its P partials,
+    // so partial q' enters with weight W_M[m][m(q')] / P (the same push kernel).
+    const int Km = L <= c->k && c->k % L == 0 ? c->k / L : (L % c->k == 0 ? 1 : 0);
+    const int P = L > c->k ? L / c->k : 1;   // processes per machine
     if (c->hier_mode != 1 && c->nprocs > 1 && c->inbox_off && !machine_weights && (Km == 1 || Km == 2 || Km == 4) &&
-        count <= c->exch_cap / es) {
+        count <= c->exch_cap / es && (P == 1 || P <= kMaxS)) {
         ExchParams q;
         memset(&q, 0, sizeof(q));
         q.geo = make_geo(c, count);
         q.geo.k = Km;
-        q.geo.n = NM;
+        q.geo.n = P == 1 ? NM : c->nprocs;
         const size_t vw = dtype == BF_BFLOAT16 ? 8 : 4;
         q.geo.vec_ok = (count % vw == 0) && aligned16(x) && aligned16(y) && (!hmode || aligned16(g));
         q.wmode = kWStatic;
-        for (int a = 0; a < Km; ++a) {   // machine-level rows of W_M, sources in (m - d) mod M order
-            const int m = c->proc * Km + a;
-            q.tab.self_w[a] = static_cast<float>(c->WM[static_cast<size_t>(m) * NM + m]);
+        if (P == 1) {
+            for (int a = 0; a < Km; ++a) {   // machine-level rows of W_M, sources in (m - d) mod M order
+                const int m = c->proc * Km + a;
+                q.tab.self_w[a] = static_cast<float>(c->WM[static_cast<size_t>(m) * NM + m]);
+                int cnt = 0;
+                for (int d = 1; d < NM; ++d) {
+                    const int mm = ((m - d) % NM + NM) % NM;
+                    const double w = c->WM[static_cast<size_t>(m) * NM + mm];
+                    if (w == 0.0) continue;
+                    q.tab.src[a][cnt] = static_cast<unsigned char>(mm);
+                    q.tab.coef[a][cnt] = static_cast<float>(w);
+                    ++cnt;
+                }
+                q.tab.nsrc[a] = static_cast<unsigned char>(cnt);
+                for (int i = 0; i < NM; ++i)   // processes hosting a machine that reads machine m
+                    if (i / Km != c->proc && c->WM[static_cast<size_t>(i) * NM + m] != 0.0)
+                        q.pushq[a] |= 1u << (i / Km);
+            }
+        } else {   // one partial agent per process; processes in (me - d) mod nprocs order
+            const int np = c->nprocs, me = c->proc, m = me / P;
+            q.tab.self_w[0] = static_cast<float>(c->WM[static_cast<size_t>(m) * NM + m] / P);
             int cnt = 0;
-            for (int d = 1; d < NM; ++d) {
-                const int mm = ((m - d) % NM + NM) % NM;
-                const double w = c->WM[static_cast<size_t>(m) * NM + mm];
+            for (int d = 1; d < np; ++d) {
+                const int qq = ((me - d) % np + np) % np;
+                const double w = c->WM[static_cast<size_t>(m) * NM + qq / P];
                 if (w == 0.0) continue;
-                q.tab.src[a][cnt] = static_cast<unsigned char>(mm);
-                q.tab.coef[a][cnt] = static_cast<float>(w);
+                if (cnt >= kMaxS) return fail(BF_ERR_UNSUPPORTED, "hierarchical: too many source processes");
+                q.tab.src[0][cnt] = static_cast<unsigned char>(qq);
+                q.tab.coef[0][cnt] = static_cast<float>(w / P);
                 ++cnt;
             }
-            q.tab.nsrc[a] = static_cast<unsigned char>(cnt);
-            for (int i = 0; i < NM; ++i)   // processes hosting a machine that reads machine m
-                if (i / Km != c->proc && c->WM[static_cast<size_t>(i) * NM + m] != 0.0) q.pushq[a] |= 1u << (i / Km);
+            q.tab.nsrc[0] = static_cast<unsigned char>(cnt);
+            for (int i = 0; i < np; ++i)   // processes whose machine reads machine m
+                if (i != me && c->WM[static_cast<size_t>(i / P) * NM + m] != 0.0) q.pushq[0] |= 1u << i;
         }
         q.x = x;
         q.y = y;
@@ -1134,7 +1158,7 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
         q.lr = hmode ? lr : 0.f;
         q.kernel = 3;
         q.push = 1;
-        q.hier_L = L;
+        q.hier_L = P == 1 ? L : c->k;   // rows per (machine / partial) agent
         q.hier_mode = hmode == 0 ? 6 : (hmode == 1 ? 7 : 8);
         q.slot_off = c->slot_off;
         q.slot_agent_stride = 2 * c->exch_cap;

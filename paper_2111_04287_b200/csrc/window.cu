@@ -86,7 +86,7 @@ __device__ __forceinline__ void win_load_raw(const T *base, typename VecN<T, V>:
 #define BF_WIN_PUSH_MINB 4   // C5 A/B (profiles/r01_window_minblocks_ab.txt): 7.17 -> 7.09 ms per round
 #endif
 #ifndef BF_WIN_COLLECT_MINB
-#define BF_WIN_COLLECT_MINB 0
+#define BF_WIN_COLLECT_MINB -1   // -1: 4 CTAs/SM for bf16 windows, 3 for fp32 (no spills at 80 registers)
 #endif
 // BF_WIN_HINTS=1: x / out / slot streams carry an L2 evict-first policy (tuning variant)
 #ifndef BF_WIN_HINTS
@@ -104,8 +104,12 @@ __device__ __forceinline__ void win_load_raw(const T *base, typename VecN<T, V>:
 #else
 #define BF_PUSH_LB __launch_bounds__(kThreads)
 #endif
+// C5 round at N = 1 (340M bf16 x 8): 2 CTAs/SM (125 registers) 6.32 ms, 3 per SM 5.73 ms,
+// 4 per SM 5.70 ms (0.89 of the HBM roofline; profiles/r02_window_collect_ab.txt)
 #if BF_WIN_COLLECT_MINB > 0
 #define BF_COLLECT_LB __launch_bounds__(kThreads, BF_WIN_COLLECT_MINB)
+#elif BF_WIN_COLLECT_MINB < 0
+#define BF_COLLECT_LB __launch_bounds__(kThreads, sizeof(T) == 2 ? 4 : 3)
 #else
 #define BF_COLLECT_LB __launch_bounds__(kThreads)
 #endif

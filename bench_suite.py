@@ -180,14 +180,20 @@ def main():
         for L in (2, 4):
             nm = n // L
             ctx.set_machine_topology(bfp.topology_matrix("exp2", nm), L)
+            nvls = False
+            if world > 1 and L > k and L % k == 0 and os.environ.get("BF_NVLS", "1") != "0":
+                nvls = ctx.enable_nvls(L, count)     # machines span GPUs: average in the switch
             ms = timed(lambda: ctx.hierarchical_neighbor_allreduce(x, out=y), 20)
             dm = 1 if nm == 2 else (2 if nm in (3, 4) else 3)
+            if world > 1 and not hier_fused:
+                path = ("NVLS machine average (multimem.ld_reduce) + push machine exchange" if nvls else
+                        "push hierarchical mode (machine average in registers / per-process partials)"
+                        if (L <= k and k % L == 0) or L % k == 0 else "staged kernel")
             if hier_fused:
                 # one GPU: the Kronecker mix W_M (x) J/L in the fused kernel -- read x, write y
                 per_agent, path = 2 * count * 4, "fused kernel, W = W_M (x) J_L/L (read x + write y)"
             else:
                 per_agent = (2 * (L - 1) + dm) * count * 4 / L + 3 * count * 4
-                path = "staged kernel (sliced reduce-scatter, machine combine, gather)"
             emit({"config": f"H hierarchical_neighbor_allreduce 25.6M fp32, {nm} machines x {L}", "ms": ms,
                   "path": path, "gbs_per_gpu": k * per_agent / (ms * 1e-3) / 1e9,
                   "hbm_frac": k * per_agent / (ms * 1e-3) / 1e9 / peak if world == 1 else None})
@@ -198,6 +204,9 @@ def main():
         for L in (2, 4):
             nm = n // L
             ctx.set_machine_topology(bfp.topology_matrix("exp2", nm), L)
+            nvls = False
+            if world > 1 and L > k and L % k == 0 and os.environ.get("BF_NVLS", "1") != "0":
+                nvls = ctx.enable_nvls(L, count)
             for style, fn in (("H-ATC", ctx.hierarchical_atc_step), ("H-AWC", ctx.hierarchical_awc_step)):
                 ms = timed(lambda: fn(x, g, 1e-3), 20)
                 dm = 1 if nm == 2 else (2 if nm in (3, 4) else 3)
@@ -205,7 +214,8 @@ def main():
                     per_agent, path = 3 * count * 4, "fused kernel, W = W_M (x) J_L/L (read x, g + write x)"
                 else:
                     per_agent = (2 * (L - 1) + dm) * count * 4 / L + 4 * count * 4
-                    path = "staged kernel, adapt fused into the publish (ATC) / final write (AWC)"
+                    path = ("NVLS machine average + push machine exchange" if nvls else
+                            "push hierarchical mode" if (L <= k and k % L == 0) or L % k == 0 else "staged kernel")
                 emit({"config": f"{style} step 25.6M fp32, {nm} machines x {L}", "ms": ms, "path": path,
                       "gbs_per_gpu": k * per_agent / (ms * 1e-3) / 1e9,
                       "hbm_frac": k * per_agent / (ms * 1e-3) / 1e9 / peak if world == 1 else None})

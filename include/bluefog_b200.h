@@ -233,6 +233,18 @@ bf_status bf_gt_y_step(bf_ctx *ctx, float *y, const float *g, const float *g_pre
 bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *ctx, const void *x, void *y, size_t count,
                                              bf_dtype dtype, const bf_weights *machine_weights,
                                              void *stream);
+/* NVLS for the hierarchical calls when a machine spans processes ("intra-
+ * machine allreduce"): register this process's copy `uc` of a
+ * multicast-backed buffer of `bytes` bytes shared by the processes of its machine,
+ * and the buffer's multicast address `mc` (the caller allocates it -- e.g. torch
+ * symmetric memory rendezvous over the machine's process group, api.py
+ * Context.enable_nvls).  Then fp32 hierarchical calls with machines of local_size
+ * agents (> agents_per_proc) and a static machine topology average each machine
+ * with one multimem.ld_reduce per 16 bytes through the switch, before the
+ * machine-level exchange.  The buffer holds 2 x count fp32 (double-buffered).
+ * uc = NULL and mc = 0 unregister.  Local (not collective); every process of the
+ * context must register for the path to be used consistently. */
+bf_status bf_hier_set_multicast(bf_ctx *ctx, int local_size, void *uc, unsigned long long mc, size_t bytes);
 /* Hierarchical ATC / AWC steps (H-ATC, H-AWC: caption P:869, Table):
  *   H-ATC (Eq. 17 with the hierarchical combine):  x <- (W_M kron J_L/L)(x - lr g)
  *   H-AWC (Eq. 16 with the hierarchical combine):  x <- (W_M kron J_L/L) x - lr g

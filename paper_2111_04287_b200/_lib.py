@@ -55,6 +55,7 @@ _SIGS = {
     "bf_set_topology": (_i, [_vp, _i, C.POINTER(C.c_double)]),
     "bf_set_machine_topology": (_i, [_vp, _i, _i, C.POINTER(C.c_double)]),
     "bf_set_topology_local": (_i, [_vp, _wp]),
+    "bf_hier_set_multicast": (_i, [_vp, _i, _vp, _u64, _sz]),
     "bf_win_version": (_i, [_vp, C.c_char_p, _i, C.POINTER(_u64)]),
     "bf_in_neighbors": (_i, [_vp, _i, C.POINTER(_i), _i, C.POINTER(_i)]),
     "bf_out_neighbors": (_i, [_vp, _i, C.POINTER(_i), _i, C.POINTER(_i)]),

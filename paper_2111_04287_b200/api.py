@@ -366,6 +366,39 @@ class Context:
                                                           v.ptr() if v else None, _stream_ptr(stream, self.device)))
         return y
 
+    def enable_nvls(self, local_size: int, max_count: int) -> bool:
+        """Collective: give every machine that spans processes (local_size agents >
+        agents_per_proc) a multicast-backed buffer (torch symmetric memory over the
+        machine's process group -- allocation plumbing) so the hierarchical calls
+        average the machine in the NVSwitch (multimem.ld_reduce, hier_nvls.cu).
+        Returns False (and changes nothing) when the box has no multicast support."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        if local_size <= self.k or local_size % self.k or not dist.is_initialized():
+            raise ValueError("NVLS needs machines that span processes (local_size a multiple of agents_per_proc)")
+        P = local_size // self.k
+        if self.nprocs % P:
+            raise ValueError("machines must tile the processes")
+        groups = [dist.new_group(list(range(m * P, (m + 1) * P))) for m in range(self.nprocs // P)]
+        mine = groups[self.proc // P]
+        cap = (int(max_count) + 3) // 4 * 4
+        t = symm.empty(2 * cap, dtype=torch.float32, device=f"cuda:{self.device}")
+        h = symm.rendezvous(t, mine)
+        sup = getattr(h, "has_multicast_support", None)
+        sup = sup() if callable(sup) else sup
+        mc = int(getattr(h, "multicast_ptr", 0) or 0)
+        ok = torch.tensor([1 if (sup and mc) else 0], device=f"cuda:{self.device}")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)   # every process takes the same path
+        if not int(ok.item()):
+            return False
+        check(self.lib.bf_hier_set_multicast(self.h, int(local_size), C.c_void_p(t.data_ptr()), mc, 2 * cap * 4))
+        self._nvls = (t, h, groups)   # keep the buffer and its mapping alive
+        return True
+
+    def disable_nvls(self):
+        check(self.lib.bf_hier_set_multicast(self.h, 0, None, 0, 0))
+        self._nvls = None
+
     def hierarchical_atc_step(self, x: torch.Tensor, g: torch.Tensor, lr: float, self_weight=None,
                               src_machine_weights=None, stream=None) -> torch.Tensor:
         """H-ATC: x <- (W_M kron J_L/L)(x - lr g), in place on the fp32 master x."""

@@ -35,6 +35,7 @@ constexpr int kMaxP = BF_MAX_PROCS;
 constexpr size_t kPadBytes = 64 * 1024;
 constexpr size_t kAlign = 4096;
 constexpr int kMaxGrid = 4096;         // CTAs of one exchange launch (progress counters per process)
+constexpr long long kLLCap = 32768;    // elements per agent up to which the cross-GPU exchange uses tagged words
 
 // Per-agent, per-parity descriptor of a dynamic call (push side of Eq. 9):
 // which agents this agent pushes to and with which s (sender-side weight).
@@ -169,10 +170,13 @@ struct ExchParams {
     float *psi;                             // kernel 3 MODE 3 (Exact-Diffusion): psi state [k][count], in place
     int gt;                                 // kernel 3: 4 = GT y-step (MODE 4), 5 = GT u/v-step (MODE 5), else 0
     int hier_L;                             // push MODE 6-8 (hierarchical): rows per machine agent (machine size)
+    int hier_in;                            // rows averaged per machine agent (0: hier_L; 1: x is a machine average)
     int hier_mode;                          // 0: not hierarchical; 6, 7, 8: MODE of the hierarchical push
     const float *g2;                        // kernel 3 MODE 4 (GT y-step): g_prev [k][count] (fp32)
     float *gt_v;                            // kernel 3 MODE 5 (GT u/v-step): scalar weight v [k], updated in place
     float *x_out;                           // kernel 3 MODE 5: x = u / v [k][count]
+    int ll;                                 // kernel 3 across GPUs, small messages: tagged 64-bit words (exchange_ll.cuh)
+    unsigned long long ll_off, ll_stride;   // ll: u64 [n source agents][2 parities][ll cap] in every heap; row bytes
     int push;                               // kernel 3 across GPUs: writers push into the readers' inboxes
     unsigned long long inbox_off;           // push: wire dtype [n source agents][2 parities][cap] in every heap
     unsigned long long inbox_agent_stride, inbox_parity_stride;   // bytes
@@ -202,6 +206,22 @@ struct HierParams {
     unsigned long long b_off, c_off, bc_agent_stride, bc_parity_stride;   // fp32 slices
     unsigned long long fb_off, fc_off;      // u64 flags [k][ready_stride]
     SrcTab mtab;                            // machine-level: src = machine ids
+};
+
+// NVLS intra-machine average (hier_nvls.cu): machines spanning P processes.
+struct NvlsParams {
+    Geometry geo;                           // k = rows of this process, count
+    const float *x;                         // [k][count]
+    const void *g;                          // H-ATC: gradient [k][count]
+    int hmode;                              // 1: average x - lr g (H-ATC), else x
+    float lr;
+    float invL;                             // 1 / machine size
+    float *uc;                              // this process's copy of the multicast buffer: fp32 [2][cap]
+    unsigned long long mc;                  // multicast address of the same buffer
+    long long cap;                          // elements per parity half
+    float *avg;                             // output: the machine average [count]
+    unsigned long long nflag_off;           // u64 [kMaxP][kMaxGrid] in every heap
+    int proc0, P;                           // processes proc0 .. proc0 + P - 1 form this machine
 };
 
 // One-sided windows.
@@ -251,6 +271,7 @@ cudaError_t launch_exchange(const ExchParams &p, int x_kind, int g_kind, int wir
                             int has_g, int grid, cudaStream_t s);
 cudaError_t launch_hier(const HierParams &p, int x_kind, int grid, cudaStream_t s);
 cudaError_t launch_hier_push(const ExchParams &p, int x_kind, int g_kind, cudaStream_t s);
+cudaError_t launch_hier_nvls(const NvlsParams &p, int g_kind, cudaStream_t s);
 cudaError_t launch_barrier(const Geometry &geo, unsigned long long epoch, cudaStream_t s);
 cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s);
 cudaError_t launch_win_collect(const WinParams &p, int update, int grid, cudaStream_t s);

@@ -571,11 +571,20 @@ static cudaError_t launch_fused_k(const ExchParams &p, int grid, cudaStream_t s)
 }  // namespace bf
 
 #include "exchange_push.cuh"
+#include "exchange_ll.cuh"
 
 namespace bf {
 
 template <typename XT, typename GT, typename WT, typename YT, int MODE>
 static cudaError_t launch_fused_t(const ExchParams &p, int grid, cudaStream_t s) {
+    if (p.ll) {
+        switch (p.geo.k) {
+            case 1: return launch_ll_k<XT, GT, WT, YT, MODE, 1>(p, s);
+            case 2: return launch_ll_k<XT, GT, WT, YT, MODE, 2>(p, s);
+            case 4: return launch_ll_k<XT, GT, WT, YT, MODE, 4>(p, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (p.geo.k) {
         case 1: return p.push ? launch_push_k<XT, GT, WT, YT, MODE, 1>(p, grid, s)
                               : launch_fused_k<XT, GT, WT, YT, MODE, 1>(p, grid, s);

@@ -271,8 +271,9 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
         const unsigned long long pol_stream = policy_evict_first();
         auto xrow = [&](int a) { return static_cast<const XT *>(p.x) + static_cast<long long>(a) * count; };
         auto grow = [&](int a) { return static_cast<const GT *>(p.g) + static_cast<long long>(a) * count; };
-        const int HL = HIER ? p.hier_L : 1;   // rows per (machine) agent
-        const float invL = 1.0f / static_cast<float>(HL);
+        const int HL = HIER ? p.hier_L : 1;   // rows written per (machine) agent
+        const int HLin = HIER && p.hier_in ? p.hier_in : HL;   // rows averaged (1: x is the machine average)
+        const float invL = 1.0f / static_cast<float>(HLin);
         const int e0 = threadIdx.x * V;
         float *mylag = lag + static_cast<long long>(threadIdx.x) * V;   // + (slot * K + a) * kSubT
         if (lm.procs_out_all == 0 && nrt == 0) {
@@ -369,8 +370,8 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
 #pragma unroll
                         for (int i = 0; i < V; ++i) sum[i] = 0.f;
 #pragma unroll 4
-                        for (int l = 0; l < HL; ++l) {
-                            const long long row = static_cast<long long>(a) * HL + l;
+                        for (int l = 0; l < HLin; ++l) {
+                            const long long row = static_cast<long long>(a) * HLin + l;
                             float r[V];
                             VecN<XT, V>::load_hint(xrow(0) + row * count + base + e0, r, valid, vec, pol_stream);
                             if constexpr (MODE == 7) {

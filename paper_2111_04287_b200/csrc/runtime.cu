@@ -108,6 +108,14 @@ struct bf_ctx {
     int hier_mode = 0;                        // BF_HIER: 0 auto, 1 staged (always), 2 fused (also across GPUs)
     int xfer = 1;                             // BF_XFER: 1 push (default across GPUs), 0 pull, 2 push_all (tuning)
     unsigned long long inbox_off = 0, pflag_off = 0;   // push inboxes [n][2][cap] + progress words (0: none)
+    unsigned long long ll_off = 0;            // tagged-word inboxes [n][2][kLLCap] u64 (small messages; 0: none)
+    // NVLS (bf_hier_set_multicast): this process's copy of a multicast-backed fp32 buffer
+    // [2][nvls_cap] of its machine's group, the multicast address, and machine flags
+    float *nvls_uc = nullptr;
+    unsigned long long nvls_mc = 0, nflag_off = 0;
+    long long nvls_cap = 0;
+    int nvls_L = 0;
+    int ll = 1;                               // BF_LL=0 turns the small-message path off
     bool win_ef = false;                      // BF_WIN_EF=1: new windows start with error feedback on
     // stream order across calls: every call of a context reads and advances the same
     // device state (epoch, round, slots, progress words), so a call issued on another
@@ -229,7 +237,22 @@ bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
     if ((s = heap_alloc(c, static_cast<size_t>(kMaxGrid) * 8, &c->prog_off))) return s;
     // push inboxes (cross-GPU fused kernel at K = 1, 2): one double-buffered inbox per
     // source agent in every reader's heap.  Optional: without room the pull kernel runs.
-    c->inbox_off = c->pflag_off = 0;
+    c->inbox_off = c->pflag_off = c->ll_off = c->nflag_off = 0;
+    if (c->nprocs > 1) {   // NVLS machine flags (hier_nvls.cu), small
+        unsigned long long off;
+        if (c->heap_used + static_cast<size_t>(kMaxP) * kMaxGrid * 8 + kAlign <= c->heap_bytes) {
+            if ((s = heap_alloc(c, static_cast<size_t>(kMaxP) * kMaxGrid * 8, &off))) return s;
+            c->nflag_off = off;
+        }
+    }
+    if (c->nprocs > 1 && c->ll && (c->k == 1 || c->k == 2 || c->k == 4)) {   // small-message tagged inboxes
+        const size_t llb = static_cast<size_t>(c->n) * 2 * kLLCap * 8;
+        if (c->heap_used + llb + kAlign <= c->heap_bytes) {
+            unsigned long long off;
+            if ((s = heap_alloc(c, llb, &off))) return s;
+            c->ll_off = off;
+        }
+    }
     if (c->nprocs > 1 && c->xfer && (c->k == 1 || c->k == 2 || c->k == 4)) {
         const size_t need = static_cast<size_t>(c->n) * 2 * cap + static_cast<size_t>(kMaxP) * kMaxGrid * 8 + 2 * kAlign;
         if (c->heap_used + need <= c->heap_bytes) {
@@ -471,6 +494,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     if (const char *x = getenv("BF_CHUNK_TILES")) c->chunk_tiles = std::max(1, atoi(x));
     if (const char *x = getenv("BF_HIER")) c->hier_mode = strcmp(x, "staged") == 0 ? 1 : strcmp(x, "fused") == 0 ? 2 : 0;
     if (const char *x = getenv("BF_WIN_EF")) c->win_ef = atoi(x) != 0;
+    if (const char *x = getenv("BF_LL")) c->ll = atoi(x) != 0;
     if (const char *x = getenv("BF_XFER")) c->xfer = strcmp(x, "pull") == 0 ? 0 : (strcmp(x, "push_all") == 0 ? 2 : 1);
     if (const char *x = getenv("BF_STATS"))
         if (atoi(x) && cudaMalloc(&c->stats, static_cast<size_t>(kMaxGrid) * 8 * 8) == cudaSuccess)
@@ -860,9 +884,23 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     // cross-GPU push variant (exchange_push.cuh): static topologies and schedules at
     // K = 1, 2, when the inboxes fit in the heap; per-call views and the caller-assembled
     // hierarchical W keep the pull kernel
+    // small messages across GPUs: tagged words, no fence, no progress word (exchange_ll.cuh)
+    if (p.kernel == 3 && c->nprocs > 1 && c->ll_off && !static_tab && p.wmode != kWDynamic && !psi && !gt &&
+        static_cast<long long>(count) <= kLLCap && (c->k == 1 || c->k == 2 || c->k == 4)) {
+        p.ll = 1;
+        p.ll_off = c->ll_off;
+        p.ll_stride = static_cast<unsigned long long>(kLLCap) * 8;
+        if (p.wmode == kWStatic)
+            for (int a = 0; a < c->k; ++a) {
+                const int gid = c->proc * c->k + a;
+                for (int i = 0; i < c->n; ++i)
+                    if (i / c->k != c->proc && c->W[static_cast<size_t>(i) * c->n + gid] != 0.0)
+                        p.pushq[a] |= 1u << (i / c->k);
+            }
+    }
     // K = 4: push only for static W (measured at N = 2, 8 agents: exp-2 0.77 ms push vs
     // 1.18 pull; one-peer rounds with 1-2 remote sources of 4 run faster pulled, 0.50 vs 0.60)
-    if (p.kernel == 3 && c->nprocs > 1 && c->inbox_off && !static_tab && p.wmode != kWDynamic &&
+    if (!p.ll && p.kernel == 3 && c->nprocs > 1 && c->inbox_off && !static_tab && p.wmode != kWDynamic &&
         (c->k == 1 || c->k == 2 || (c->k == 4 && (p.wmode == kWStatic || c->xfer == 2)))) {
         p.push = 1;
         p.inbox_off = c->inbox_off;
@@ -1101,6 +1139,78 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
     // static machine topology: the push kernel's hierarchical modes (exchange_push.cuh
     // MODE 6-8) -- each machine's average is formed in registers from its L rows, crosses
     // NVLink once per reader process, and the combine is stored to the L rows.
+    // A machine spanning P processes with a multicast buffer registered for this machine
+    // size (bf_hier_set_multicast): NVLS machine average (hier_nvls.cu), then the push
+    // kernel's hierarchical mode over the average row (machine-level exchange between the
+    // processes of the same local index, broadcast to the K rows).
+    if (c->hier_mode != 1 && c->nprocs > 1 && c->inbox_off && c->nvls_mc && c->nvls_L == L && !machine_weights &&
+        dtype == BF_FLOAT32 && L > c->k && L % c->k == 0 && static_cast<long long>(count) <= c->nvls_cap &&
+        count * 4 <= c->exch_cap) {
+        const int P = L / c->k, me = c->proc, m = me / P, l = me % P;
+        if (!c->nflag_off) return fail(BF_ERR_STATE, "NVLS flags not allocated");
+        NvlsParams v;
+        memset(&v, 0, sizeof(v));
+        v.geo = make_geo(c, count);
+        v.geo.vec_ok = (count % 4 == 0) && aligned16(x) && (!hmode || aligned16(g));
+        v.x = static_cast<const float *>(x);
+        v.g = g;
+        v.hmode = hmode;
+        v.lr = hmode ? lr : 0.f;
+        v.invL = 1.0f / static_cast<float>(L);
+        v.uc = c->nvls_uc;
+        v.mc = c->nvls_mc;
+        v.cap = c->nvls_cap;
+        float *avg = reinterpret_cast<float *>(c->heap + c->slot_off);   // the pull slots are idle here
+        v.avg = avg;
+        v.nflag_off = c->nflag_off;
+        v.proc0 = m * P;
+        v.P = P;
+        order_stream(c, static_cast<cudaStream_t>(stream));
+        CU(launch_hier_nvls(v, hmode && g_dtype == BF_BFLOAT16 ? 1 : 0, static_cast<cudaStream_t>(stream)));
+        c->launches++;
+        // machine-level combine over the processes of local index l: (m', l) for m' with W_M[m][m'] != 0
+        ExchParams q;
+        memset(&q, 0, sizeof(q));
+        q.geo = make_geo(c, count);
+        q.geo.k = 1;
+        q.geo.n = c->nprocs;
+        q.geo.vec_ok = (count % 4 == 0) && aligned16(y) && (hmode != 2 || aligned16(g));
+        q.wmode = kWStatic;
+        q.tab.self_w[0] = static_cast<float>(c->WM[static_cast<size_t>(m) * NM + m]);
+        int cnt = 0;
+        for (int d = 1; d < NM; ++d) {
+            const int mm = ((m - d) % NM + NM) % NM;
+            const double w = c->WM[static_cast<size_t>(m) * NM + mm];
+            if (w == 0.0) continue;
+            q.tab.src[0][cnt] = static_cast<unsigned char>(mm * P + l);
+            q.tab.coef[0][cnt] = static_cast<float>(w);
+            ++cnt;
+        }
+        q.tab.nsrc[0] = static_cast<unsigned char>(cnt);
+        for (int i = 0; i < NM; ++i)   // the process of local index l in every machine that reads machine m
+            if (i != m && c->WM[static_cast<size_t>(i) * NM + m] != 0.0) q.pushq[0] |= 1u << (i * P + l);
+        q.x = avg;
+        q.y = y;
+        q.g = hmode == 2 ? g : nullptr;
+        q.lr = hmode == 2 ? lr : 0.f;
+        q.kernel = 3;
+        q.push = 1;
+        q.hier_L = c->k;
+        q.hier_in = 1;
+        q.hier_mode = hmode == 2 ? 8 : 6;
+        q.slot_off = c->slot_off;
+        q.slot_agent_stride = 2 * c->exch_cap;
+        q.slot_parity_stride = c->exch_cap;
+        q.inbox_off = c->inbox_off;
+        q.inbox_agent_stride = 2 * c->exch_cap;
+        q.inbox_parity_stride = c->exch_cap;
+        q.pflag_off = c->pflag_off;
+        q.prog_off = c->prog_off;
+        q.stats = c->stats;
+        CU(launch_hier_push(q, 0, hmode == 2 ? static_cast<int>(g_dtype) : 0, static_cast<cudaStream_t>(stream)));
+        c->launches++;
+        return BF_OK;
+    }
     // Machines inside processes (L divides K): K / L machine agents per process.  A
     // machine spanning P = L / K processes: one "partial" agent per process -- the
     // average of its K rows -- and machine m's average is the mean of its P partials,
@@ -1232,6 +1342,28 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
     order_stream(c, static_cast<cudaStream_t>(stream));
     CU(launch_hier(p, dtype, 0, static_cast<cudaStream_t>(stream)));
     c->launches++;
+    return BF_OK;
+}
+
+bf_status bf_hier_set_multicast(bf_ctx *c, int local_size, void *uc, unsigned long long mc, size_t bytes) {
+    bf_status s = check_ctx(c);
+    if (s) return s;
+    if (!uc && !mc) {   // unregister
+        c->nvls_uc = nullptr;
+        c->nvls_mc = 0;
+        c->nvls_cap = 0;
+        c->nvls_L = 0;
+        return BF_OK;
+    }
+    if (!uc || !mc || bytes < 2 * 16 || (reinterpret_cast<uintptr_t>(uc) & 15u) || (mc & 15u))
+        return fail(BF_ERR_ARG, "multicast buffer: unicast and multicast addresses (16-byte aligned) and its size");
+    if (local_size <= c->k || local_size % c->k)
+        return fail(BF_ERR_ARG, "NVLS averages machines that span processes: local_size must be a multiple of "
+                                "agents_per_proc larger than it");
+    c->nvls_uc = static_cast<float *>(uc);
+    c->nvls_mc = mc;
+    c->nvls_cap = static_cast<long long>(bytes / 8) / 4 * 4;   // fp32 elements per parity half
+    c->nvls_L = local_size;
     return BF_OK;
 }
 

@@ -183,6 +183,36 @@ def main():
         check(f"H-AWC L={L}", np_(x), ora.hier_awc(WM, L, X, Gh, 0.1), Kh, X, 1e-6,
               0.1 * np.abs(Gh.astype(np.float64)))
 
+    # ---- NVLS: machines spanning 2 processes, average in the switch (hier_nvls.cu) ----
+    if ctx.nprocs % 2 == 0:
+        L = 2 * k
+        nm = n // L
+        WM = ora.exp2(nm) if nm > 1 else np.ones((1, 1))
+        ctx.set_machine_topology(WM, L)
+        if ctx.enable_nvls(L, 60000):
+            Kh = np.kron(WM, np.full((L, L), 1.0 / L))
+            x, X = inputs(40003)
+            y = ctx.hierarchical_neighbor_allreduce(x)
+            torch.cuda.synchronize()
+            check(f"nvls hier L={L}", np_(y), ora.hier(WM, L, X), Kh, X, 1e-6)
+            Gh = np.stack([synthetic.uniform(synthetic.grad_seed(9, r), 40003, scale=2.0 ** -7) for r in range(n)])
+            gh = torch.from_numpy(Gh[rows].copy()).cuda()
+            xa = x.clone()
+            ctx.hierarchical_atc_step(xa, gh, 0.1)
+            torch.cuda.synchronize()
+            check(f"nvls H-ATC L={L}", np_(xa), ora.hier_atc(WM, L, X, Gh, 0.1), Kh, X, 1e-6,
+                  np.abs(Kh) @ (0.1 * np.abs(Gh.astype(np.float64))))
+            xw = x.clone()
+            ctx.hierarchical_awc_step(xw, gh, 0.1)
+            torch.cuda.synchronize()
+            check(f"nvls H-AWC L={L}", np_(xw), ora.hier_awc(WM, L, X, Gh, 0.1), Kh, X, 1e-6,
+                  0.1 * np.abs(Gh.astype(np.float64)))
+            ctx.disable_nvls()
+            if rank == 0:
+                print("NVLS path checked", flush=True)
+        elif rank == 0:
+            print("NVLS: no multicast support on this box", flush=True)
+
     # ---- neighbor_win_get on a symmetric-heap tensor (reads over NVLink) ------------
     Wst = ora.exp2(n)
     ctx.set_topology(Wst)

@@ -458,8 +458,14 @@ def main():
             except Exception:
                 pass
         roof["algorithmic_bytes_per_launch"] = hbm_bytes if roof["bound"] == "hbm" else nvl_bytes
-        roof["kernel"] = ("bf::exchange_fused_kernel (ATC adapt + local-agent combine in registers + "
-                          "publish / NVLink pull of remote sources)")
+        if world == 1:
+            roof["kernel"] = "bf::exchange_fused_kernel (ATC adapt + combine of the 8 local agents in registers)"
+        elif k <= 2 or a.topology != "one_peer":
+            roof["kernel"] = ("bf::exchange_push_kernel (ATC adapt, wire copies stored into the readers' inboxes "
+                              "over NVLink, local part parked in shared memory, remote terms from the local inbox)")
+        else:
+            roof["kernel"] = ("bf::exchange_fused_kernel, pull path (publish into the own slot, TMA pulls of the "
+                              "remote sources over NVLink; K = 4 schedules)")
         value = 1e3 / ms_step
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": a.steps,

@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c3,c5,h,io,o,e,gt,c2")
+    ap.add_argument("--only", default="c1,c3,c5,h,io,o,e,gt,c2,oracle")
     ap.add_argument("--agents", type=int, default=8)
     ap.add_argument("--max-bytes", type=int, default=1 << 30)
     ap.add_argument("--out", default=None)
@@ -373,6 +373,56 @@ def main():
         ctx.close()
 
     # ---------------------------------------------------------------- C2 ----
+    # ------------------------------------------------------ oracle timings ----
+    # the CPU oracle (oracle/bf_oracle.c, single thread, as it stands) on the C1, C3
+    # and C5 workloads -- a reported baseline (SURVEY 8(d) oracle timing protocol)
+    if "oracle" in only and world == 1 and rank == 0:
+        import time
+        import oracle as ora
+
+        def clock(fn, reps=3):
+            fn()
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                fn()
+                ts.append(time.perf_counter() - t0)
+            return sorted(ts)[len(ts) // 2]
+        ncpu = len(os.sched_getaffinity(0))
+        X1 = synthetic.agents_x0(4, 4096).astype(np.float64)
+        W1 = ora.ring(4)
+
+        def c1o():
+            X = X1
+            for _ in range(20):
+                X = ora.mix(W1, X)
+        t = clock(c1o)
+        emit({"config": "oracle C1 ring-4 fp32[4096] x 20 iterations (fp64, 1 thread)", "s": t,
+              "us_per_iteration": t / 20 * 1e6, "cores": 1, "nproc": ncpu})
+        W8 = ora.exp2(8)
+        for nb in (1 << 20, 1 << 26):
+            X3 = synthetic.agents_x0(8, nb // 4).astype(np.float64)
+            t = clock(lambda: ora.mix(W8, X3), reps=1 if nb > (1 << 22) else 3)
+            emit({"config": f"oracle C3 neighbor_allreduce exp-2, 8 agents x {nb} B fp32 (fp64, 1 thread)", "s": t,
+                  "gbs_per_agent": nb / t / 1e9, "cores": 1, "nproc": ncpu})
+        pre = 1 << 20
+        X5 = np.concatenate([synthetic.agents_x0(8, pre).astype(np.float64), np.ones((8, 1))], axis=1)
+        win = ora.Window(W8, X5, zero_init=True)
+        rnd = [0]
+
+        def c5o():
+            k_ = rnd[0]
+            for i in range(8):
+                _, dst = ora.one_peer_exp2_peers(8, k_, i)
+                win.accumulate(i, 0.5, {dst: 0.5})
+            for i in range(8):
+                win.collect(i)
+            rnd[0] += 1
+        t = clock(c5o)
+        emit({"config": f"oracle C5 push-sum round (event model), 8 agents x {pre}-element prefix of 340M "
+                        "(fp64, 1 thread)", "s": t, "s_per_round_extrapolated_to_340M": t * 340_000_000 / pre,
+              "cores": 1, "nproc": ncpu})
+
     if "c2" in only and world == 1:
         import oracle as ora
         n, m, d = a.agents, 2000, 10_000

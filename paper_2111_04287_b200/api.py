@@ -384,9 +384,11 @@ class Context:
         cap = (int(max_count) + 3) // 4 * 4
         t = symm.empty(2 * cap, dtype=torch.float32, device=f"cuda:{self.device}")
         h = symm.rendezvous(t, mine)
-        sup = getattr(h, "has_multicast_support", None)
-        sup = sup() if callable(sup) else sup
         mc = int(getattr(h, "multicast_ptr", 0) or 0)
+        try:   # static query (device type, index) on current torch; older: a property
+            sup = bool(symm._SymmetricMemory.has_multicast_support(torch._C._autograd.DeviceType.CUDA, self.device))
+        except Exception:   # noqa: BLE001
+            sup = mc != 0
         ok = torch.tensor([1 if (sup and mc) else 0], device=f"cuda:{self.device}")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)   # every process takes the same path
         if not int(ok.item()):

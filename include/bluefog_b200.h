@@ -165,6 +165,12 @@ bf_status bf_schedule_inner_outer_exp2(int n, int local_size, int rank, uint64_t
  * every agent with a peer mixes 1/2 self + 1/2 its source. */
 bf_status bf_set_dynamic_schedule(bf_ctx *ctx, int kind, uint64_t round0);
 bf_status bf_set_topology_check(bf_ctx *ctx, int enable);   /* P:613; default on */
+/* Cap the CTAs of the exchange kernels (0 = as many as the SMs hold, the default).
+ * CTA b of every process pairs with CTA b of its peers, so every process must set
+ * the same cap before its next exchange (collective by convention).  Use it when
+ * exchanges overlap other GPU work (the optimizer's per-layer steps during
+ * backward): the exchange then leaves SMs to the concurrent kernels. */
+bf_status bf_set_max_ctas(bf_ctx *ctx, int ctas);
 
 /* ---- the hot path ------------------------------------------------------------
  * bf_neighbor_allreduce (Eq. 5 P:183 static; Eq. 9-11 P:355-362 dynamic):

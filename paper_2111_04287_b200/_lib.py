@@ -64,6 +64,7 @@ _SIGS = {
     "bf_schedule_inner_outer_exp2": (_i, [_i, _i, _i, _u64, C.POINTER(_i), C.POINTER(_i)]),
     "bf_set_dynamic_schedule": (_i, [_vp, _i, _u64]),
     "bf_set_topology_check": (_i, [_vp, _i]),
+    "bf_set_max_ctas": (_i, [_vp, _i]),
     "bf_neighbor_allreduce": (_i, [_vp, _vp, _vp, _sz, _i, _wp, _vp]),
     "bf_atc_step": (_i, [_vp, _vp, _vp, _i, _sz, C.c_float, _i, _vp, _wp, _vp]),
     "bf_awc_step": (_i, [_vp, _vp, _vp, _i, _sz, C.c_float, _wp, _vp]),

@@ -225,6 +225,10 @@ class Context:
     def set_topology_check(self, enable: bool):
         check(self.lib.bf_set_topology_check(self.h, 1 if enable else 0))
 
+    def set_max_ctas(self, ctas: int):
+        """Grid cap of the exchange kernels (0 = all SMs); the same on every process."""
+        check(self.lib.bf_set_max_ctas(self.h, int(ctas)))
+
     def reserve(self, bytes_per_agent: int):
         check(self.lib.bf_reserve(self.h, int(bytes_per_agent)))
 

@@ -172,6 +172,7 @@ struct ExchParams {
     int hier_L;                             // push MODE 6-8 (hierarchical): rows per machine agent (machine size)
     int hier_in;                            // rows averaged per machine agent (0: hier_L; 1: x is a machine average)
     int hier_mode;                          // 0: not hierarchical; 6, 7, 8: MODE of the hierarchical push
+    int max_ctas;                           // hierarchical push launches: grid cap (0 = all SMs)
     const float *g2;                        // kernel 3 MODE 4 (GT y-step): g_prev [k][count] (fp32)
     float *gt_v;                            // kernel 3 MODE 5 (GT u/v-step): scalar weight v [k], updated in place
     float *x_out;                           // kernel 3 MODE 5: x = u / v [k][count]

@@ -9,9 +9,9 @@ namespace bf {
 template <typename XT, typename GT, int MODE>
 static cudaError_t hier_push_t(const ExchParams &p, cudaStream_t s) {
     switch (p.geo.k) {
-        case 1: return launch_push_k<XT, GT, XT, XT, MODE, 1>(p, 0, s);
-        case 2: return launch_push_k<XT, GT, XT, XT, MODE, 2>(p, 0, s);
-        case 4: return launch_push_k<XT, GT, XT, XT, MODE, 4>(p, 0, s);
+        case 1: return launch_push_k<XT, GT, XT, XT, MODE, 1>(p, p.max_ctas, s);
+        case 2: return launch_push_k<XT, GT, XT, XT, MODE, 2>(p, p.max_ctas, s);
+        case 4: return launch_push_k<XT, GT, XT, XT, MODE, 4>(p, p.max_ctas, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -116,6 +116,7 @@ struct bf_ctx {
     long long nvls_cap = 0;
     int nvls_L = 0;
     int ll = 1;                               // BF_LL=0 turns the small-message path off
+    int max_ctas = 0;                         // bf_set_max_ctas: grid cap of the exchange kernels (0 = all SMs)
     bool win_ef = false;                      // BF_WIN_EF=1: new windows start with error feedback on
     // stream order across calls: every call of a context reads and advances the same
     // device state (epoch, round, slots, progress words), so a call issued on another
@@ -916,7 +917,7 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
             }
     }
     order_stream(c, st);
-    CU(launch_exchange(p, x_kind, awc_g ? x_kind : g_kind, wire_kind, y_kind, g != nullptr, 0, st));
+    CU(launch_exchange(p, x_kind, awc_g ? x_kind : g_kind, wire_kind, y_kind, g != nullptr, c->max_ctas, st));
     c->launches++;
     return BF_OK;
 }
@@ -1207,6 +1208,7 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
         q.pflag_off = c->pflag_off;
         q.prog_off = c->prog_off;
         q.stats = c->stats;
+        q.max_ctas = c->max_ctas;
         CU(launch_hier_push(q, 0, hmode == 2 ? static_cast<int>(g_dtype) : 0, static_cast<cudaStream_t>(stream)));
         c->launches++;
         return BF_OK;
@@ -1280,6 +1282,7 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
         q.prog_off = c->prog_off;
         q.stats = c->stats;
         order_stream(c, static_cast<cudaStream_t>(stream));
+        q.max_ctas = c->max_ctas;
         CU(launch_hier_push(q, dtype, hmode ? static_cast<int>(g_dtype) : 0, static_cast<cudaStream_t>(stream)));
         c->launches++;
         return BF_OK;
@@ -1342,6 +1345,14 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
     order_stream(c, static_cast<cudaStream_t>(stream));
     CU(launch_hier(p, dtype, 0, static_cast<cudaStream_t>(stream)));
     c->launches++;
+    return BF_OK;
+}
+
+bf_status bf_set_max_ctas(bf_ctx *c, int ctas) {
+    bf_status s = check_ctx(c, false);
+    if (s) return s;
+    if (ctas < 0 || ctas > kMaxGrid) return fail(BF_ERR_ARG, "max_ctas must be in [0, %d]", kMaxGrid);
+    c->max_ctas = ctas;
     return BF_OK;
 }
 

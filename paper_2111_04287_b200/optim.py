@@ -79,14 +79,17 @@ class DistributedAdaptThenCombineOptimizer:
     lr:       SGD step (momentum is out of scope)
     wire:     dtype of the published copy (torch.float32 or torch.bfloat16)
     bucket_bytes: tensor-fusion bucket size (fp32 bytes per agent)
-    overlap:  launch each bucket's step from backward hooks
+    overlap:  launch each bucket's step from backward hooks, on a side stream, so the
+              exchange runs while backward computes the earlier layers
+    overlap_ctas: with overlap, the exchange kernels' CTA cap (bf_set_max_ctas) -- the
+              exchange leaves the other SMs to backward; 0 keeps the context's setting
     awc:      adapt-WITH-combine (Eq. 16) instead of ATC
     grad_dtype: dtype of the flat gradient buffers (fp32 or bf16)
     """
 
     def __init__(self, ctx, params: Iterable[torch.Tensor], lr: float, wire: torch.dtype = torch.float32,
                  bucket_bytes: int = 25 << 20, overlap: bool = False, awc: bool = False,
-                 grad_dtype: torch.dtype = torch.float32):
+                 grad_dtype: torch.dtype = torch.float32, overlap_ctas: int = 0):
         self.ctx = ctx
         self.lr = float(lr)
         self.wire = wire
@@ -104,7 +107,11 @@ class DistributedAdaptThenCombineOptimizer:
         self.buckets = [_Bucket([params[i] for i in idx], ctx.k, grad_dtype) for idx in plan]
         self.steps_launched = 0
         self._hooks = []
+        self._side = None
         if overlap:
+            self._side = torch.cuda.Stream(device=params[0].device)
+            if overlap_ctas:
+                ctx.set_max_ctas(overlap_ctas)
             for b in self.buckets:
                 for p in b.params:
                     self._hooks.append(p.register_post_accumulate_grad_hook(self._make_hook(b)))
@@ -120,18 +127,27 @@ class DistributedAdaptThenCombineOptimizer:
     def _make_hook(self, b: _Bucket):
         def hook(_p):
             b.pending -= 1
-            if b.pending == 0:   # every gradient of the bucket is accumulated: step it now
-                self._step_bucket(b)
+            if b.pending == 0:   # every gradient of the bucket is accumulated: step it now, beside backward
+                self._side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(self._side):
+                    self._step_bucket(b)
         return hook
 
     def step(self):
         """Without overlap: one fused ATC call per bucket.  With overlap the
-        buckets were already stepped by the hooks during backward; step()
-        re-arms them (and steps any bucket whose hooks did not all fire)."""
+        buckets were already stepped by the hooks during backward (side stream);
+        step() steps any bucket whose hooks did not all fire, joins the side
+        stream into the current one and re-arms the hooks."""
         for b in self.buckets:
-            if not self.overlap or b.pending > 0:
+            if not self.overlap:
                 self._step_bucket(b)
+            elif b.pending > 0:
+                self._side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(self._side):
+                    self._step_bucket(b)
             b.pending = len(b.params)
+        if self.overlap:
+            torch.cuda.current_stream().wait_stream(self._side)
 
     def zero_grad(self):
         for b in self.buckets:

@@ -705,7 +705,9 @@ def test_optimizer_bucketed_matches_oracle(overlap, awc):
     torch.manual_seed(0)
     params = [torch.nn.Parameter(torch.randn(n, *s, device="cuda")) for s in shapes]
     X = np.concatenate([_np(p.detach().reshape(n, -1)) for p in params], axis=1)
-    opt = DistributedAdaptThenCombineOptimizer(ctx, params, lr, bucket_bytes=4 * 2000, overlap=overlap, awc=awc)
+    # with overlap: steps on a side stream during backward, exchange capped at 24 CTAs
+    opt = DistributedAdaptThenCombineOptimizer(ctx, params, lr, bucket_bytes=4 * 2000, overlap=overlap, awc=awc,
+                                               overlap_ctas=24 if overlap else 0)
     assert len(opt.buckets) >= 3
     # gradients from a real backward: loss = sum_i c_i * sum(p_i^2) / 2  ->  g_i = c_i * p_i
     coef = [0.1 * (i + 1) for i in range(len(params))]

@@ -316,26 +316,33 @@ def main():
         ctx.atc_step(x, gs[s % 2], a.lr, wire=wire_dt)
     barrier()
     stream = torch.cuda.current_stream()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     l0 = ctx.kernel_launches()
     t_begin = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    # the timed region: K back-to-back steps, no event between them
     t_begin.record(stream)
     for s in range(a.steps):
-        starts[s].record(stream)
         ctx.atc_step(x, gs[s % 2], a.lr, wire=wire_dt)
-        ends[s].record(stream)
     t_end.record(stream)
     barrier()
     launches = ctx.kernel_launches() - l0
     total_ms = t_begin.elapsed_time(t_end)
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    kern_ms = sum(step_ms) / a.steps
-    # one-peer rotates through tau = ceil(log2 n) graphs: mean step time per graph
+    kern_ms = total_ms / a.steps   # one launch per step: the kernel's average launch duration
+    # per-round detail (diagnostic, after the timed region): one-peer rotates through
+    # tau = ceil(log2 n) graphs; each step bracketed by its own events
     tau_r = max(1, (ctx.n - 1).bit_length()) if a.topology == "one_peer" else 1
-    by_round = [statistics.mean(step_ms[i] for i in range(a.steps) if (a.warmup + i) % tau_r == r)
-                for r in range(min(tau_r, a.steps))]
+    n_diag = max(tau_r * 3, 3)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(n_diag)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(n_diag)]
+    for s in range(n_diag):
+        starts[s].record(stream)
+        ctx.atc_step(x, gs[s % 2], a.lr, wire=wire_dt)
+        ends[s].record(stream)
+    barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    r_diag0 = a.warmup + a.steps
+    by_round = [statistics.mean(step_ms[i] for i in range(n_diag) if (r_diag0 + i) % tau_r == r)
+                for r in range(tau_r)]
     ctx.poll_error()
 
     # ---- end to end through the public API: host gradients in, sample out ----
@@ -377,7 +384,7 @@ def main():
         n1.record(stream)
         barrier()
         # schedule rounds of the timed calls (every schedule-mode call advances the round)
-        r0 = a.warmup + a.steps + (0 if a.no_e2e else 2 + a.steps) + 3
+        r0 = a.warmup + a.steps + n_diag + (0 if a.no_e2e else 2 + a.steps) + 3
         nar = {"ms": n0.elapsed_time(n1) / nsteps, "steps": nsteps, "rounds": range(r0, r0 + nsteps)}
         del xn, yn
     clk = clocks.stop()
@@ -400,7 +407,7 @@ def main():
         # process also publishes its wire copy (w B per element).  Local sources
         # are combined in registers, remote sources cross NVLink (d_in remote x w).
         tau = max(1, (n - 1).bit_length())
-        rounds = range(a.warmup, a.warmup + a.steps)
+        rounds = range(a.warmup, a.warmup + a.steps)   # the schedule rounds of the timed steps
 
         def sources(gid, r):
             if n == 1 or a.topology == "self":
@@ -445,8 +452,12 @@ def main():
         # mean over rounds of max(HBM time, NVLink time) at the peaks, / measured
         roof["t_roof_ms"] = t_roof * 1e3
         roof["frac_per_round_bound"] = t_roof * 1e3 / ms_kern
-        roof["by_round"] = [{"ms": m, "t_roof_ms": roof_by_round[r] * 1e3, "frac": roof_by_round[r] * 1e3 / m}
+        roof["by_round"] = [{"ms": m, "t_roof_ms": roof_by_round.get(r, 0.0) * 1e3,
+                             "frac": roof_by_round.get(r, 0.0) * 1e3 / m if m > 0 else None}
                             for r, m in enumerate(ms_by_round)]
+        roof["by_round_note"] = "per-round times from separate event-bracketed steps after the timed region"
+        # every schedule round of the timed steps is one roofline class: one-peer with
+        # tau graphs needs steps >= tau for every class to be present
         roof["traffic"] = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):

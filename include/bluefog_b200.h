@@ -30,12 +30,20 @@
  * (later calls return BF_ERR_STATE).  bf_last_error() gives a message
  * (thread-local).  No call ever blocks forever: every device wait is bounded.
  *
- * Collectives: bf_connect_peers, bf_set_topology, bf_set_machine_topology,
- * bf_reserve, bf_neighbor_allreduce, bf_atc_step,
- * bf_hierarchical_neighbor_allreduce (and its ATC / AWC steps), bf_win_create, bf_win_free and
- * bf_barrier must be called by every process in the same order.  Window
- * data calls (put / accumulate / update / collect) are one-sided and need
- * no matching call.
+ * Collectives: bf_connect_peers, bf_set_topology, bf_set_topology_local,
+ * bf_set_machine_topology, bf_reserve, bf_alloc, bf_neighbor_allreduce,
+ * bf_atc_step, bf_awc_step, bf_exact_diffusion_step, bf_gt_uv_step,
+ * bf_gt_y_step, bf_hierarchical_neighbor_allreduce (and its ATC / AWC steps),
+ * bf_win_create, bf_win_free and bf_barrier must be called by every process in
+ * the same order (bf_set_max_ctas and bf_hier_set_multicast with the same
+ * arguments on every process).  Window data calls (put / accumulate / update /
+ * collect / get) are one-sided and need no matching call.
+ *
+ * Transfer across GPUs (internal, chosen per call): messages up to 32768
+ * elements per agent travel as epoch-tagged 64-bit words (no fence on the data
+ * path); larger ones are pushed into the readers' inboxes (static topologies and
+ * schedules) or pulled by the readers (per-call pull-only views).  BF_XFER=pull
+ * and BF_LL=0 (read at bf_init) force the pull path / turn the tagged words off.
  */
 #ifndef BLUEFOG_B200_H
 #define BLUEFOG_B200_H

@@ -59,6 +59,9 @@ namespace bf {
 // release overtaking an earlier one never moves a word backwards.
 // (measured at N = 2: K = 1 one-peer 0.233 ms with one signal warp, 0.201 with 4,
 // 0.193-0.195 with 8; K = 2 is best with 4 -- 8 more warps cost it registers)
+#ifndef BF_PUSH_PREFETCH
+#define BF_PUSH_PREFETCH 1   // K >= 4: issue sub-item m's x / g loads before the combine of sub-item m - kLag
+#endif
 #ifndef BF_PUSH_K4_MINB
 #define BF_PUSH_K4_MINB 2   // CTAs per SM of the K = 4 push kernel (1: 192 KB lag, 4 signal warps;
                             // measured N = 2 exp-2: 2 per SM 0.72 ms, 1 per SM 0.78 ms)
@@ -280,8 +283,35 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
             // nothing crosses processes for this process (e.g. a schedule round inside it)
         }
         int slot = 0;
+        // non-hierarchical modes: the x / g loads of sub-item m are issued before the
+        // combine of sub-item m - L, so their HBM latency overlaps the inbox reads
+        // (measured at N = 2: K = 4 exp-2 0.715 -> 0.704 ms; K = 1 one-peer 0.183 -> 0.195 ms, so K >= 4 only)
+        constexpr bool PREFETCH = !HIER && BF_PUSH_PREFETCH && K >= 4;
         for (int m = 0; m < nmine + L; ++m, slot = slot + 1 == L ? 0 : slot + 1) {
             const int mc = m - L;
+            typename VecN<XT, V>::Raw xraw[PREFETCH ? K : 1];
+            typename VecN<GT, V>::Raw graw[PREFETCH && HAS_G ? K : 1];
+            if constexpr (PREFETCH) {
+                if (m < nmine) {
+                    const long long base = static_cast<long long>(sub(m)) * kSubT;
+                    const int valid = clamp_valid_v<V>(count - base, e0);
+                    if (vec && valid == V) {
+#pragma unroll
+                        for (int a = 0; a < K; ++a) VecN<XT, V>::load_raw_fast(xrow(a) + base + e0, xraw[a], pol_stream);
+                        if constexpr (HAS_G) {
+#pragma unroll
+                            for (int a = 0; a < K; ++a) VecN<GT, V>::load_raw_fast(grow(a) + base + e0, graw[a], pol_stream);
+                        }
+                    } else {
+#pragma unroll
+                        for (int a = 0; a < K; ++a) VecN<XT, V>::load_raw(xrow(a) + base + e0, xraw[a], valid, pol_stream);
+                        if constexpr (HAS_G) {
+#pragma unroll
+                            for (int a = 0; a < K; ++a) VecN<GT, V>::load_raw(grow(a) + base + e0, graw[a], valid, pol_stream);
+                        }
+                    }
+                }
+            }
             // ---------------- combine sub-item mc: local part (smem) + remote tiles (inbox) ----------------
             if (mc >= 0) {
                 const long long base = static_cast<long long>(sub(mc)) * kSubT;
@@ -386,13 +416,21 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
 #pragma unroll
                         for (int i = 0; i < V; ++i) xv[a][i] = sum[i] * invL;
                     }
+                } else if constexpr (PREFETCH) {
+#pragma unroll
+                    for (int a = 0; a < K; ++a) VecN<XT, V>::unpack(xraw[a], xv[a]);
                 } else {
 #pragma unroll
                     for (int a = 0; a < K; ++a) VecN<XT, V>::load_hint(xrow(a) + base + e0, xv[a], valid, vec, pol_stream);
                 }
                 if constexpr (HAS_G && !HIER) {
+                    if constexpr (PREFETCH) {
 #pragma unroll
-                    for (int a = 0; a < K; ++a) VecN<GT, V>::load_hint(grow(a) + base + e0, gv[a], valid, vec, pol_stream);
+                        for (int a = 0; a < K; ++a) VecN<GT, V>::unpack(graw[a], gv[a]);
+                    } else {
+#pragma unroll
+                        for (int a = 0; a < K; ++a) VecN<GT, V>::load_hint(grow(a) + base + e0, gv[a], valid, vec, pol_stream);
+                    }
                 }
                 if constexpr (MODE == 1 || MODE == 5) {   // Eq. 4 (GT: u - lr y)
 #pragma unroll

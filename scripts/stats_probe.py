@@ -44,7 +44,7 @@ def main():
     ctx.exchange_stats(reset=True)
     tau = max(1, (n - 1).bit_length()) if topo == "one_peer" else 1
     names = ["kernel", "cons_wait", "comm_wait_peer", "comm_wait_slot", "fence", "fences", "polls", "prologue"]
-    if os.environ.get("BF_XFER", "push") != "pull" and k <= 2 and world > 1:   # exchange_push.cuh slots
+    if os.environ.get("BF_XFER", "push") != "pull" and (k <= 2 or os.environ.get("BF_XFER") == "push_all") and world > 1:   # exchange_push.cuh slots
         names = ["kernel", "cons_wait", "first_ready", "loop_end", "fence", "fences", "polls", "prologue"]
     rows = {r: [] for r in range(tau)}
     for s in range(6 * tau):

@@ -59,6 +59,23 @@ def main():
                 torch.cuda.synchronize()
                 check(f"static {topo} {dtype} {count}", np_(y), ora.mix(W, X), W, X, tol)
 
+    # ---- around the small-message threshold (tagged words <= 32768 elements, push above) ----
+    ctx.set_topology(ora.exp2(n))
+    We = ora.exp2(n)
+    for count in (32767, 32768, 32769, 40001):
+        for dtype, tol in ((torch.float32, 1e-6), (torch.bfloat16, 1e-2)):
+            x, X = inputs(count, dtype, seed_off=11)
+            y = ctx.neighbor_allreduce(x)
+            torch.cuda.synchronize()
+            check(f"threshold nar {dtype} {count}", np_(y), ora.mix(We, X), We, X, tol)
+        x, X = inputs(count, seed_off=12)
+        G = np.stack([synthetic.uniform(synthetic.grad_seed(2, r), count, scale=2.0 ** -7) for r in range(n)])
+        g = torch.from_numpy(G[rows].copy()).cuda()
+        ctx.atc_step(x, g, 0.1, wire=torch.bfloat16)
+        torch.cuda.synchronize()
+        check(f"threshold atc bf16 wire {count}", np_(x), ora.atc(We, X, G.astype(np.float64), 0.1, wire_bf16=True),
+              We, X, 1e-2, np.abs(We) @ (0.1 * np.abs(G.astype(np.float64))))
+
     # ---- dynamic push / pull / push-pull ------------------------------------
     rng = np.random.default_rng(11)
     W = (rng.random((n, n)) < 0.6) * rng.uniform(0.1, 1.0, (n, n))
@@ -170,6 +187,10 @@ def main():
         y = ctx.hierarchical_neighbor_allreduce(x)
         torch.cuda.synchronize()
         check(f"hier L={L}", np_(y), ora.hier(WM, L, X), np.kron(WM, np.full((L, L), 1.0 / L)), X, 1e-6)
+        xb, Xb = inputs(40000, torch.bfloat16)
+        yb = ctx.hierarchical_neighbor_allreduce(xb)
+        torch.cuda.synchronize()
+        check(f"hier bf16 L={L}", np_(yb), ora.hier(WM, L, Xb), np.kron(WM, np.full((L, L), 1.0 / L)), Xb, 1e-2)
         Gh = np.stack([synthetic.uniform(synthetic.grad_seed(6, r), 40000, scale=2.0 ** -7) for r in range(n)])
         gh = torch.from_numpy(Gh[rows].copy()).cuda()
         Kh = np.kron(WM, np.full((L, L), 1.0 / L))

@@ -383,7 +383,11 @@ class Context:
         P = local_size // self.k
         if self.nprocs % P:
             raise ValueError("machines must tile the processes")
-        groups = [dist.new_group(list(range(m * P, (m + 1) * P))) for m in range(self.nprocs // P)]
+        cache = getattr(self, "_machine_groups", None) or {}
+        if P not in cache:   # every process creates every machine's group once (collective)
+            cache[P] = [dist.new_group(list(range(m * P, (m + 1) * P))) for m in range(self.nprocs // P)]
+            self._machine_groups = cache
+        groups = cache[P]
         mine = groups[self.proc // P]
         cap = (int(max_count) + 3) // 4 * 4
         t = symm.empty(2 * cap, dtype=torch.float32, device=f"cuda:{self.device}")
@@ -428,6 +432,9 @@ class Context:
     # ---- windows ---------------------------------------------------
     def win_create(self, tensor: torch.Tensor, name: str, zero_init: bool = True, with_p: bool = False) -> bool:
         count = self._rows(self._dev(tensor))
+        if not hasattr(self, "_windows"):
+            self._windows = {}
+        self._windows[name] = (tensor.dtype, tensor.numel())
         torch.cuda.synchronize(self.device)
         check(self.lib.bf_win_create(self.h, name.encode(), C.c_void_p(tensor.data_ptr()), count,
                                      _DT[tensor.dtype], 1 if zero_init else 0, 1 if with_p else 0))
@@ -472,6 +479,7 @@ class Context:
     def win_free(self, name: str) -> bool:
         torch.cuda.synchronize(self.device)
         check(self.lib.bf_win_free(self.h, name.encode()))
+        getattr(self, "_windows", {}).pop(name, None)
         return True
 
     def win_put(self, name: str, self_weight=None, dst_weights=None, agent_mask: int = 0, stream=None) -> bool:
@@ -491,6 +499,9 @@ class Context:
         """Gradient-in-window push (SGP-style): x <- x - lr g, then win_accumulate, in one kernel.
         g: device tensor of the window's dtype and shape."""
         self._dev(g, "g")
+        win = getattr(self, "_windows", {}).get(name)
+        if win is not None and (g.dtype != win[0] or g.numel() != win[1]):
+            raise ValueError(f"g must have the window's dtype {win[0]} and {win[1]} elements")
         if not g.is_contiguous():
             raise ValueError("g must be contiguous")
         v = self._views(self_weight, None, dst_weights)

@@ -86,6 +86,8 @@ def lib():
         L.ora_winp_get_x.argtypes = [C.c_void_p, _dp]
         L.ora_atc_fixed_point.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, C.c_double, C.c_double,
                                           C.c_int, _dp]
+        L.ora_comm_cost.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double]
+        L.ora_comm_cost.restype = C.c_double
     return _lib
 
 
@@ -425,3 +427,11 @@ def atc_fixed_point(W, A_stack, b_stack, lr, X0=None, tol=1e-15, max_iter=200000
     if it < 0:
         raise RuntimeError("ATC fixed-point iteration did not converge")
     return X, it
+
+
+COMM_PRIMITIVES = {"parameter_server": 0, "ring_allreduce": 1, "byte_ps": 2, "partial_averaging": 3}
+
+
+def comm_cost(primitive, n, M, B, L):
+    """Table 1: seconds for one averaging (ora_comm_cost)."""
+    return lib().ora_comm_cost(COMM_PRIMITIVES[primitive], int(n), float(M), float(B), float(L))

@@ -713,3 +713,24 @@ int ora_atc_fixed_point(int n, int m, int d, const double *W, const double *A, c
     free(xh); free(Xn); free(g);
     return it >= max_iter ? -1 : it;
 }
+
+/* ========================================================================
+ * Communication cost model, Table 1 (after [ben2019]):
+ * time of one averaging of an M-byte message over n nodes with link bandwidth
+ * B (bytes/s) and direct-communication latency L (s).
+ *   0 parameter server   nM/B + nL        (global averaging)
+ *   1 ring-allreduce     2M/B + 2nL       (global averaging)
+ *   2 Byte-PS            M/B + nL         (global averaging)
+ *   3 partial averaging  M/B + L          (BlueFog, one neighbour at a time;
+ *                        d_in in-neighbours over independent links: still M/B + L)
+ * Returns a negative value for an unknown primitive.
+ * ====================================================================== */
+double ora_comm_cost(int primitive, int n, double M, double B, double L) {
+    switch (primitive) {
+        case 0: return n * M / B + n * L;
+        case 1: return 2.0 * M / B + 2.0 * n * L;
+        case 2: return M / B + n * L;
+        case 3: return M / B + L;
+        default: return -1.0;
+    }
+}

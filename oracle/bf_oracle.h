@@ -129,6 +129,11 @@ int ora_lsq_solve(int n, int m, int d, const double *A, const double *b, double 
 int ora_atc_fixed_point(int n, int m, int d, const double *W, const double *A, const double *b, double lr,
                         double tol, int max_iter, double *X);
 
+/* ---- communication cost model, Table 1 ----------
+ * 0 parameter server nM/B + nL, 1 ring-allreduce 2M/B + 2nL, 2 Byte-PS M/B + nL,
+ * 3 partial averaging M/B + L (seconds; M bytes, B bytes/s, L seconds). */
+double ora_comm_cost(int primitive, int n, double M, double B, double L);
+
 #ifdef __cplusplus
 }
 #endif

@@ -807,3 +807,17 @@ def test_win_adapt_then_accumulate_by_hand():
     assert win.x()[:, 0].tolist() == [0.5, 0.5]
     # mass after the step: the step removes lr * g from the total, nothing else does
     assert win.mass(0) == 1.0
+
+
+def test_comm_cost_table1_by_hand():
+    # Table 1 evaluated by hand for n = 8, M = 100 MB,
+    # B = 1e9 B/s, L = 1e-5 s; and P:242 "O(1) latency and O(1) transmission time,
+    # independent of n" for partial averaging, O(n) for every global primitive
+    M, B, L = 1e8, 1e9, 1e-5
+    assert ora.comm_cost("parameter_server", 8, M, B, L) == 8 * 0.1 + 8e-5
+    assert ora.comm_cost("ring_allreduce", 8, M, B, L) == 0.2 + 16e-5
+    assert ora.comm_cost("byte_ps", 8, M, B, L) == 0.1 + 8e-5
+    assert ora.comm_cost("partial_averaging", 8, M, B, L) == 0.1 + 1e-5
+    for prim in ("parameter_server", "ring_allreduce", "byte_ps"):
+        assert ora.comm_cost(prim, 64, M, B, L) > ora.comm_cost(prim, 8, M, B, L)
+    assert ora.comm_cost("partial_averaging", 64, M, B, L) == ora.comm_cost("partial_averaging", 8, M, B, L)

@@ -252,6 +252,7 @@ struct WinParams {
     unsigned long long p_off;               // double [k]
     unsigned long long dec_off;             // u64 [k][maxdout] push decisions
     unsigned long long snap_off;            // u64 [k][maxdin][2] collect snapshot (c, v)
+    unsigned long long ctl_off;             // u64 [4]: push gate (snapshot, done), collect gate (snapshot, done)
     // per-call tables
     float self_w[kMaxK];
     unsigned char nout[kMaxK];              // selected destinations of local agent a

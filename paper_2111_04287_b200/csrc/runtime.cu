@@ -1451,6 +1451,7 @@ bf_status bf_win_create(bf_ctx *c, const char *name, void *x, size_t count, bf_d
     WALLOC(p_off, K * 8);
     WALLOC(dec_off, K * DO * 8);
     WALLOC(snap_off, K * DI * 16);
+    WALLOC(ctl_off, 4 * 8);
 #undef WALLOC
     w.alloc_end = c->heap_used;
     b.maxdin = w.maxdin;
@@ -1566,7 +1567,7 @@ static bf_status win_push(bf_ctx *c, const char *name, const bf_weights *weights
     }
     order_stream(c, static_cast<cudaStream_t>(stream));
     CU(launch_win_push(p, 0, static_cast<cudaStream_t>(stream)));
-    c->launches += 2;
+    c->launches += 1;
     return BF_OK;
 }
 
@@ -1631,7 +1632,7 @@ static bf_status win_pull(bf_ctx *c, const char *name, const bf_weights *weights
     }
     order_stream(c, static_cast<cudaStream_t>(stream));
     CU(launch_win_collect(p, update, 0, static_cast<cudaStream_t>(stream)));
-    c->launches += 2;
+    c->launches += 1;
     return BF_OK;
 }
 

@@ -10,8 +10,9 @@
 //   outbox and later payloads accumulate onto it (sender-side accumulation).
 //   The consumer's collect sums the payloads consumed..version-1, then
 //   releases consumed = version into i's heap.
-// Decisions are snapshotted by a one-block kernel before the streaming kernel
-// so every CTA acts on the same decision.  Nothing here waits on another
+// Decisions are snapshotted by CTA 0 of the streaming kernel and published to the
+// other CTAs through a per-window gate (win_gate), so every CTA acts on the same
+// decision -- one launch per operation.  Nothing here waits on another
 // agent, so these kernels can run on a single GPU for any number of agents.
 #include <cuda_bf16.h>
 
@@ -27,8 +28,46 @@ __device__ __forceinline__ bool active(const WinParams &p, int a) {
     return (p.agent_mask >> a) & 1ull;
 }
 
+// ---- snapshot gate ---------------------------------------------------------
+// The decisions of one launch (push: deliver or keep in the outbox; collect: the
+// (consumed, version) window of every slot) must be the same in every CTA while
+// peers keep moving the counters, so CTA 0 takes them and the others wait for it.
+// ctl[0] = last snapshot taken, ctl[1] = last launch finished (written by the last
+// CTA): a launch's number is ctl[1] + 1, read by every CTA at its start -- ctl[1]
+// changes only at the end of a launch, and launches of one window are stream
+// ordered -- so no host counter is involved (CUDA-graph capturable).  The grid
+// is co-resident (cooperative launch).  Returns the launch number, 0 on a fault.
+static __device__ __noinline__ bool win_wait_snapshot(const Geometry &g, const unsigned long long *flag,
+                                                      unsigned long long want) {
+    return spin_ge(g, flag, want, false);
+}
+
+template <typename F>
+__device__ unsigned long long win_gate(const WinParams &p, unsigned long long *ctl, F snapshot) {
+    __shared__ unsigned long long s_want;
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) {
+        s_want = *reinterpret_cast<volatile unsigned long long *>(&ctl[1]) + 1;
+        s_ok = 1;
+    }
+    __syncthreads();
+    const unsigned long long want = s_want;
+    if (blockIdx.x == 0) {
+        snapshot();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_gpu(&ctl[0], want);
+        }
+    } else if (threadIdx.x == 0) {
+        s_ok = win_wait_snapshot(p.geo, &ctl[0], want) ? 1 : 0;
+    }
+    __syncthreads();
+    return s_ok ? want : 0ull;
+}
+
 // ---- push side ------------------------------------------------------------
-__global__ void win_push_decide(const __grid_constant__ WinParams p) {
+__device__ __noinline__ void win_push_decide(const WinParams &p) {
     const Geometry &g = p.geo;
     const unsigned long long me = g.peer_base[g.me];
     for (int idx = threadIdx.x; idx < g.k * kMaxS; idx += blockDim.x) {
@@ -86,7 +125,7 @@ __device__ __forceinline__ void win_load_raw(const T *base, typename VecN<T, V>:
 #define BF_WIN_PUSH_MINB 4   // C5 A/B (profiles/r01_window_minblocks_ab.txt): 7.17 -> 7.09 ms per round
 #endif
 #ifndef BF_WIN_COLLECT_MINB
-#define BF_WIN_COLLECT_MINB -1   // -1: 4 CTAs/SM for bf16 windows, 3 for fp32 (no spills at 80 registers)
+#define BF_WIN_COLLECT_MINB 3    // 3 CTAs/SM (80 registers); -1: 4 for bf16, 3 for fp32
 #endif
 // BF_WIN_HINTS=1: x / out / slot streams carry an L2 evict-first policy (tuning variant)
 #ifndef BF_WIN_HINTS
@@ -105,7 +144,8 @@ __device__ __forceinline__ void win_load_raw(const T *base, typename VecN<T, V>:
 #define BF_PUSH_LB __launch_bounds__(kThreads)
 #endif
 // C5 round at N = 1 (340M bf16 x 8): 2 CTAs/SM (125 registers) 6.32 ms, 3 per SM 5.73 ms,
-// 4 per SM 5.70 ms (0.89 of the HBM roofline; profiles/r02_window_collect_ab.txt)
+// 4 per SM 5.70 ms (0.89 of the HBM roofline; profiles/r02_window_collect_ab.txt); with
+// the snapshot gate folded in (win_gate), 4 per SM spills: 5.90 ms, 3 per SM 5.72 ms
 #if BF_WIN_COLLECT_MINB > 0
 #define BF_COLLECT_LB __launch_bounds__(kThreads, BF_WIN_COLLECT_MINB)
 #elif BF_WIN_COLLECT_MINB < 0
@@ -124,6 +164,9 @@ __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) 
     const long long count = g.count;
     const bool vec = g.vec_ok != 0;
     const int k = g.k;
+    unsigned long long *ctl = at<unsigned long long>(me, p.ctl_off);   // [0..1]: push gate
+    const unsigned long long launch = win_gate(p, ctl, [&] { win_push_decide(p); });
+    if (!launch) return;
     const unsigned long long *dec = at<unsigned long long>(me, p.dec_off);
     const unsigned long long *dlv = at<unsigned long long>(me, p.delivered_off);
     const unsigned int *obv = at<unsigned int>(me, p.obvalid_off);
@@ -223,6 +266,7 @@ __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) 
         if (prev == gridDim.x - 1) {
             __threadfence_system();
             pad->done_ctr = 0;
+            ctl[1] = launch;   // this launch is finished: the next one takes launch + 1
             unsigned long long *dlvw = at<unsigned long long>(me, p.delivered_off);
             unsigned int *obvw = at<unsigned int>(me, p.obvalid_off);
             double *P = at<double>(me, p.p_off);
@@ -259,7 +303,7 @@ __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) 
 }
 
 // ---- consumer side ----------------------------------------------------------
-__global__ void win_collect_decide(const __grid_constant__ WinParams p) {
+__device__ __noinline__ void win_collect_decide(const WinParams &p) {
     const Geometry &g = p.geo;
     const unsigned long long me = g.peer_base[g.me];
     for (int idx = threadIdx.x; idx < g.k * kMaxS; idx += blockDim.x) {
@@ -284,6 +328,9 @@ __global__ void BF_COLLECT_LB win_collect_kernel(const __grid_constant__ WinPara
     const long long count = g.count;
     const bool vec = g.vec_ok != 0;
     const int k = g.k;
+    unsigned long long *ctl = at<unsigned long long>(me, p.ctl_off) + 2;   // [2..3]: collect gate
+    const unsigned long long launch = win_gate(p, ctl, [&] { win_collect_decide(p); });
+    if (!launch) return;
     const unsigned long long *snap = at<unsigned long long>(me, p.snap_off);
     // per-CTA acquire of the producers' versions (orders the slot reads below)
     for (int idx = threadIdx.x; idx < k * p.maxdin; idx += blockDim.x)
@@ -371,6 +418,7 @@ __global__ void BF_COLLECT_LB win_collect_kernel(const __grid_constant__ WinPara
         if (prev == gridDim.x - 1) {
             __threadfence();
             pad->done_ctr = 0;
+            ctl[1] = launch;
             unsigned long long *cl = at<unsigned long long>(me, p.conslocal_off);
             double *P = at<double>(me, p.p_off);
             const double *ps = at<const double>(me, p.pslot_off);
@@ -477,25 +525,28 @@ static int occ_grid(F fn, long long items) {
     return g < 1 ? 1 : static_cast<int>(g);
 }
 
+// cooperative launch: CTAs 1.. wait for CTA 0's snapshot, so every CTA is resident
+template <typename K>
+static cudaError_t coop(K kernel, int grid, cudaStream_t s, const WinParams &p) {
+    void *args[] = {const_cast<WinParams *>(&p)};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kernel), dim3(grid), dim3(kThreads), args, 0, s);
+}
+template <typename K>
+static cudaError_t coop2(K kernel, int grid, cudaStream_t s, const WinParams &p, int update) {
+    void *args[] = {const_cast<WinParams *>(&p), &update};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kernel), dim3(grid), dim3(kThreads), args, 0, s);
+}
+
 cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s) {
-    win_push_decide<<<1, 256, 0, s>>>(p);
     const long long items = p.dtype == 0 ? win_items<float>(p.geo.k, p.geo.count) : win_items<bf16>(p.geo.k, p.geo.count);
     if (p.g) {
         if (grid <= 0)
             grid = p.dtype == 0 ? occ_grid(win_push_kernel<float, true>, items) : occ_grid(win_push_kernel<bf16, true>, items);
-        if (p.dtype == 0)
-            win_push_kernel<float, true><<<grid, kThreads, 0, s>>>(p);
-        else
-            win_push_kernel<bf16, true><<<grid, kThreads, 0, s>>>(p);
-        return cudaGetLastError();
+        return p.dtype == 0 ? coop(win_push_kernel<float, true>, grid, s, p) : coop(win_push_kernel<bf16, true>, grid, s, p);
     }
     if (grid <= 0)
         grid = p.dtype == 0 ? occ_grid(win_push_kernel<float, false>, items) : occ_grid(win_push_kernel<bf16, false>, items);
-    if (p.dtype == 0)
-        win_push_kernel<float, false><<<grid, kThreads, 0, s>>>(p);
-    else
-        win_push_kernel<bf16, false><<<grid, kThreads, 0, s>>>(p);
-    return cudaGetLastError();
+    return p.dtype == 0 ? coop(win_push_kernel<float, false>, grid, s, p) : coop(win_push_kernel<bf16, false>, grid, s, p);
 }
 
 cudaError_t launch_win_get(const WinParams &p, unsigned long long x_off, cudaStream_t s) {
@@ -510,15 +561,11 @@ cudaError_t launch_win_get(const WinParams &p, unsigned long long x_off, cudaStr
 }
 
 cudaError_t launch_win_collect(const WinParams &p, int update, int grid, cudaStream_t s) {
-    win_collect_decide<<<1, 256, 0, s>>>(p);
     if (grid <= 0)
         grid = p.dtype == 0 ? occ_grid(win_collect_kernel<float>, win_items<float>(p.geo.k, p.geo.count))
                             : occ_grid(win_collect_kernel<bf16>, win_items<bf16>(p.geo.k, p.geo.count));
-    if (p.dtype == 0)
-        win_collect_kernel<float><<<grid, kThreads, 0, s>>>(p, update);
-    else
-        win_collect_kernel<bf16><<<grid, kThreads, 0, s>>>(p, update);
-    return cudaGetLastError();
+    return p.dtype == 0 ? coop2(win_collect_kernel<float>, grid, s, p, update)
+                        : coop2(win_collect_kernel<bf16>, grid, s, p, update);
 }
 
 }  // namespace bf

@@ -17,7 +17,7 @@ def _ngpus():
 
 
 @pytest.mark.parametrize("nproc,k,hier", [(2, 1, "auto"), (2, 2, "auto"), (2, 4, "auto"), (2, 2, "fused"),
-                                          (4, 1, "auto"), (4, 2, "auto")])
+                                          (2, 3, "auto"), (4, 1, "auto"), (4, 2, "auto")])
 def test_multiprocess_parity(nproc, k, hier):
     # hier="fused": the hierarchical calls take the Kronecker mix in the fused
     # kernel across GPUs (BF_HIER=fused) instead of the staged kernel

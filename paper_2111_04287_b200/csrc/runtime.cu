@@ -117,6 +117,9 @@ struct bf_ctx {
     int nvls_L = 0;
     int ll = 1;                               // BF_LL=0 turns the small-message path off
     int max_ctas = 0;                         // bf_set_max_ctas: grid cap of the exchange kernels (0 = all SMs)
+    // host copy of the schedule round (advanced with every schedule-mode exchange call):
+    // only picks the kernel of a K = 4 round; the device counter drives the schedule
+    unsigned long long host_round = 0;
     bool win_ef = false;                      // BF_WIN_EF=1: new windows start with error feedback on
     // stream order across calls: every call of a context reads and advances the same
     // device state (epoch, round, slots, progress words), so a call issued on another
@@ -770,10 +773,11 @@ bf_status bf_set_dynamic_schedule(bf_ctx *c, int kind, uint64_t round0) {
         return fail(BF_ERR_STATE, "inner-outer schedule needs bf_set_machine_topology (machine size)");
     c->sched_kind = kind;
     c->sched_L = kind == 2 ? c->machine_L : 1;
+    c->host_round = round0;
     if (kind) {
         Pad *pad = reinterpret_cast<Pad *>(c->heap);
         order_stream(c, nullptr);
-    CU(launch_set_u64(&pad->round, round0, nullptr));
+        CU(launch_set_u64(&pad->round, round0, nullptr));
         c->launches++;
         CU(cudaDeviceSynchronize());
     }
@@ -793,6 +797,20 @@ bf_status bf_reserve(bf_ctx *c, size_t bytes_per_agent) {
 }
 
 // ---- hot path ---------------------------------------------------------------
+// K = 4 schedule rounds: push when every local agent's source sits on another process
+// (measured at N = 2, one-peer: that round 0.69 ms pushed vs 0.75 pulled; rounds with 1-2
+// remote sources of 4 run faster pulled).  Decided from the host copy of the round; in a
+// captured CUDA graph the capture-time choice is replayed -- either kernel is correct for
+// any round, the device counter drives the schedule.
+static bool all_remote_round(const bf_ctx *c) {
+    for (int a = 0; a < c->k; ++a) {
+        int src, dst;
+        sched_peers(c->sched_kind, c->n, c->sched_L, c->host_round, c->proc * c->k + a, src, dst);
+        if (src < 0 || src / c->k == c->proc) return false;
+    }
+    return true;
+}
+
 struct GtArgs {                     // push-sum gradient tracking steps (MODE 4 / 5)
     int mode = 0;
     const float *g2 = nullptr;
@@ -899,10 +917,11 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
                         p.pushq[a] |= 1u << (i / c->k);
             }
     }
-    // K = 4: push only for static W (measured at N = 2, 8 agents: exp-2 0.77 ms push vs
+        // K = 4: push only for static W (measured at N = 2, 8 agents: exp-2 0.77 ms push vs
     // 1.18 pull; one-peer rounds with 1-2 remote sources of 4 run faster pulled, 0.50 vs 0.60)
     if (!p.ll && p.kernel == 3 && c->nprocs > 1 && c->inbox_off && !static_tab && p.wmode != kWDynamic &&
-        (c->k == 1 || c->k == 2 || (c->k == 4 && (p.wmode == kWStatic || c->xfer == 2)))) {
+        (c->k == 1 || c->k == 2 ||
+         (c->k == 4 && (p.wmode == kWStatic || c->xfer == 2 || (p.wmode == kWSchedule && all_remote_round(c)))))) {
         p.push = 1;
         p.inbox_off = c->inbox_off;
         p.inbox_agent_stride = 2 * c->exch_cap;
@@ -918,6 +937,7 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     }
     order_stream(c, st);
     CU(launch_exchange(p, x_kind, awc_g ? x_kind : g_kind, wire_kind, y_kind, g != nullptr, c->max_ctas, st));
+    if (p.wmode == kWSchedule) c->host_round++;
     c->launches++;
     return BF_OK;
 }

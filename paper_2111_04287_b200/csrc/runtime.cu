@@ -108,7 +108,8 @@ struct bf_ctx {
     int hier_mode = 0;                        // BF_HIER: 0 auto, 1 staged (always), 2 fused (also across GPUs)
     int xfer = 1;                             // BF_XFER: 1 push (default across GPUs), 0 pull, 2 push_all (tuning)
     unsigned long long inbox_off = 0, pflag_off = 0;   // push inboxes [n][2][cap] + progress words (0: none)
-    unsigned long long ll_off = 0;            // tagged-word inboxes [n][2][kLLCap] u64 (small messages; 0: none)
+    unsigned long long ll_off = 0;            // tagged-word inboxes [n][2][ll_cap] u64 (small messages; 0: none)
+    long long ll_cap = kLLCap;                // BF_LL_CAP: elements per agent up to which tagged words are used
     // NVLS (bf_hier_set_multicast): this process's copy of a multicast-backed fp32 buffer
     // [2][nvls_cap] of its machine's group, the multicast address, and machine flags
     float *nvls_uc = nullptr;
@@ -250,7 +251,7 @@ bf_status ensure_exchange(bf_ctx *c, size_t bytes_per_agent) {
         }
     }
     if (c->nprocs > 1 && c->ll && (c->k == 1 || c->k == 2 || c->k == 4)) {   // small-message tagged inboxes
-        const size_t llb = static_cast<size_t>(c->n) * 2 * kLLCap * 8;
+        const size_t llb = static_cast<size_t>(c->n) * 2 * static_cast<size_t>(c->ll_cap) * 8;
         if (c->heap_used + llb + kAlign <= c->heap_bytes) {
             unsigned long long off;
             if ((s = heap_alloc(c, llb, &off))) return s;
@@ -499,6 +500,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     if (const char *x = getenv("BF_HIER")) c->hier_mode = strcmp(x, "staged") == 0 ? 1 : strcmp(x, "fused") == 0 ? 2 : 0;
     if (const char *x = getenv("BF_WIN_EF")) c->win_ef = atoi(x) != 0;
     if (const char *x = getenv("BF_LL")) c->ll = atoi(x) != 0;
+    if (const char *x = getenv("BF_LL_CAP")) c->ll_cap = std::max(4LL, std::min(atoll(x), 1LL << 26)) / 4 * 4;
     if (const char *x = getenv("BF_XFER")) c->xfer = strcmp(x, "pull") == 0 ? 0 : (strcmp(x, "push_all") == 0 ? 2 : 1);
     if (const char *x = getenv("BF_STATS"))
         if (atoi(x) && cudaMalloc(&c->stats, static_cast<size_t>(kMaxGrid) * 8 * 8) == cudaSuccess)
@@ -905,10 +907,10 @@ static bf_status exchange_common(bf_ctx *c, const void *x, const void *g, void *
     // hierarchical W keep the pull kernel
     // small messages across GPUs: tagged words, no fence, no progress word (exchange_ll.cuh)
     if (p.kernel == 3 && c->nprocs > 1 && c->ll_off && !static_tab && p.wmode != kWDynamic && !psi && !gt &&
-        static_cast<long long>(count) <= kLLCap && (c->k == 1 || c->k == 2 || c->k == 4)) {
+        static_cast<long long>(count) <= c->ll_cap && (c->k == 1 || c->k == 2 || c->k == 4)) {
         p.ll = 1;
         p.ll_off = c->ll_off;
-        p.ll_stride = static_cast<unsigned long long>(kLLCap) * 8;
+        p.ll_stride = static_cast<unsigned long long>(c->ll_cap) * 8;
         if (p.wmode == kWStatic)
             for (int a = 0; a < c->k; ++a) {
                 const int gid = c->proc * c->k + a;

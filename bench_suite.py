@@ -90,7 +90,9 @@ def main():
 
     def xheap(k, n, bytes_per_agent, extra):
         # exchange slots (k agents x 2 parities) + across GPUs the push inboxes (n x 2)
-        return (k + (n if world > 1 else 0)) * 2 * bytes_per_agent + extra
+        # and the tagged-word inboxes (n x 2 x BF_LL_CAP x 8 B)
+        ll = n * 2 * int(os.environ.get("BF_LL_CAP", "262144")) * 8 if world > 1 else 0
+        return (k + (n if world > 1 else 0)) * 2 * bytes_per_agent + extra + ll
 
     # ---------------------------------------------------------------- C1 ----
     if "c1" in only:

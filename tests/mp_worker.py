@@ -59,10 +59,11 @@ def main():
                 torch.cuda.synchronize()
                 check(f"static {topo} {dtype} {count}", np_(y), ora.mix(W, X), W, X, tol)
 
-    # ---- around the small-message threshold (tagged words <= 32768 elements, push above) ----
+    # ---- around the small-message thresholds (tagged words <= 262144 elements, or <= 32768
+    # when the heap is small; push above) ----
     ctx.set_topology(ora.exp2(n))
     We = ora.exp2(n)
-    for count in (32767, 32768, 32769, 40001):
+    for count in (32767, 32768, 32769, 262143, 262144, 262145):
         for dtype, tol in ((torch.float32, 1e-6), (torch.bfloat16, 1e-2)):
             x, X = inputs(count, dtype, seed_off=11)
             y = ctx.neighbor_allreduce(x)

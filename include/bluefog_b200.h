@@ -255,7 +255,8 @@ bf_status bf_hierarchical_neighbor_allreduce(bf_ctx *ctx, const void *x, void *y
  * Context.enable_nvls).  Then fp32 hierarchical calls with machines of local_size
  * agents (> agents_per_proc) and a static machine topology average each machine
  * with one multimem.ld_reduce per 16 bytes through the switch, before the
- * machine-level exchange.  The buffer holds 2 x count fp32 (double-buffered).
+ * machine-level exchange.  The buffer holds 4 x count fp32 (partial sums and
+ * machine averages, each double-buffered).
  * uc = NULL and mc = 0 unregister.  Local (not collective); every process of the
  * context must register for the path to be used consistently. */
 bf_status bf_hier_set_multicast(bf_ctx *ctx, int local_size, void *uc, unsigned long long mc, size_t bytes);

@@ -390,7 +390,7 @@ class Context:
         groups = cache[P]
         mine = groups[self.proc // P]
         cap = (int(max_count) + 3) // 4 * 4
-        t = symm.empty(2 * cap, dtype=torch.float32, device=f"cuda:{self.device}")
+        t = symm.empty(4 * cap, dtype=torch.float32, device=f"cuda:{self.device}")   # partials + averages, x 2
         h = symm.rendezvous(t, mine)
         mc = int(getattr(h, "multicast_ptr", 0) or 0)
         try:   # static query (device type, index) on current torch; older: a property
@@ -401,7 +401,7 @@ class Context:
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)   # every process takes the same path
         if not int(ok.item()):
             return False
-        check(self.lib.bf_hier_set_multicast(self.h, int(local_size), C.c_void_p(t.data_ptr()), mc, 2 * cap * 4))
+        check(self.lib.bf_hier_set_multicast(self.h, int(local_size), C.c_void_p(t.data_ptr()), mc, 4 * cap * 4))
         self._nvls = (t, h, groups)   # keep the buffer and its mapping alive
         return True
 

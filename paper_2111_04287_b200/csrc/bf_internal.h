@@ -171,6 +171,7 @@ struct ExchParams {
     int gt;                                 // kernel 3: 4 = GT y-step (MODE 4), 5 = GT u/v-step (MODE 5), else 0
     int hier_L;                             // push MODE 6-8 (hierarchical): rows per machine agent (machine size)
     int hier_in;                            // rows averaged per machine agent (0: hier_L; 1: x is a machine average)
+    const void *x_alt;                      // non-null: read x_alt instead of x when (epoch - 1) is odd (NVLS averages)
     int hier_mode;                          // 0: not hierarchical; 6, 7, 8: MODE of the hierarchical push
     int max_ctas;                           // hierarchical push launches: grid cap (0 = all SMs)
     const float *g2;                        // kernel 3 MODE 4 (GT y-step): g_prev [k][count] (fp32)
@@ -217,10 +218,11 @@ struct NvlsParams {
     int hmode;                              // 1: average x - lr g (H-ATC), else x
     float lr;
     float invL;                             // 1 / machine size
-    float *uc;                              // this process's copy of the multicast buffer: fp32 [2][cap]
+    float *uc;                              // this process's copy of the multicast buffer: fp32 [4][cap]
+                                            // (partials [2 parities], averages [2 parities])
     unsigned long long mc;                  // multicast address of the same buffer
     long long cap;                          // elements per parity half
-    float *avg;                             // output: the machine average [count]
+    float *avg;                             // (unused: the average stays in the buffer's average half)
     unsigned long long nflag_off;           // u64 [kMaxP][kMaxGrid] in every heap
     int proc0, P;                           // processes proc0 .. proc0 + P - 1 form this machine
 };

@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
     } else {
         // ============================ consumer warps ============================
         const unsigned long long pol_stream = policy_evict_first();
-        auto xrow = [&](int a) { return static_cast<const XT *>(p.x) + static_cast<long long>(a) * count; };
+        const XT *xbase = static_cast<const XT *>(p.x_alt && ((e - 1) & 1) ? p.x_alt : p.x);
+        auto xrow = [&](int a) { return xbase + static_cast<long long>(a) * count; };
         auto grow = [&](int a) { return static_cast<const GT *>(p.g) + static_cast<long long>(a) * count; };
         const int HL = HIER ? p.hier_L : 1;   // rows written per (machine) agent
         const int HLin = HIER && p.hier_in ? p.hier_in : HL;   // rows averaged (1: x is the machine average)

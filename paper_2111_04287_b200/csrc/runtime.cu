@@ -118,6 +118,10 @@ struct bf_ctx {
     unsigned long long nvls_mc = 0, nflag_off = 0;
     long long nvls_cap = 0;
     int nvls_L = 0;
+    // NVLS only pays when a machine spans enough processes: measured at N = 4, one machine of
+    // 4 GPUs 0.399 ms (NVLS) vs 0.522 ms (per-process partials pushed); machines of 2 GPUs
+    // 0.527 / 0.564 vs 0.516 / 0.533 ms.  BF_NVLS_MIN_P overrides.
+    int nvls_min_p = 4;
     int ll = 1;                               // BF_LL=0 turns the small-message path off
     int max_ctas = 0;                         // bf_set_max_ctas: grid cap of the exchange kernels (0 = all SMs)
     // host copy of the schedule round (advanced with every schedule-mode exchange call):
@@ -506,6 +510,7 @@ bf_status bf_init(int proc_rank, int n_procs, int agents_per_proc, int cuda_devi
     if (const char *x = getenv("BF_HIER")) c->hier_mode = strcmp(x, "staged") == 0 ? 1 : strcmp(x, "fused") == 0 ? 2 : 0;
     if (const char *x = getenv("BF_WIN_EF")) c->win_ef = atoi(x) != 0;
     if (const char *x = getenv("BF_LL")) c->ll = atoi(x) != 0;
+    if (const char *x = getenv("BF_NVLS_MIN_P")) c->nvls_min_p = std::max(2, atoi(x));
     if (const char *x = getenv("BF_LL_CAP")) c->ll_cap_req = std::max(4LL, std::min(atoll(x), 1LL << 26)) / 4 * 4;
     if (const char *x = getenv("BF_XFER")) c->xfer = strcmp(x, "pull") == 0 ? 0 : (strcmp(x, "push_all") == 0 ? 2 : 1);
     if (const char *x = getenv("BF_STATS"))
@@ -1173,7 +1178,8 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
     // kernel's hierarchical mode over the average row (machine-level exchange between the
     // processes of the same local index, broadcast to the K rows).
     if (c->hier_mode != 1 && c->nprocs > 1 && c->inbox_off && c->nvls_mc && c->nvls_L == L && !machine_weights &&
-        dtype == BF_FLOAT32 && L > c->k && L % c->k == 0 && static_cast<long long>(count) <= c->nvls_cap &&
+        dtype == BF_FLOAT32 && L > c->k && L % c->k == 0 && L / c->k >= c->nvls_min_p &&
+        static_cast<long long>(count) <= c->nvls_cap &&
         count * 4 <= c->exch_cap) {
         const int P = L / c->k, me = c->proc, m = me / P, l = me % P;
         if (!c->nflag_off) return fail(BF_ERR_STATE, "NVLS flags not allocated");
@@ -1189,8 +1195,7 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
         v.uc = c->nvls_uc;
         v.mc = c->nvls_mc;
         v.cap = c->nvls_cap;
-        float *avg = reinterpret_cast<float *>(c->heap + c->slot_off);   // the pull slots are idle here
-        v.avg = avg;
+        v.avg = nullptr;   // the average lands in the local copy of the buffer's average half
         v.nflag_off = c->nflag_off;
         v.proc0 = m * P;
         v.P = P;
@@ -1218,7 +1223,10 @@ static bf_status hier_common(bf_ctx *c, const void *x, void *y, size_t count, bf
         q.tab.nsrc[0] = static_cast<unsigned char>(cnt);
         for (int i = 0; i < NM; ++i)   // the process of local index l in every machine that reads machine m
             if (i != m && c->WM[static_cast<size_t>(i) * NM + m] != 0.0) q.pushq[0] |= 1u << (i * P + l);
-        q.x = avg;
+        // the machine exchange reads the average half of the NVLS launch's parity: that launch
+        // is the epoch before this one, so the push kernel picks x / x_alt by its epoch - 1
+        q.x = c->nvls_uc + 2 * c->nvls_cap;
+        q.x_alt = c->nvls_uc + 3 * c->nvls_cap;
         q.y = y;
         q.g = hmode == 2 ? g : nullptr;
         q.lr = hmode == 2 ? lr : 0.f;
@@ -1401,7 +1409,7 @@ bf_status bf_hier_set_multicast(bf_ctx *c, int local_size, void *uc, unsigned lo
                                 "agents_per_proc larger than it");
     c->nvls_uc = static_cast<float *>(uc);
     c->nvls_mc = mc;
-    c->nvls_cap = static_cast<long long>(bytes / 8) / 4 * 4;   // fp32 elements per parity half
+    c->nvls_cap = static_cast<long long>(bytes / 16) / 4 * 4;   // fp32 elements per half (partials and averages x 2)
     c->nvls_L = local_size;
     return BF_OK;
 }

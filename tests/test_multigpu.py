@@ -23,7 +23,8 @@ def test_multiprocess_parity(nproc, k, hier):
     # kernel across GPUs (BF_HIER=fused) instead of the staged kernel
     if _ngpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    env = dict(os.environ, BF_TEST_K=str(k), BF_TIMEOUT_MS="8000", BF_HIER=hier)
+    # BF_NVLS_MIN_P=2: the NVLS path also for machines of 2 processes (parity coverage)
+    env = dict(os.environ, BF_TEST_K=str(k), BF_TIMEOUT_MS="8000", BF_HIER=hier, BF_NVLS_MIN_P="2")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mp_worker.py")]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)

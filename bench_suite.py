@@ -185,6 +185,7 @@ def main():
             nvls = False
             if world > 1 and L > k and L % k == 0 and os.environ.get("BF_NVLS", "1") != "0":
                 nvls = ctx.enable_nvls(L, count)     # machines span GPUs: average in the switch
+                nvls = nvls and L // k >= int(os.environ.get("BF_NVLS_MIN_P", "4"))   # the library's threshold
             ms = timed(lambda: ctx.hierarchical_neighbor_allreduce(x, out=y), 20)
             dm = 1 if nm == 2 else (2 if nm in (3, 4) else 3)
             if world > 1 and not hier_fused:
@@ -208,7 +209,7 @@ def main():
             ctx.set_machine_topology(bfp.topology_matrix("exp2", nm), L)
             nvls = False
             if world > 1 and L > k and L % k == 0 and os.environ.get("BF_NVLS", "1") != "0":
-                nvls = ctx.enable_nvls(L, count)
+                nvls = ctx.enable_nvls(L, count) and L // k >= int(os.environ.get("BF_NVLS_MIN_P", "4"))
             for style, fn in (("H-ATC", ctx.hierarchical_atc_step), ("H-AWC", ctx.hierarchical_awc_step)):
                 ms = timed(lambda: fn(x, g, 1e-3), 20)
                 dm = 1 if nm == 2 else (2 if nm in (3, 4) else 3)

@@ -331,7 +331,7 @@ def main():
     # per-round detail (diagnostic, after the timed region): one-peer rotates through
     # tau = ceil(log2 n) graphs; each step bracketed by its own events
     tau_r = max(1, (ctx.n - 1).bit_length()) if a.topology == "one_peer" else 1
-    n_diag = max(tau_r * 3, 3)
+    n_diag = max(tau_r * 3, min(a.steps, 48) // tau_r * tau_r, 3)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(n_diag)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(n_diag)]
     for s in range(n_diag):
@@ -340,6 +340,8 @@ def main():
         ends[s].record(stream)
     barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    srt = sorted(step_ms)
+    step_stats = [statistics.median(step_ms), srt[0], srt[min(len(srt) - 1, int(0.9 * len(srt)))]]
     r_diag0 = a.warmup + a.steps
     by_round = [statistics.mean(step_ms[i] for i in range(n_diag) if (r_diag0 + i) % tau_r == r)
                 for r in range(tau_r)]
@@ -391,13 +393,14 @@ def main():
     ctx.poll_error()
 
     # ---- max over ranks ----
-    vals = torch.tensor([total_ms / a.steps, kern_ms, e2e["ms"] if e2e else 0.0, nar["ms"] if nar else 0.0] + by_round,
-                        dtype=torch.float64, device="cuda")
+    vals = torch.tensor([total_ms / a.steps, kern_ms, e2e["ms"] if e2e else 0.0, nar["ms"] if nar else 0.0]
+                        + step_stats + by_round, dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     vals = [float(v) for v in vals.cpu()]
     ms_step, ms_kern, ms_e2e, ms_nar = vals[:4]
-    ms_by_round = vals[4:]
+    ms_med, ms_min, ms_p90 = vals[4:7]
+    ms_by_round = vals[7:]
 
     if rank == 0:
         d = degree(a.topology, n)
@@ -456,6 +459,7 @@ def main():
                              "frac": roof_by_round.get(r, 0.0) * 1e3 / m if m > 0 else None}
                             for r, m in enumerate(ms_by_round)]
         roof["by_round_note"] = "per-round times from separate event-bracketed steps after the timed region"
+        roof["step_ms_event_bracketed"] = {"median": ms_med, "min": ms_min, "p90": ms_p90, "steps": n_diag}
         # every schedule round of the timed steps is one roofline class: one-peer with
         # tau graphs needs steps >= tau for every class to be present
         roof["traffic"] = None

@@ -190,6 +190,34 @@ def main():
         torch.cuda.synchronize()
         check("gt y", np_(y), ora.gt_y(Wg, Y, Gn, Gp), Wg, np.abs(Y) + np.abs(Gn) + np.abs(Gp), 1e-6)
 
+    # ---- C2 across GPUs: ATC-DSGD on least squares reaches the oracle's fixed point ----
+    # (Eq. 12-13, Eq. 17) -- hundreds of consecutive small
+    # exchanges (the tagged-word path), gradients of the local agents by torch bmm
+    if fused:
+        m2, d2 = 40, 24
+        rs = np.random.default_rng(77)
+        A2 = rs.standard_normal((n, m2, d2)) / np.sqrt(m2)
+        b2 = np.einsum("imd,d->im", A2, rs.standard_normal(d2)) + 0.01 * rs.standard_normal((n, m2))
+        W2 = ora.exp2(n)
+        lam = max(np.linalg.eigvalsh(A2[i].T @ A2[i]).max() for i in range(n))
+        lr2 = float(np.float32(1.0 / lam))
+        xinf, _ = ora.atc_fixed_point(W2, A2, b2, lr2)
+        H = np.zeros((n * d2, n * d2))
+        for i in range(n):
+            H[i * d2:(i + 1) * d2, i * d2:(i + 1) * d2] = A2[i].T @ A2[i]
+        rho = np.abs(np.linalg.eigvals(np.kron(W2, np.eye(d2)) @ (np.eye(n * d2) - lr2 * H))).max()
+        ctx.set_topology(W2)
+        At2 = torch.from_numpy(A2[rows].copy()).cuda()
+        bt2 = torch.from_numpy(b2[rows].copy()).cuda()
+        xc = torch.zeros(k, d2, device="cuda")
+        for _ in range(int(40 / (1 - rho)) + 200):
+            gr = torch.bmm(At2.transpose(1, 2), (torch.bmm(At2, xc.double().unsqueeze(2)).squeeze(2) - bt2).unsqueeze(2))
+            ctx.atc_step(xc, gr.squeeze(2).float().contiguous(), lr2)
+        torch.cuda.synchronize()
+        err = np.abs(np_(xc) - xinf[rows]).max() / np.abs(xinf).max()
+        if err > 64 * 2.0 ** -24 / (1 - rho):
+            failures.append(f"C2 fixed point: {err:.3e} (rho {rho:.3f})")
+
     # ---- hierarchical -------------------------------------------------------------
     for L in sorted({1, 2, n}):
         if n % L or n // L < 1:

@@ -81,6 +81,9 @@ struct FusedVec {
 // 96 KB ring changed nothing for exp-2 and slowed one-peer at N = 2 by 4%)
 constexpr int kRingBytes = BF_RING_KB * 1024;
 constexpr int kMaxSlot = 64;
+#ifndef BF_REVERSE
+#define BF_REVERSE 1
+#endif
 #ifndef BF_LEAD
 #define BF_LEAD 24
 #endif
@@ -210,7 +213,14 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
         return at<WT>(g.peer_base[agent / K],
                       p.slot_off + (agent % K) * p.slot_agent_stride + parity * p.slot_parity_stride);
     };
-    auto sub = [&](int m) { return static_cast<int>(blockIdx.x) + m * G; };
+    // One process (HBM-bound): odd epochs walk the sub-items backwards, so a step starts
+    // on the lines the previous step wrote last -- still in the 126 MB L2 -- instead of
+    // the ones it wrote first (BF_REVERSE=0 at build time keeps the forward walk)
+    const bool reverse = BF_REVERSE && g.nprocs == 1 && (e & 1);
+    auto sub = [&](int m) {
+        const int s = static_cast<int>(blockIdx.x) + m * G;
+        return reverse ? S - 1 - s : s;
+    };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (warp == kThreads / 32 + 1) {

@@ -59,6 +59,9 @@ namespace bf {
 // release overtaking an earlier one never moves a word backwards.
 // (measured at N = 2: K = 1 one-peer 0.233 ms with one signal warp, 0.201 with 4,
 // 0.193-0.195 with 8; K = 2 is best with 4 -- 8 more warps cost it registers)
+#ifndef BF_PUSH_REVERSE
+#define BF_PUSH_REVERSE 1
+#endif
 #ifndef BF_PUSH_PREFETCH
 #define BF_PUSH_PREFETCH 1   // K >= 4: issue sub-item m's x / g loads before the combine of sub-item m - kLag
 #endif
@@ -200,7 +203,14 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
     const int nmine = static_cast<int>(blockIdx.x) < S ? (S - static_cast<int>(blockIdx.x) + G - 1) / G : 0;
     const int nrt = lm.rbeg[K];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    auto sub = [&](int m) { return static_cast<int>(blockIdx.x) + m * G; };
+    // odd epochs walk the sub-items backwards on every process (the pairing of CTA b with
+    // the peers' CTA b is unchanged): a step starts on the lines the previous one left in L2
+    // (measured at N = 4: K = 2 exp-2 0.680 -> 0.660 ms; K = 1 one-peer 0.187 -> 0.191 ms, so K >= 2)
+    const bool reverse = BF_PUSH_REVERSE && K >= 2 && (e & 1);
+    auto sub = [&](int m) {
+        const int s = static_cast<int>(blockIdx.x) + m * G;
+        return reverse ? S - 1 - s : s;
+    };
     // inbox of source agent j in process q's heap, this epoch's parity
     auto inbox = [&](int q, int j) {
         return at<WT>(g.peer_base[q], p.inbox_off + static_cast<unsigned long long>(j) * p.inbox_agent_stride +

@@ -84,6 +84,9 @@ constexpr int kMaxSlot = 64;
 #ifndef BF_REVERSE
 #define BF_REVERSE 1
 #endif
+#ifndef BF_REVERSE_X
+#define BF_REVERSE_X 0   // also across processes (the pull path; every process flips with the epoch)
+#endif
 #ifndef BF_LEAD
 #define BF_LEAD 24
 #endif
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     // One process (HBM-bound): odd epochs walk the sub-items backwards, so a step starts
     // on the lines the previous step wrote last -- still in the 126 MB L2 -- instead of
     // the ones it wrote first (BF_REVERSE=0 at build time keeps the forward walk)
-    const bool reverse = BF_REVERSE && g.nprocs == 1 && (e & 1);
+    const bool reverse = BF_REVERSE && (g.nprocs == 1 || BF_REVERSE_X) && (e & 1);
     auto sub = [&](int m) {
         const int s = static_cast<int>(blockIdx.x) + m * G;
         return reverse ? S - 1 - s : s;

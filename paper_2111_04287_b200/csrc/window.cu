@@ -92,17 +92,20 @@ __device__ __noinline__ void win_push_decide(const WinParams &p) {
 #ifndef BF_WIN_BYTES
 #define BF_WIN_BYTES 128   // bytes of each stream in flight per thread
 #endif
-template <typename T>
+#ifndef BF_WIN_PUSH_BYTES
+#define BF_WIN_PUSH_BYTES BF_WIN_BYTES   // the push kernel holds one stream (x): tuning variant
+#endif
+template <typename T, int BYTES = BF_WIN_BYTES>
 struct WinVec {
     static constexpr int V = sizeof(T) >= 4 ? 4 : 8;
-    static constexpr int NV = BF_WIN_BYTES / 16 / (sizeof(T) >= 4 ? 1 : 2);   // 32 fp32 values per stream
+    static constexpr int NV = BYTES / 16 / (sizeof(T) >= 4 ? 1 : 2);   // 32 fp32 values per stream
     static constexpr int TILE = NV * kThreads * V;
 };
 template <int V>
 __device__ __forceinline__ int win_elem(int j) { return (j * kThreads + threadIdx.x) * V; }
-template <typename T>
+template <typename T, int BYTES = BF_WIN_BYTES>
 __host__ __device__ __forceinline__ long long win_items(int k, long long count) {
-    return static_cast<long long>(k) * ((count + WinVec<T>::TILE - 1) / WinVec<T>::TILE);
+    return static_cast<long long>(k) * ((count + WinVec<T, BYTES>::TILE - 1) / WinVec<T, BYTES>::TILE);
 }
 
 // all NV raw vectors of one stream of an item, issued before any use
@@ -157,7 +160,8 @@ __device__ __forceinline__ void win_load_raw(const T *base, typename VecN<T, V>:
 // x_half = x - lr g (Eq. 4) replaces x before the payloads and the self scaling.
 template <typename T, bool SGD>
 __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) {
-    constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV, TILE = WinVec<T>::TILE;
+    constexpr int V = WinVec<T, BF_WIN_PUSH_BYTES>::V, NV = WinVec<T, BF_WIN_PUSH_BYTES>::NV,
+                  TILE = WinVec<T, BF_WIN_PUSH_BYTES>::TILE;
     const Geometry &g = p.geo;
     const unsigned long long me = g.peer_base[g.me];
     Pad *pad = pad_of(g, g.me);
@@ -170,7 +174,7 @@ __global__ void BF_PUSH_LB win_push_kernel(const __grid_constant__ WinParams p) 
     const unsigned long long *dec = at<unsigned long long>(me, p.dec_off);
     const unsigned long long *dlv = at<unsigned long long>(me, p.delivered_off);
     const unsigned int *obv = at<unsigned int>(me, p.obvalid_off);
-    const long long items = win_items<T>(k, count);
+    const long long items = win_items<T, BF_WIN_PUSH_BYTES>(k, count);
     for (long long w = blockIdx.x; w < items; w += gridDim.x) {
         const int t = static_cast<int>(w / k), a = static_cast<int>(w % k);
         if (!active(p, a)) continue;
@@ -538,7 +542,8 @@ static cudaError_t coop2(K kernel, int grid, cudaStream_t s, const WinParams &p,
 }
 
 cudaError_t launch_win_push(const WinParams &p, int grid, cudaStream_t s) {
-    const long long items = p.dtype == 0 ? win_items<float>(p.geo.k, p.geo.count) : win_items<bf16>(p.geo.k, p.geo.count);
+    const long long items = p.dtype == 0 ? win_items<float, BF_WIN_PUSH_BYTES>(p.geo.k, p.geo.count)
+                                         : win_items<bf16, BF_WIN_PUSH_BYTES>(p.geo.k, p.geo.count);
     if (p.g) {
         if (grid <= 0)
             grid = p.dtype == 0 ? occ_grid(win_push_kernel<float, true>, items) : occ_grid(win_push_kernel<bf16, true>, items);

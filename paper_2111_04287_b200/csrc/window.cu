@@ -92,6 +92,9 @@ __device__ __noinline__ void win_push_decide(const WinParams &p) {
 #ifndef BF_WIN_BYTES
 #define BF_WIN_BYTES 128   // bytes of each stream in flight per thread
 #endif
+#ifndef BF_WIN_COLLECT_REVERSE
+#define BF_WIN_COLLECT_REVERSE 1
+#endif
 #ifndef BF_WIN_PUSH_BYTES
 #define BF_WIN_PUSH_BYTES BF_WIN_BYTES   // the push kernel holds one stream (x): tuning variant
 #endif
@@ -125,7 +128,7 @@ __device__ __forceinline__ void win_load_raw(const T *base, typename VecN<T, V>:
 
 // min CTAs per SM for the streaming window kernels (0 = no bound; tuning variants: -DBF_WIN_COLLECT_MINB=6)
 #ifndef BF_WIN_PUSH_MINB
-#define BF_WIN_PUSH_MINB 4   // C5 A/B (profiles/r01_window_minblocks_ab.txt): 7.17 -> 7.09 ms per round
+#define BF_WIN_PUSH_MINB 3   // C5 A/B: r01 (4-element tiles) 4 per SM best; r02 (128 B per stream) 3 per SM 5.73 -> 5.59 ms
 #endif
 #ifndef BF_WIN_COLLECT_MINB
 #define BF_WIN_COLLECT_MINB 3    // 3 CTAs/SM (80 registers); -1: 4 for bf16, 3 for fp32
@@ -342,7 +345,10 @@ __global__ void BF_COLLECT_LB win_collect_kernel(const __grid_constant__ WinPara
     __syncthreads();
     constexpr int V = WinVec<T>::V, NV = WinVec<T>::NV, TILE = WinVec<T>::TILE;
     const long long items = win_items<T>(k, count);
-    for (long long w = blockIdx.x; w < items; w += gridDim.x) {
+    // the collect walks the items backwards: it starts on the x / slot lines the push
+    // kernel wrote last (still in L2), and the next push (forwards) on the ones it wrote last
+    for (long long wi = blockIdx.x; wi < items; wi += gridDim.x) {
+        const long long w = BF_WIN_COLLECT_REVERSE ? items - 1 - wi : wi;
         const int t = static_cast<int>(w / k), b = static_cast<int>(w % k);
         if (!active(p, b)) continue;
         const long long base = static_cast<long long>(t) * TILE, rem = count - base;

@@ -421,3 +421,25 @@ def test_window_gpu_equals_paper_semantics_without_backlog():
     assert np.allclose(ctx.win_p("pw"), ref[:, -1], rtol=0, atol=1e-12)
     ctx.win_free("pw")
     ctx.close()
+
+
+def test_win_version_matches_counters():
+    # SURVEY 8(b) bf_win_version: payloads delivered from src_rank to the first local agent
+    # that has it as an in-neighbour (= bf_win_counters' version for that pair)
+    n = 4
+    W = ora.ring(n)
+    ctx = _ctx(n)
+    ctx.set_topology(W)
+    x = _gpu(synthetic.agents_x0(n, 1001))
+    ctx.win_create(x, "v", zero_init=True)
+    for _ in range(2):
+        ctx.win_put("v")
+        ctx.win_update_then_collect("v")
+    torch.cuda.synchronize()
+    for src in range(n):
+        first = min(i for i in range(n) if src in ora.in_neighbors(W, i))
+        assert ctx.win_version("v", src) == ctx.win_counters("v", first, src)[0] == 2
+    with pytest.raises(BluefogError):
+        ctx.win_version("v", 99)   # no local agent receives from it
+    ctx.win_free("v")
+    ctx.close()

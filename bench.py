@@ -468,8 +468,10 @@ def main():
             try:
                 with open(tp) as f:
                     tj = json.load(f)
+                # ncu DRAM bytes per launch: N = 1 from a --set full capture, N > 1 from the
+                # one-rank capture of scripts/ncu_nvlink.py (profiles/r02_ncu_multirank_n2.md)
                 key = f"{a.topology}_{a.wire}_n{world}"
-                roof["traffic"] = tj.get(key)
+                roof["traffic"] = tj.get(f"{key}_a{n}", tj.get(key))
             except Exception:
                 pass
         roof["algorithmic_bytes_per_launch"] = hbm_bytes if roof["bound"] == "hbm" else nvl_bytes

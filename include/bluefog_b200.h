@@ -39,9 +39,9 @@
  * arguments on every process).  Window data calls (put / accumulate / update /
  * collect / get) are one-sided and need no matching call.
  *
- * Transfer across GPUs (internal, chosen per call): messages up to 32768
- * elements per agent travel as epoch-tagged 64-bit words (no fence on the data
- * path); larger ones are pushed into the readers' inboxes (static topologies and
+ * Transfer across GPUs (internal, chosen per call): messages up to 262144
+ * elements per agent (BF_LL_CAP; 32768 when the heap has no room for that
+ * region) travel as epoch-tagged 64-bit words (no fence on the data path); larger ones are pushed into the readers' inboxes (static topologies and
  * schedules) or pulled by the readers (per-call pull-only views).  BF_XFER=pull
  * and BF_LL=0 (read at bf_init) force the pull path / turn the tagged words off.
  */

@@ -87,23 +87,30 @@ struct PushCfg {
     static constexpr int kSmem = kLag * kPerSub;
     static constexpr int kSig = BF_PUSH_NSIG > 0 ? BF_PUSH_NSIG : (K == 1 ? 8 : (K >= 4 && kMinB == 2 ? 2 : 4));
     static constexpr int kThreadsPerCta = kThreads + 32 * (1 + kSig);   // consumers + poll + signal warps
+    // sub-items per progress release.  Deadlock freedom: the combine of sub-item m - kLag
+    // runs before sub-item m is pushed, and needs the peer's batch holding m - kLag released,
+    // i.e. pushed up to its end -- so a batch may not span more than kLag sub-items
+    // (bf16 at K = 4: kLag = 3 -> batches of 3)
+    static constexpr int kBatch = BF_PUSH_BATCH < kLag ? BF_PUSH_BATCH : kLag;
     static_assert(kPubRing % kSig == 0, "a publish-barrier slot must always map to the same signal warp");
+    static_assert(kBatch >= 1 && kBatch <= kLag, "a batch must fit in the lag");
 };
-constexpr int kPushBatch = BF_PUSH_BATCH;
 #ifndef BF_PUSH_FIRST
 #define BF_PUSH_FIRST 0   // 1: the first batch is a single sub-item (an early first release)
 #endif
-// batches: with BF_PUSH_FIRST, batch 0 = sub-item 0, batch b >= 1 = sub-items 1 + (b-1)B .. bB;
-// else batch b = sub-items bB .. (b+1)B - 1
+// batches of B sub-items: with BF_PUSH_FIRST, batch 0 = sub-item 0, batch b >= 1 = sub-items
+// 1 + (b-1)B .. bB; else batch b = sub-items bB .. (b+1)B - 1
+template <int B>
 __device__ __forceinline__ int push_nbatch(int nmine) {
-    return BF_PUSH_FIRST ? (nmine > 0 ? 1 + (nmine - 1 + kPushBatch - 1) / kPushBatch : 0)
-                         : (nmine + kPushBatch - 1) / kPushBatch;
+    return BF_PUSH_FIRST ? (nmine > 0 ? 1 + (nmine - 1 + B - 1) / B : 0) : (nmine + B - 1) / B;
 }
+template <int B>
 __device__ __forceinline__ int push_batch_end(int b, int nmine) {   // sub-items covered by batches 0..b
-    return min(BF_PUSH_FIRST ? 1 + b * kPushBatch : (b + 1) * kPushBatch, nmine);
+    return min(BF_PUSH_FIRST ? 1 + b * B : (b + 1) * B, nmine);
 }
+template <int B>
 __device__ __forceinline__ int push_batch_of(int m) {
-    return BF_PUSH_FIRST ? (m == 0 ? 0 : 1 + (m - 1) / kPushBatch) : m / kPushBatch;
+    return BF_PUSH_FIRST ? (m == 0 ? 0 : 1 + (m - 1) / B) : m / B;
 }
 
 __device__ __forceinline__ void red_max_sys(unsigned long long *p, unsigned long long v) {
@@ -139,6 +146,7 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
     constexpr int kSubT = kThreads * V;
     constexpr int L = PushCfg<K, V>::kLag;
     constexpr int kPushSig = PushCfg<K, V>::kSig;
+    constexpr int B = PushCfg<K, V>::kBatch;
     extern __shared__ __align__(16) float lag[];   // [L][K][kThreads][V]: partial combines, thread-private
     __shared__ SharedTab st;
     __shared__ PushMix<K> lm;
@@ -239,13 +247,13 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
     if (warp >= kThreads / 32 + 1) {
         // ============ signal warps (lane 0): system-scope releases, batch rb -> warp rb mod NSIG ============
         const int sw = warp - (kThreads / 32 + 1);
-        const int nbatch = lm.procs_out_all ? push_nbatch(nmine) : 0;
+        const int nbatch = lm.procs_out_all ? push_nbatch<B>(nmine) : 0;
         if (lane == 0) {
             volatile int *rel = s_rel;
             for (int rb = sw; rb < nbatch; rb += kPushSig) {
                 if (!mbar_wait_acq_b(g, &pubbar[rb % kPubRing], static_cast<unsigned>(rb / kPubRing) & 1u, fail)) break;
                 rel[rb % kPubRing] = rb;   // the barrier slot may take its next phase
-                const int done = push_batch_end(rb, nmine);
+                const int done = push_batch_end<B>(rb, nmine);
                 BF_STAT(const unsigned long long tf = globaltimer();)
                 fence_acq_rel(true);   // the consumers' remote inbox stores, visible system-wide ...
                 BF_STAT(if (stat) { atomicAdd(stat + 4, globaltimer() - tf); atomicAdd(stat + 5, 1ull); })
@@ -526,8 +534,8 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
                         for (int i = 0; i < V; ++i) lp[i] = fmaf(-p.lr, gv[a][i], lp[i]);
                     }
                 }
-                if (lm.procs_out_all && (push_batch_end(push_batch_of(m), nmine) == m + 1)) {
-                    const int b = push_batch_of(m);
+                if (lm.procs_out_all && (push_batch_end<B>(push_batch_of<B>(m), nmine) == m + 1)) {
+                    const int b = push_batch_of<B>(m);
                     if (b >= kPubRing) {   // the slot's previous phase must have been consumed by its signal warp
                         volatile int *rel = s_rel;
                         while (rel[b % kPubRing] < b - kPubRing && !*fail) __nanosleep(64);

@@ -26,7 +26,7 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     k = int(os.environ.get("BF_TEST_K", "1"))
-    ctx = bfp.Context(agents_per_proc=k, heap_bytes=1 << 28, device=local)
+    ctx = bfp.Context(agents_per_proc=k, heap_bytes=1 << 29, device=local)
     n, r0 = ctx.n, ctx.rank
     rows = slice(r0, r0 + k)
     failures = []
@@ -76,6 +76,23 @@ def main():
         torch.cuda.synchronize()
         check(f"threshold atc bf16 wire {count}", np_(x), ora.atc(We, X, G.astype(np.float64), 0.1, wire_bf16=True),
               We, X, 1e-2, np.abs(We) @ (0.1 * np.abs(G.astype(np.float64))))
+
+    # ---- the push path with several progress batches per CTA (> 4 sub-items per CTA
+    # at every K; bf16 at K = 4 has a lag of 3 sub-items, so its batches are shorter) ----
+    for count, dtype, tol in ((1_300_001, torch.float32, 1e-6), (2_600_003, torch.bfloat16, 1e-2)):
+        x, X = inputs(count, dtype, seed_off=13)
+        for topo in ("exp2", "one_peer"):
+            if topo == "exp2":
+                ctx.set_topology(We)
+                Wr = We
+            else:
+                ctx.set_dynamic_schedule("one_peer_exp2", 0)
+                Wr = ora.one_peer_exp2(n, 0)
+            y = ctx.neighbor_allreduce(x)
+            torch.cuda.synchronize()
+            ctx.set_dynamic_schedule("none")
+            check(f"multi-batch nar {topo} {dtype} {count}", np_(y), ora.mix(Wr, X), Wr, X, tol)
+        del x, y
 
     # ---- dynamic push / pull / push-pull ------------------------------------
     rng = np.random.default_rng(11)

@@ -228,8 +228,9 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // odd epochs walk the sub-items backwards on every process (the pairing of CTA b with
     // the peers' CTA b is unchanged): a step starts on the lines the previous one left in L2
-    // (measured at N = 4: K = 2 exp-2 0.680 -> 0.660 ms; K = 1 one-peer 0.187 -> 0.191 ms, so K >= 2)
-    const bool reverse = BF_PUSH_REVERSE && K >= 2 && (e & 1);
+    // (measured at N = 4: K = 2 exp-2 0.680 -> 0.660 ms; K = 1 one-peer 0.187 -> 0.191 ms; at N = 2
+    // K = 4 it costs: exp-2 0.71 -> 0.80 ms, profiles/r02_push_k4_knobs_n2.txt -- so K = 2 only)
+    const bool reverse = BF_PUSH_REVERSE && K == 2 && (e & 1);
     auto sub = [&](int m) {
         const int s = static_cast<int>(blockIdx.x) + m * G;
         return reverse ? S - 1 - s : s;
@@ -255,7 +256,9 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
                 rel[rb % kPubRing] = rb;   // the barrier slot may take its next phase
                 const int done = push_batch_end<B>(rb, nmine);
                 BF_STAT(const unsigned long long tf = globaltimer();)
+#ifndef BF_PUSH_NOFENCE   // diagnostic builds only (timing of the protocol without its fence; results may be stale)
                 fence_acq_rel(true);   // the consumers' remote inbox stores, visible system-wide ...
+#endif
                 BF_STAT(if (stat) { atomicAdd(stat + 4, globaltimer() - tf); atomicAdd(stat + 5, 1ull); })
                 for (int q = 0; q < g.nprocs; ++q)   // ... before the progress word in every reader's heap
                     if ((lm.procs_out_all >> q) & 1u)
@@ -503,7 +506,11 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
                     const unsigned out = lm.procs_out[a];
                     if (!out) continue;
                     for (int q = 0; q < g.nprocs; ++q)
+#ifndef BF_PUSH_LOCALSTORE
                         if ((out >> q) & 1u) VecN<WT, V>::store(inbox(q, g.me * K + a) + base + e0, xv[a], valid, true);
+#else   // diagnostic builds only: the wire copy lands in the writer's own heap (timing of the remote stores)
+                        if ((out >> q) & 1u) VecN<WT, V>::store(inbox(g.me, g.me * K + a) + base + e0, xv[a], valid, true);
+#endif
                 }
                 // local part of every combine: self, then same-process sources ((a - b) mod K)
 #pragma unroll

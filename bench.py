@@ -270,9 +270,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BF_BENCH_SHARE_GPUS=G (diagnostic, never a bench number): rank r on GPU r mod G with a
+    # gloo bootstrap -- runs the N-process flow (e.g. N = 8) on a box with fewer GPUs
+    share = int(os.environ.get("BF_BENCH_SHARE_GPUS", "0"))
+    if share:
+        local = local % share
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if a.agents % world:
         raise SystemExit(f"{a.agents} agents do not split over {world} GPUs")
     k = a.agents // world
@@ -494,6 +502,8 @@ def main():
                              f"{3 * n * count * 4 / 1e9:.2f} GB)"},
             "gpu_launches": launches,
             "roofline": roof,
+            **({"diagnostic": f"BF_BENCH_SHARE_GPUS={share}: {world} processes time-share {share} GPUs; "
+                              "not a measurement"} if share else {}),
             "clocks": clk,
         }
         if e2e:

@@ -21,6 +21,13 @@ METRICS = {   # two small sets, each meant to fit one pass
     "nvl": "gpu__time_duration.sum,nvlrx__bytes.sum,nvltx__bytes.sum,"
            "nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum",
     "dram": "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum",
+    # warp stall counters (why the consumers of the cross-GPU kernels are slower than local streaming)
+    "stall1": "gpu__time_duration.sum,smsp__warps_active.sum,smsp__warps_issue_stalled_long_scoreboard.sum,"
+              "smsp__warps_issue_stalled_lg_throttle.sum,smsp__warps_issue_stalled_membar.sum,"
+              "smsp__warps_issue_stalled_sleeping.sum",
+    "stall2": "gpu__time_duration.sum,smsp__warps_issue_stalled_barrier.sum,smsp__warps_issue_stalled_drain.sum,"
+              "smsp__warps_issue_stalled_short_scoreboard.sum,smsp__warps_issue_stalled_mio_throttle.sum,"
+              "smsp__warps_issue_stalled_wait.sum,smsp__warps_issue_stalled_selected.sum",
 }
 HERE = os.path.dirname(os.path.abspath(__file__))
 

@@ -23,10 +23,17 @@ from paper_2111_04287_b200 import BluefogError  # noqa: E402
 def main():
     local = int(os.environ["LOCAL_RANK"])
     rank = int(os.environ["RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # BF_TEST_SHARE_GPUS=G: more processes than GPUs (process p on GPU p mod G, gloo bootstrap,
+    # time-sliced contexts) -- the 8-process logic of the 8-GPU setting on a smaller box
+    share = int(os.environ.get("BF_TEST_SHARE_GPUS", "0"))
+    dev = local % share if share else local
+    torch.cuda.set_device(dev)
+    if share:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     k = int(os.environ.get("BF_TEST_K", "1"))
-    ctx = bfp.Context(agents_per_proc=k, heap_bytes=1 << 29, device=local)
+    ctx = bfp.Context(agents_per_proc=k, heap_bytes=1 << 29, device=dev)
     n, r0 = ctx.n, ctx.rank
     rows = slice(r0, r0 + k)
     failures = []
@@ -264,7 +271,7 @@ def main():
               0.1 * np.abs(Gh.astype(np.float64)))
 
     # ---- NVLS: machines spanning 2 processes, average in the switch (hier_nvls.cu) ----
-    if ctx.nprocs % 2 == 0:
+    if ctx.nprocs % 2 == 0 and not share:   # multicast objects need one process per GPU
         L = 2 * k
         nm = n // L
         WM = ora.exp2(nm) if nm > 1 else np.ones((1, 1))

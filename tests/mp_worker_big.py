@@ -29,8 +29,15 @@ import paper_2111_04287_b200 as bfp  # noqa: E402
 def main():
     local = int(os.environ["LOCAL_RANK"])
     rank = int(os.environ["RANK"])
+    # BF_TEST_SHARE_GPUS=G: more processes than GPUs (process p on GPU p mod G, gloo bootstrap)
+    share = int(os.environ.get("BF_TEST_SHARE_GPUS", "0"))
+    if share:
+        local = local % share
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if share:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     k = int(os.environ.get("BF_TEST_K", "1"))
     count = int(os.environ.get("BF_TEST_COUNT", str(25_600_000)))
     ctx = bfp.Context(agents_per_proc=k, heap_bytes=3 << 30, device=local)
@@ -48,6 +55,8 @@ def main():
     def gather(t):
         """(n, ncols) fp64: the sampled columns of every agent (all ranks)."""
         mine = t[:, ct].float().contiguous()
+        if share:   # gloo: gather on the host
+            mine = mine.cpu()
         out = [torch.empty_like(mine) for _ in range(dist.get_world_size())]
         dist.all_gather(out, mine)
         return torch.cat(out).cpu().numpy().astype(np.float64)
@@ -190,6 +199,8 @@ def main():
 
 def _gather_cols(t, cw):
     mine = t[:, cw].float().contiguous()
+    if dist.get_backend() == "gloo":   # BF_TEST_SHARE_GPUS: gather on the host
+        mine = mine.cpu()
     out = [torch.empty_like(mine) for _ in range(dist.get_world_size())]
     dist.all_gather(out, mine)
     return torch.cat(out).cpu().numpy().astype(np.float64)

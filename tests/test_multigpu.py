@@ -46,3 +46,33 @@ def test_multiprocess_production_shape(nproc, k):
     out = res.stdout + res.stderr
     assert res.returncode == 0, out[-4000:]
     assert out.count("ALL OK") == nproc, out[-4000:]
+
+
+def test_eight_processes_time_shared():
+    # the 8-GPU setting's process logic (8 processes, one agent each: push inboxes of 8
+    # writers, one-peer over 8 agents, tagged words, windows, hierarchical) on the GPUs this
+    # box has -- process p on GPU p mod G, time-sliced contexts, gloo bootstrap
+    g = _ngpus()
+    if g < 1:
+        pytest.skip("needs a GPU")
+    env = dict(os.environ, BF_TEST_K="1", BF_TIMEOUT_MS="20000", BF_TEST_SHARE_GPUS=str(min(g, 8)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr=127.0.0.1", "--master-port=29535", os.path.join(ROOT, "tests", "mp_worker.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert out.count("ALL OK") == 8, out[-4000:]
+
+
+def test_eight_processes_time_shared_production_shape():
+    # the same at 25.6M fp32 per agent (the 8-GPU target's per-GPU shape): mp_worker_big.py
+    g = _ngpus()
+    if g < 1:
+        pytest.skip("needs a GPU")
+    env = dict(os.environ, BF_TEST_K="1", BF_TIMEOUT_MS="30000", BF_TEST_SHARE_GPUS=str(min(g, 8)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr=127.0.0.1", "--master-port=29536", os.path.join(ROOT, "tests", "mp_worker_big.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert out.count("ALL OK") == 8, out[-4000:]

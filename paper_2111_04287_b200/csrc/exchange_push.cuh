@@ -65,6 +65,9 @@ namespace bf {
 #ifndef BF_PUSH_PREFETCH
 #define BF_PUSH_PREFETCH 1   // K >= 4: issue sub-item m's x / g loads before the combine of sub-item m - kLag
 #endif
+#ifndef BF_PUSH_PREFETCH_MINK
+#define BF_PUSH_PREFETCH_MINK 4   // smallest K with the prefetch
+#endif
 #ifndef BF_PUSH_K4_MINB
 #define BF_PUSH_K4_MINB 2   // CTAs per SM of the K = 4 push kernel (1: 192 KB lag, 4 signal warps;
                             // measured N = 2 exp-2: 2 per SM 0.72 ms, 1 per SM 0.78 ms)
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
         // non-hierarchical modes: the x / g loads of sub-item m are issued before the
         // combine of sub-item m - L, so their HBM latency overlaps the inbox reads
         // (measured at N = 2: K = 4 exp-2 0.715 -> 0.704 ms; K = 1 one-peer 0.183 -> 0.195 ms, so K >= 4 only)
-        constexpr bool PREFETCH = !HIER && BF_PUSH_PREFETCH && K >= 4;
+        constexpr bool PREFETCH = !HIER && BF_PUSH_PREFETCH && K >= BF_PUSH_PREFETCH_MINK;
         for (int m = 0; m < nmine + L; ++m, slot = slot + 1 == L ? 0 : slot + 1) {
             const int mc = m - L;
             typename VecN<XT, V>::Raw xraw[PREFETCH ? K : 1];

@@ -218,8 +218,11 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
     };
     // One process (HBM-bound): odd epochs walk the sub-items backwards, so a step starts
     // on the lines the previous step wrote last -- still in the 126 MB L2 -- instead of
-    // the ones it wrote first (BF_REVERSE=0 at build time keeps the forward walk)
-    const bool reverse = BF_REVERSE && (g.nprocs == 1 || BF_REVERSE_X) && (e & 1);
+    // the ones it wrote first (BF_REVERSE=0 at build time keeps the forward walk).  Only the
+    // in-place updates (ATC, AWC, ED, GT): neighbor_allreduce writes y, not the x the next call
+    // reads, and walked backwards it measured slower (hierarchical 4x2 0.271 -> 0.283 ms;
+    // ATC 0.410 -> 0.398 ms with it, profiles/r02c_fused_reverse_ab_n1.txt)
+    const bool reverse = BF_REVERSE && MODE != 0 && (g.nprocs == 1 || BF_REVERSE_X) && (e & 1);
     auto sub = [&](int m) {
         const int s = static_cast<int>(blockIdx.x) + m * G;
         return reverse ? S - 1 - s : s;

@@ -88,6 +88,15 @@ def main():
 
     only = set(a.only.split(","))
 
+    def fresh():
+        # every config starts from fresh allocations: carving its buffers out of the
+        # previous config's freed blocks measurably changed the HBM-bound lines (e.g. the
+        # Exact-Diffusion step after C5 0.684 -> 0.786 ms at N = 1, profiles/r02c_suite_order_n1.txt)
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
     def xheap(k, n, bytes_per_agent, extra):
         # exchange slots (k agents x 2 parities) + across GPUs the push inboxes (n x 2)
         # and the tagged-word inboxes (n x 2 x BF_LL_CAP x 8 B)
@@ -130,6 +139,8 @@ def main():
 
     # ---------------------------------------------------------------- C3 ----
     if "c3" in only:
+        x = g = y = psi = u = gp = xo = None   # the previous config's buffers
+        fresh()
         n = a.agents
         k = n // world
         maxb = a.max_bytes
@@ -168,6 +179,8 @@ def main():
 
     # ----------------------------------------------------------------- H ----
     if "h" in only:
+        x = g = y = psi = u = gp = xo = None   # the previous config's buffers
+        fresh()
         hier_env = os.environ.get("BF_HIER", "")
         hier_fused = (world == 1 and hier_env != "staged") or hier_env == "fused"
         n = a.agents
@@ -226,6 +239,8 @@ def main():
 
     # ------------------------------------------- inner-outer exp-2 schedule ----
     if "io" in only:
+        x = g = y = psi = u = gp = xo = None   # the previous config's buffers
+        fresh()
         n = a.agents
         k = n // world
         count = 25_600_000
@@ -248,6 +263,8 @@ def main():
 
     # ---------------------------------------------------------------- C5 ----
     if "c5" in only:
+        x = g = y = psi = u = gp = xo = None   # the previous config's buffers
+        fresh()
         n = a.agents
         k = n // world
         count = 340_000_000
@@ -302,6 +319,8 @@ def main():
     # ----------------------------------------------------------------- E ----
     # Exact-Diffusion step (appendix ed-1..ed-3) fused like ATC, C4-sized vectors
     if "e" in only:
+        x = g = y = psi = u = gp = xo = None   # the previous config's buffers
+        fresh()
         n = a.agents
         k = n // world
         count = 25_600_000
@@ -325,6 +344,8 @@ def main():
     # push-sum gradient tracking round (appendix): the two fused
     # launches (gt_uv_step, gt_y_step) over C4-sized vectors, static exp-2
     if "gt" in only:
+        x = g = y = psi = u = gp = xo = None   # the previous config's buffers
+        fresh()
         n = a.agents
         k = n // world
         count = 25_600_000
@@ -351,6 +372,8 @@ def main():
     # ATC optimizer over ResNet-50's 161 parameter tensors (tensor fusion into
     # buckets, one fused kernel per bucket), synthetic gradients (§8(f) rank 3)
     if "o" in only:
+        x = g = y = psi = u = gp = xo = None   # the previous config's buffers
+        fresh()
         import math
         from paper_2111_04287_b200.optim import DistributedAdaptThenCombineOptimizer, resnet50_param_shapes
         n = a.agents

@@ -233,7 +233,9 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
     // the peers' CTA b is unchanged): a step starts on the lines the previous one left in L2
     // (measured at N = 4: K = 2 exp-2 0.680 -> 0.660 ms; K = 1 one-peer 0.187 -> 0.191 ms; at N = 2
     // K = 4 it costs: exp-2 0.71 -> 0.80 ms, profiles/r02_push_k4_knobs_n2.txt -- so K = 2 only)
-    const bool reverse = BF_PUSH_REVERSE && K == 2 && (e & 1);
+    // ATC only: Exact-Diffusion walked backwards at K = 2 measured 0.81 ms against 0.37 ms
+    // forward (N = 2, profiles/r02c_ed_ab_n2.txt)
+    const bool reverse = BF_PUSH_REVERSE && K == 2 && MODE == 1 && (e & 1);
     auto sub = [&](int m) {
         const int s = static_cast<int>(blockIdx.x) + m * G;
         return reverse ? S - 1 - s : s;
@@ -326,7 +328,9 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
         // non-hierarchical modes: the x / g loads of sub-item m are issued before the
         // combine of sub-item m - L, so their HBM latency overlaps the inbox reads
         // (measured at N = 2: K = 4 exp-2 0.715 -> 0.704 ms; K = 1 one-peer 0.183 -> 0.195 ms, so K >= 4 only)
-        constexpr bool PREFETCH = !HIER && BF_PUSH_PREFETCH && K >= BF_PUSH_PREFETCH_MINK;
+        // (neighbor_allreduce / ATC / AWC only: Exact-Diffusion and the GT steps read a third
+        // stream and were slower with it at K = 4 -- E 0.776 -> 0.96 ms, GT 1.47 -> 1.69 ms, N = 2)
+        constexpr bool PREFETCH = !HIER && MODE <= 2 && BF_PUSH_PREFETCH && K >= BF_PUSH_PREFETCH_MINK;
         for (int m = 0; m < nmine + L; ++m, slot = slot + 1 == L ? 0 : slot + 1) {
             const int mc = m - L;
             typename VecN<XT, V>::Raw xraw[PREFETCH ? K : 1];

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "exchange_common.cuh"
 
@@ -81,6 +82,9 @@ struct FusedVec {
 // 96 KB ring changed nothing for exp-2 and slowed one-peer at N = 2 by 4%)
 constexpr int kRingBytes = BF_RING_KB * 1024;
 constexpr int kMaxSlot = 64;
+#ifndef BF_SLOTX_PUB_STREAM
+#define BF_SLOTX_PUB_STREAM 0   // 1: the publish loads of x / g evict-first when the combine reads the slot back
+#endif
 #ifndef BF_REVERSE
 #define BF_REVERSE 1
 #endif
@@ -320,6 +324,12 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
         const unsigned pub = lm.pub;
         const unsigned long long pol_stream = policy_evict_first();
         const unsigned long long pol_keep = policy_evict_normal();
+        // fp32-wire neighbor_allreduce / ATC: an agent another process reads takes its x_half
+        // in the combine back from its own slot (stored kLead sub-items earlier by this thread,
+        // bit-identical, 4 B and often still in L2) instead of re-reading x and g (8 B)
+        constexpr bool SLOTX = (MODE == 0 || MODE == 1) && std::is_same<XT, float>::value &&
+                               std::is_same<WT, float>::value && FusedCfg<K>::kRing;
+        const unsigned long long pol_pub = BF_SLOTX_PUB_STREAM && SLOTX ? pol_stream : pol_keep;   // x / g of the publish
         auto xrow = [&](int a) { return static_cast<const XT *>(p.x) + static_cast<long long>(a) * count; };
         auto grow = [&](int a) { return static_cast<const GT *>(p.g) + static_cast<long long>(a) * count; };
         unsigned long long *prog = at<unsigned long long>(g.peer_base[g.me], p.prog_off) + blockIdx.x;
@@ -348,10 +358,10 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                 for (int a = 0; a < K; ++a) {
                     if (!((pub >> a) & 1u)) continue;
                     float v[V];
-                    VecN<XT, V>::load_hint(xrow(a) + base + e0, v, valid, vec, pol_keep);
+                    VecN<XT, V>::load_hint(xrow(a) + base + e0, v, valid, vec, pol_pub);
                     if constexpr (MODE == 1 || MODE == 5) {
                         float gv[V];
-                        VecN<GT, V>::load_hint(grow(a) + base + e0, gv, valid, vec, pol_keep);
+                        VecN<GT, V>::load_hint(grow(a) + base + e0, gv, valid, vec, pol_pub);
 #pragma unroll
                         for (int i = 0; i < V; ++i) v[i] = fmaf(-p.lr, gv[i], v[i]);
                     }
@@ -400,10 +410,21 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                     for (int u = 0; u < U; ++u) {
                         const long long base = static_cast<long long>(sub(mc + u)) * kSubT + e0;
 #pragma unroll
-                        for (int a = 0; a < K; ++a) VecN<XT, V>::load_raw_fast(xrow(a) + base, xr[u][a], pol_stream);
+                        for (int a = 0; a < K; ++a) {
+                            const XT *src = xrow(a) + base;
+                            if constexpr (SLOTX)
+                                if ((pub >> a) & 1u) src = reinterpret_cast<const XT *>(slot_of(g.me * K + a)) + base;
+                            VecN<XT, V>::load_raw_fast(src, xr[u][a], pol_stream);
+                        }
                         if constexpr (HAS_G) {
 #pragma unroll
-                            for (int a = 0; a < K; ++a) VecN<GT, V>::load_raw_fast(grow(a) + base, gr[u][a], pol_stream);
+                            for (int a = 0; a < K; ++a) {
+                                if (SLOTX && ((pub >> a) & 1u)) {
+                                    gr[u][a] = typename VecN<GT, V>::Raw{};
+                                    continue;
+                                }
+                                VecN<GT, V>::load_raw_fast(grow(a) + base, gr[u][a], pol_stream);
+                            }
                         }
                         if constexpr (THIRD) {
 #pragma unroll
@@ -419,12 +440,21 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                         const long long base = static_cast<long long>(sub(mc + u)) * kSubT;
                         const int valid = u < nu ? clamp_valid_v<V>(count - base, e0) : 0;
 #pragma unroll
-                        for (int a = 0; a < K; ++a)
-                            VecN<XT, V>::load_raw(xrow(a) + base + e0, xr[u][a], valid, pol_stream);
+                        for (int a = 0; a < K; ++a) {
+                            const XT *src = xrow(a) + base + e0;
+                            if constexpr (SLOTX)
+                                if ((pub >> a) & 1u) src = reinterpret_cast<const XT *>(slot_of(g.me * K + a)) + base + e0;
+                            VecN<XT, V>::load_raw(src, xr[u][a], valid, pol_stream);
+                        }
                         if constexpr (HAS_G) {
 #pragma unroll
-                            for (int a = 0; a < K; ++a)
+                            for (int a = 0; a < K; ++a) {
+                                if (SLOTX && ((pub >> a) & 1u)) {
+                                    gr[u][a] = typename VecN<GT, V>::Raw{};
+                                    continue;
+                                }
                                 VecN<GT, V>::load_raw(grow(a) + base + e0, gr[u][a], valid, pol_stream);
+                            }
                         }
                         if constexpr (THIRD) {
 #pragma unroll
@@ -464,9 +494,11 @@ __global__ void __launch_bounds__(FusedCfg<K>::kThreadsPerCta, (K >= 2 ? 2 : 3))
                 const int valid = clamp_valid_v<V>(count - base, e0);
                 if constexpr (MODE == 1 || MODE == 5) {
 #pragma unroll
-                    for (int a = 0; a < K; ++a)
+                    for (int a = 0; a < K; ++a) {
+                        if (SLOTX && ((pub >> a) & 1u)) continue;   // read back adapted from the slot
 #pragma unroll
                         for (int i = 0; i < V; ++i) xv[u][a][i] = fmaf(-p.lr, gv[u][a][i], xv[u][a][i]);   // Eq. 4
+                    }
                 }
                 if constexpr (MODE == 3) {   // store psi^(k) over psi^(k-1) (same elements, same thread)
 #pragma unroll

@@ -144,7 +144,8 @@ def main():
         n = a.agents
         k = n // world
         maxb = a.max_bytes
-        ctx = bfp.Context(agents_per_proc=k, heap_bytes=xheap(k, n, maxb, 256 << 20), device=local)
+        # + room for the registered (bf_alloc) fp32 input of the largest size
+        ctx = bfp.Context(agents_per_proc=k, heap_bytes=xheap(k, n, maxb, k * maxb + (256 << 20)), device=local)
         ctx.reserve(maxb)
         W = bfp.topology_matrix("exp2", n)
         for dtype, es in ((torch.float32, 4), (torch.bfloat16, 2)):
@@ -172,9 +173,35 @@ def main():
                     hbm = (k * 2 + pubs) * nb / (ms * 1e-3) / 1e9
                     emit({"config": "C3 neighbor_allreduce sweep", "bytes_per_agent": nb,
                           "dtype": str(dtype).split(".")[-1], "topology": topo, "agents": n, "agents_per_gpu": k,
+                          "input": "torch tensor (unregistered)",
                           "us": ms * 1e3, "exchange_gbs_per_gpu": gbs, "hbm_gbs": hbm, "hbm_frac": hbm / peak})
                 del x, y
                 nb *= 4
+        # the same call on a registered input (bf_alloc: the tensor lives in the symmetric heap).
+        # Nothing to save here: across GPUs the writer stores its wire copy into the readers'
+        # inboxes straight from registers, and on one GPU nothing is published -- there is no
+        # publish copy that registration could avoid (SURVEY C3 asks for both lines)
+        nb = maxb
+        count = nb // 4
+        x = ctx.alloc((k, count))
+        for la in range(k):
+            bfp.Context.fill_uniform(x[la], synthetic.SEED_X0 + ctx.rank + la)
+        y = torch.empty_like(x)
+        for topo in ("exp2", "one_peer"):
+            if topo == "exp2":
+                ctx.set_topology(W)
+                d = 3 if n == 8 else int(np.count_nonzero(W[0])) - 1
+            else:
+                ctx.set_dynamic_schedule("one_peer_exp2", 0)
+                d = 1
+            ms = timed(lambda: ctx.neighbor_allreduce(x, out=y), 3)
+            ctx.set_dynamic_schedule("none")
+            gbs = k * d * nb / (ms * 1e-3) / 1e9
+            hbm = (k * 2 + (0 if world == 1 else k)) * nb / (ms * 1e-3) / 1e9
+            emit({"config": "C3 neighbor_allreduce sweep", "bytes_per_agent": nb, "dtype": "float32", "topology": topo,
+                  "agents": n, "agents_per_gpu": k, "input": "registered (bf_alloc, symmetric heap)",
+                  "us": ms * 1e3, "exchange_gbs_per_gpu": gbs, "hbm_gbs": hbm, "hbm_frac": hbm / peak})
+        del x, y
         ctx.close()
 
     # ----------------------------------------------------------------- H ----

@@ -398,20 +398,31 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
                                 for (int j = 0; j < V; ++j) acc[j] = fmaf(c, v[u][j], acc[j]);
                             }
                     }
-                    if constexpr (HIER) {   // broadcast to the machine's rows (H-AWC: - lr g per row)
+                    if constexpr (MODE == 8) {   // H-AWC: broadcast to the machine's rows, - lr g per row;
+                        // the g rows are loaded 2 at a time before their first use (4 spill)
+                        for (int l0 = 0; l0 < HL; l0 += 2) {
+                            float gr[2][V];
+#pragma unroll
+                            for (int u = 0; u < 2; ++u)
+                                if (l0 + u < HL)
+                                    VecN<GT, V>::load_hint(static_cast<const GT *>(p.g) +
+                                                               (static_cast<long long>(a) * HL + l0 + u) * count + base + e0,
+                                                           gr[u], valid, vec, pol_stream);
+#pragma unroll
+                            for (int u = 0; u < 2; ++u)
+                                if (l0 + u < HL) {
+                                    const long long row = static_cast<long long>(a) * HL + l0 + u;
+                                    float out[V];
+#pragma unroll
+                                    for (int i = 0; i < V; ++i) out[i] = fmaf(-p.lr, gr[u][i], acc[i]);
+                                    VecN<YT, V>::store_hint(static_cast<YT *>(p.y) + row * count + base + e0, out, valid,
+                                                            vec, pol_stream);
+                                }
+                        }
+                    } else if constexpr (HIER) {   // broadcast to the machine's rows
                         for (int l = 0; l < HL; ++l) {
                             const long long row = static_cast<long long>(a) * HL + l;
-                            float out[V];
-#pragma unroll
-                            for (int i = 0; i < V; ++i) out[i] = acc[i];
-                            if constexpr (MODE == 8) {
-                                float gr[V];
-                                VecN<GT, V>::load_hint(static_cast<const GT *>(p.g) + row * count + base + e0, gr, valid,
-                                                       vec, pol_stream);
-#pragma unroll
-                                for (int i = 0; i < V; ++i) out[i] = fmaf(-p.lr, gr[i], out[i]);
-                            }
-                            VecN<YT, V>::store_hint(static_cast<YT *>(p.y) + row * count + base + e0, out, valid, vec,
+                            VecN<YT, V>::store_hint(static_cast<YT *>(p.y) + row * count + base + e0, acc, valid, vec,
                                                     pol_stream);
                         }
                     } else {

@@ -21,7 +21,8 @@ METRICS = {   # two small sets, each meant to fit one pass
     "nvl": "gpu__time_duration.sum,nvlrx__bytes.sum,nvltx__bytes.sum,"
            "nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum",
     "dram": "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum",
-    # warp stall counters (why the consumers of the cross-GPU kernels are slower than local streaming)
+    # warp stall counters (why the consumers of the cross-GPU kernels are slower than local streaming):
+    # like the NVLink counters they answer UnknownError in the one-rank capture on the gpurun boxes
     "stall1": "gpu__time_duration.sum,smsp__warps_active.sum,smsp__warps_issue_stalled_long_scoreboard.sum,"
               "smsp__warps_issue_stalled_lg_throttle.sum,smsp__warps_issue_stalled_membar.sum,"
               "smsp__warps_issue_stalled_sleeping.sum",

@@ -66,7 +66,7 @@ namespace bf {
 #define BF_PUSH_PREFETCH 1   // K >= 4: issue sub-item m's x / g loads before the combine of sub-item m - kLag
 #endif
 #ifndef BF_PUSH_PREFETCH_MINK
-#define BF_PUSH_PREFETCH_MINK 4   // smallest K with the prefetch
+#define BF_PUSH_PREFETCH_MINK 2   // smallest K with the prefetch (K = 2 one-peer: 0.294 -> 0.286 ms at N = 2; K = 1 slower)
 #endif
 #ifndef BF_PUSH_K4_MINB
 #define BF_PUSH_K4_MINB 2   // CTAs per SM of the K = 4 push kernel (1: 192 KB lag, 4 signal warps;

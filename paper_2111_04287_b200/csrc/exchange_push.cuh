@@ -384,6 +384,19 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
                         const float4 t = *reinterpret_cast<const float4 *>(lp + i);
                         acc[i] = t.x, acc[i + 1] = t.y, acc[i + 2] = t.z, acc[i + 3] = t.w;
                     }
+                    // H-AWC at K >= 2: the first two g rows of the broadcast are loaded before the remote
+                    // tiles (4x2 at N = 2: 0.595 -> 0.557 ms; K = 1, short of registers, got slower)
+                    float g2[MODE == 8 ? 2 : 1][V];
+                    auto load_g2 = [&](int l0) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+                            if (l0 + u < HL)
+                                VecN<GT, V>::load_hint(static_cast<const GT *>(p.g) +
+                                                           (static_cast<long long>(a) * HL + l0 + u) * count + base + e0,
+                                                       g2[u], valid, vec, pol_stream);
+                    };
+                    constexpr bool kG2Early = MODE == 8 && K >= 2;
+                    if constexpr (kG2Early) load_g2(0);
                     const int rb = lm.rbeg[a], re = lm.rbeg[a + 1];
                     for (int i0 = rb; i0 < re; i0 += 4) {   // up to 4 remote tiles in flight
                         float v[4][V];
@@ -399,22 +412,17 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
                             }
                     }
                     if constexpr (MODE == 8) {   // H-AWC: broadcast to the machine's rows, - lr g per row;
-                        // the g rows are loaded 2 at a time before their first use (4 spill)
+                        // the g rows are loaded 2 at a time before their first use (4 spill); rows 0-1
+                        // were issued before the remote tiles
                         for (int l0 = 0; l0 < HL; l0 += 2) {
-                            float gr[2][V];
-#pragma unroll
-                            for (int u = 0; u < 2; ++u)
-                                if (l0 + u < HL)
-                                    VecN<GT, V>::load_hint(static_cast<const GT *>(p.g) +
-                                                               (static_cast<long long>(a) * HL + l0 + u) * count + base + e0,
-                                                           gr[u], valid, vec, pol_stream);
+                            if (l0 > 0 || !kG2Early) load_g2(l0);
 #pragma unroll
                             for (int u = 0; u < 2; ++u)
                                 if (l0 + u < HL) {
                                     const long long row = static_cast<long long>(a) * HL + l0 + u;
                                     float out[V];
 #pragma unroll
-                                    for (int i = 0; i < V; ++i) out[i] = fmaf(-p.lr, gr[u][i], acc[i]);
+                                    for (int i = 0; i < V; ++i) out[i] = fmaf(-p.lr, g2[u][i], acc[i]);
                                     VecN<YT, V>::store_hint(static_cast<YT *>(p.y) + row * count + base + e0, out, valid,
                                                             vec, pol_stream);
                                 }

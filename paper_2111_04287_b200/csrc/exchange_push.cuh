@@ -68,6 +68,9 @@ namespace bf {
 #ifndef BF_PUSH_PREFETCH_MINK
 #define BF_PUSH_PREFETCH_MINK 2   // smallest K with the prefetch (K = 2 one-peer: 0.294 -> 0.286 ms at N = 2; K = 1 slower)
 #endif
+#ifndef BF_PUSH_PREFETCH_GT5
+#define BF_PUSH_PREFETCH_GT5 0   // 1: the prefetch also for the GT u/v-step (two streams, like ATC)
+#endif
 #ifndef BF_PUSH_K4_MINB
 #define BF_PUSH_K4_MINB 2   // CTAs per SM of the K = 4 push kernel (1: 192 KB lag, 4 signal warps;
                             // measured N = 2 exp-2: 2 per SM 0.72 ms, 1 per SM 0.78 ms)
@@ -330,7 +333,8 @@ __global__ void __launch_bounds__(PushCfg<K, FusedVec<XT>::V>::kThreadsPerCta, P
         // (measured at N = 2: K = 4 exp-2 0.715 -> 0.704 ms; K = 1 one-peer 0.183 -> 0.195 ms, so K >= 4 only)
         // (neighbor_allreduce / ATC / AWC only: Exact-Diffusion and the GT steps read a third
         // stream and were slower with it at K = 4 -- E 0.776 -> 0.96 ms, GT 1.47 -> 1.69 ms, N = 2)
-        constexpr bool PREFETCH = !HIER && MODE <= 2 && BF_PUSH_PREFETCH && K >= BF_PUSH_PREFETCH_MINK;
+        constexpr bool PREFETCH = !HIER && (MODE <= 2 || (BF_PUSH_PREFETCH_GT5 && MODE == 5)) && BF_PUSH_PREFETCH &&
+                                  K >= BF_PUSH_PREFETCH_MINK;
         for (int m = 0; m < nmine + L; ++m, slot = slot + 1 == L ? 0 : slot + 1) {
             const int mc = m - L;
             typename VecN<XT, V>::Raw xraw[PREFETCH ? K : 1];
